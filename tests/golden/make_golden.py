@@ -1,0 +1,198 @@
+"""Regenerate the golden fixtures from the REAL reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the reference `specpipe` package from /root/reference (read-only,
+present only in the build container) and records its outputs as JSON so the
+oracle port and the GPU path can be checked against them anywhere, including
+the GPU box where /root/reference does not exist. Nothing at test/bench time
+reads /root/reference.
+
+Fixture files:
+  toylm_decode.json   decode_ppsd / decode_autoregressive (greedy) on ToyLM
+  bernoulli.json      simulate_ppsd (traced machine + untraced fast path)
+  acceptance200.json  the 200-case sweep of test_acceptance.py:133-154
+  eesd_toy.json       simulate_eesd with the toy greedy oracle + Bernoulli
+  transformer.json    reference decode_ppsd driving oracle/transformer.py
+"""
+
+from __future__ import annotations
+
+import hashlib
+import io
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import specpipe as sp  # noqa: E402
+from specpipe.pipesim import EventTrace  # noqa: E402
+
+
+def trace_text(trace) -> str:
+    buf = io.StringIO()
+    trace.write_csv(buf)
+    return buf.getvalue()
+
+
+def metrics_list(m) -> list:
+    return [m.committed_tokens, m.ticks, m.accepts, m.rejects,
+            m.alpha_all_measured, m.throughput, m.speedup_vs_ar]
+
+
+def run_rng(seed):
+    return sp.RngStream(sp.derive_seed(seed, "run"))
+
+
+TOY_CASES = [
+    # name, n_layers, vocab, lm seed label, beta, cfg kwargs, prompt, max_tokens
+    ("survey_b0", 32, 16, 0, 0.0, dict(n_layers=32, exit_depth=8), None, 128),
+    ("survey_b1", 32, 16, 0, 1.0, dict(n_layers=32, exit_depth=8), None, 128),
+    ("survey_b2", 32, 16, 0, 2.0, dict(n_layers=32, exit_depth=8), None, 128),
+    ("decode_lm3", 32, 16, 3, 1.0, dict(n_layers=32, exit_depth=8), [1, 2, 3, 4], 96),
+    ("deep_exit", 32, 16, 5, 1.0, dict(n_layers=32, exit_depth=8, exit_stage=2), [6, 6], 48),
+    ("comm_lat2", 32, 16, 5, 1.0, dict(n_layers=32, exit_depth=8, comm_latency=2), [6, 6], 48),
+    ("remainder33", 33, 16, 7, 1.5, dict(n_layers=33, exit_depth=8), [9, 0, 2], 80),
+    ("two_stage", 40, 16, 8, 0.7, dict(n_layers=40, exit_depth=20), [4], 64),
+    ("eight_stage", 80, 16, 9, 1.0, dict(n_layers=80, exit_depth=10), [3, 1, 4, 1, 5], 100),
+    ("vocab1000", 32, 1000, 10, 0.3, dict(n_layers=32, exit_depth=8), [17, 999, 0, 512], 128),
+    ("vocab32000", 32, 32000, 11, 0.2, dict(n_layers=32, exit_depth=8), [1, 31999], 40),
+    ("deep_exit3_lat1", 48, 16, 12, 1.0, dict(n_layers=48, exit_depth=8, exit_stage=3, comm_latency=1), [2, 2, 2], 60),
+    ("single_token", 32, 16, 13, 1.0, dict(n_layers=32, exit_depth=8), [5], 1),
+    ("zero_tokens", 32, 16, 13, 1.0, dict(n_layers=32, exit_depth=8), [5], 0),
+]
+
+
+def make_toy():
+    out = []
+    for name, n, vocab, seed, beta, cfgkw, prompt, max_tokens in TOY_CASES:
+        lm = sp.ToyLM(n_layers=n, vocab=vocab, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        cfg = sp.PipelineConfig(**cfgkw)
+        rng = run_rng(seed)
+        if prompt is None:
+            prompt = sp.default_prompt(vocab, rng)
+        toks, m, tr = sp.decode_ppsd(lm, cfg, prompt, max_tokens, "greedy", run_rng(seed))
+        ar = sp.decode_autoregressive(lm, prompt, max_tokens, "greedy", run_rng(seed))
+        fr_toks, fr_m, _ = sp.decode_ppsd(lm, cfg, prompt, max_tokens, "greedy", run_rng(seed),
+                                          force_reject=True)
+        assert toks == ar == fr_toks
+        out.append(dict(
+            name=name, n_layers=n, vocab=vocab, lm_seed=lm.seed, beta=beta, cfg=cfgkw,
+            prompt=list(map(int, prompt)), max_tokens=max_tokens, rng_seed=run_rng(seed).seed,
+            tokens=toks, metrics=metrics_list(m), trace_csv=trace_text(tr), ar_tokens=ar,
+            force_reject_metrics=metrics_list(fr_m)))
+    return out
+
+
+BERN_CASES = [
+    # alpha, cfg kwargs, horizon, seed
+    (0.6, dict(n_layers=32, exit_depth=8), 300, 0),
+    (1.0, dict(n_layers=32, exit_depth=8), 200, 0),
+    (0.0, dict(n_layers=32, exit_depth=8), 50, 1),
+    (0.5, dict(n_layers=32, exit_depth=8), 200, 5),
+    (0.7, dict(n_layers=33, exit_depth=8), 300, 11),
+    (0.6, dict(n_layers=32, exit_depth=8, exit_stage=2), 300, 12),
+    (0.8, dict(n_layers=32, exit_depth=8, comm_latency=1), 300, 13),
+    (0.4, dict(n_layers=80, exit_depth=10), 500, 14),
+    (0.9, dict(n_layers=40, exit_depth=20), 400, 15),
+]
+
+
+def make_bernoulli():
+    out = []
+    for alpha, cfgkw, horizon, seed in BERN_CASES:
+        cfg = sp.PipelineConfig(**cfgkw)
+        tr = EventTrace()
+        m = sp.simulate_ppsd(cfg, sp.AcceptanceOracle.bernoulli(alpha), horizon, run_rng(seed), trace=tr)
+        fast = sp.simulate_ppsd(cfg, sp.AcceptanceOracle.bernoulli(alpha), horizon, run_rng(seed))
+        assert fast == m
+        out.append(dict(alpha=alpha, cfg=cfgkw, horizon=horizon, rng_seed=run_rng(seed).seed,
+                        metrics=metrics_list(m), trace_csv=trace_text(tr)))
+    return out
+
+
+def tokens_digest(tokens) -> str:
+    return hashlib.sha256(",".join(map(str, tokens)).encode()).hexdigest()
+
+
+def make_acceptance200():
+    """Mirror of test_acceptance.py:133-154 inputs, with outputs recorded."""
+    gen = np.random.default_rng(2026)
+    cfg = sp.PipelineConfig(32, 8)
+    cases = []
+    for i in range(200):
+        seed = int(gen.integers(2**63))
+        lm = sp.ToyLM(n_layers=32, vocab=16, seed=seed, misalignment=1.0)
+        prompt = [int(t) for t in gen.integers(16, size=8)]
+        toks, m, _ = sp.decode_ppsd(lm, cfg, prompt, 256, "greedy", run_rng(i))
+        cases.append(dict(lm_seed=seed, prompt=prompt, tokens_sha256=tokens_digest(toks),
+                          first8=toks[:8], metrics=metrics_list(m)))
+    return cases
+
+
+def make_eesd():
+    out = []
+    for gamma, beta, seed in ((5, 1.0, 0), (3, 0.0, 1), (10, 2.0, 2), (1, 1.0, 3)):
+        lm = sp.ToyLM(n_layers=32, vocab=16, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        cfg = sp.PipelineConfig(32, 8)
+        tr = EventTrace()
+        m = sp.simulate_eesd(cfg, gamma, sp.AcceptanceOracle.toylm_greedy(lm), 128, run_rng(seed), trace=tr)
+        out.append(dict(kind="toy", gamma=gamma, beta=beta, lm_seed=lm.seed, rng_seed=run_rng(seed).seed,
+                        horizon=128, metrics=metrics_list(m), trace_csv=trace_text(tr)))
+    for gamma, alpha, seed in ((4, 0.5, 4), (10, 0.3, 5)):
+        cfg = sp.PipelineConfig(32, 8)
+        tr = EventTrace()
+        m = sp.simulate_eesd(cfg, gamma, sp.AcceptanceOracle.bernoulli(alpha), 200, run_rng(seed), trace=tr)
+        out.append(dict(kind="bernoulli", gamma=gamma, alpha=alpha, rng_seed=run_rng(seed).seed,
+                        horizon=200, metrics=metrics_list(m), trace_csv=trace_text(tr)))
+    return out
+
+
+def make_transformer():
+    """Reference decode_ppsd / decode_autoregressive driving the CPU fp64
+    transformer oracle through the reference's own 7-member model protocol."""
+    from oracle.transformer import TransformerOracle, tiny_config
+
+    out = []
+    for name, deep_scale, cfgkw, n_tok, seed in (
+        ("tiny_ds010", 0.10, dict(n_layers=32, exit_depth=8), 128, 0),
+        ("tiny_ds025", 0.25, dict(n_layers=32, exit_depth=8), 128, 1),
+        ("tiny_ds000", 0.0, dict(n_layers=32, exit_depth=8), 64, 2),
+        ("tiny_deep_exit", 0.15, dict(n_layers=32, exit_depth=8, exit_stage=2), 64, 3),
+    ):
+        mc = tiny_config()
+        lm = TransformerOracle(mc, seed=seed, deep_scale=deep_scale, deep_from=8, dtype=np.float64)
+        cfg = sp.PipelineConfig(**cfgkw)
+        prompt = sp.default_prompt(mc.vocab, run_rng(seed))
+        toks, m, tr = sp.decode_ppsd(lm, cfg, prompt, n_tok, "greedy", run_rng(seed))
+        ar = sp.decode_autoregressive(lm, prompt, n_tok, "greedy", run_rng(seed))
+        assert toks == ar, name
+        out.append(dict(name=name, model=mc.to_dict(), seed=seed, deep_scale=deep_scale, deep_from=8,
+                        cfg=cfgkw, prompt=prompt, max_tokens=n_tok, tokens=toks,
+                        metrics=metrics_list(m), trace_csv=trace_text(tr),
+                        min_margins=lm.margin_report()))
+        print(name, metrics_list(m), flush=True)
+    return out
+
+
+def main(argv):
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf"}
+    jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
+            ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
+            ("tf", "transformer.json", make_transformer)]
+    for key, fname, fn in jobs:
+        if key in which:
+            data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",
+                        cases=fn())
+            with open(os.path.join(HERE, fname), "w") as fh:
+                json.dump(data, fh, indent=0, sort_keys=True)
+            print("wrote", fname, len(data["cases"]), "cases")
+
+
+if __name__ == "__main__":
+    main(sys.argv)
