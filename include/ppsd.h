@@ -1,0 +1,180 @@
+/*
+ * ppsd.h — C ABI of the B200 greedy PPSD decode engine (libppsd.so).
+ *
+ * This is the drop-in boundary for the reference's decode path. The reference
+ * (`specpipe`, pure Python) exposes the path as Python functions; each entry
+ * point below is what a ctypes binding inside the reference would call in
+ * place of the named reference function (binding shown in INTEGRATION.md):
+ *
+ *   ppsd_engine_create   <- the (model, PipelineConfig) pair handed to
+ *                           decode_ppsd: ToyLM(...) pkg/src/specpipe/toylm.py:55-68,
+ *                           PipelineConfig(...) pkg/src/specpipe/pipesim.py:60-114
+ *   ppsd_decode          <- decode_ppsd, pkg/src/specpipe/pipesim.py:595-633
+ *                           (its machine: _ppsd_machine, pipesim.py:670-789)
+ *   ppsd_decode_ar       <- decode_autoregressive, pkg/src/specpipe/pipesim.py:390-409
+ *   ppsd_decode_eesd     <- simulate_eesd with a greedy model oracle,
+ *                           pkg/src/specpipe/pipesim.py:435-551
+ *   ppsd_simulate        <- simulate_ppsd with AcceptanceOracle.bernoulli,
+ *                           pkg/src/specpipe/pipesim.py:571-592, 636-667
+ *   ppsd_metrics         <- RunMetrics, pkg/src/specpipe/pipesim.py:235-275
+ *   ppsd_trace_row       <- TraceRow / EventTrace, pkg/src/specpipe/pipesim.py:145-189
+ *
+ * Conventions: every function returns PPSD_OK (0) or a negative status;
+ * PPSD_EINVAL maps to the reference's ValueError (pipesim.py:412-428, 76-99),
+ * PPSD_ECUDA / PPSD_ESTATE to RuntimeError. ppsd_last_error() returns a
+ * thread-local message for the last failure. Device pointers passed in are
+ * BORROWED for the engine's lifetime; the engine owns only its KV pool,
+ * activation slots and scheduler state. One host thread drives one engine.
+ */
+#ifndef PPSD_H
+#define PPSD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPSD_OK 0
+#define PPSD_EINVAL (-1)
+#define PPSD_ECUDA (-2)
+#define PPSD_ESTATE (-3)
+#define PPSD_EUNSUPPORTED (-4)
+
+#define PPSD_MODEL_BERNOULLI 0  /* schedule-only oracle, no model compute  */
+#define PPSD_MODEL_TOYLM 1      /* the reference ToyLM, bit-exact on GPU    */
+#define PPSD_MODEL_TRANSFORMER 2 /* Llama-style decoder, bf16 weights       */
+
+/* trace row kinds, pipesim.py:47-51; verdicts "", "accept", "reject" */
+#define PPSD_ACTIVATION 0
+#define PPSD_DRAFT_TOKEN 1
+#define PPSD_FINAL_TOKEN 2
+#define PPSD_CHECK_TOKEN 3
+#define PPSD_VERDICT_NONE 0
+#define PPSD_VERDICT_ACCEPT 1
+#define PPSD_VERDICT_REJECT 2
+#define PPSD_NO_TOKEN (-1) /* the reference's `token=None` */
+
+typedef struct ppsd_engine ppsd_engine;
+
+typedef struct {
+  int32_t kind;        /* PPSD_MODEL_* */
+  int32_t n_layers;    /* N, pipesim.py:69 / toylm.py:57 */
+  int32_t vocab;       /* V */
+  /* transformer shape (ignored for other kinds) */
+  int32_t d_model, n_heads, n_kv_heads, head_dim, ffn_dim;
+  float rms_eps, rope_theta;
+  int32_t kv_bf16;     /* 1: bf16 KV cache, 0: fp32 KV cache */
+  int32_t max_ctx;     /* prompt + generated tokens capacity */
+  /* ToyLM (toylm.py:55-68) */
+  uint64_t toy_seed;
+  double toy_misalignment;
+} ppsd_model_desc;
+
+/* Transformer weights, device pointers in the engine's physical layout
+ * (see DESIGN.md §"Data layout"): bf16 matrices row-major [rows][cols],
+ * q/k rows pair-interleaved for RoPE, gate/up rows interleaved. Arrays of
+ * per-layer pointers are HOST arrays of length n_layers (entries for layers
+ * that are not local to this engine may be NULL). */
+typedef struct {
+  const void* embed;        /* [V][d] bf16 */
+  const void* lm_head;      /* [V][d] bf16, shared by the exit and final heads */
+  const float* final_norm;  /* [d] */
+  const float* exit_norm;   /* [d] */
+  const void* const* w_qkv; /* [(H+2KV)*hd][d] bf16 */
+  const void* const* w_o;   /* [d][H*hd]       bf16 */
+  const void* const* w_gu;  /* [2*ffn][d]      bf16 */
+  const void* const* w_down;/* [d][ffn]        bf16 */
+  const float* const* attn_norm; /* [d] */
+  const float* const* mlp_norm;  /* [d] */
+  const float* rope_cos;    /* [max_ctx][hd/2] */
+  const float* rope_sin;
+} ppsd_weights;
+
+typedef struct {
+  int32_t n_layers, exit_depth;
+  int32_t exit_stage;   /* 0 = default (1), pipesim.py:92-99 */
+  int32_t comm_latency; /* pipesim.py:72, 107-110 */
+  int32_t stage_lo, stage_hi; /* local stages (1-based, inclusive); 0,0 = all */
+  int32_t device;
+} ppsd_pipeline_desc;
+
+typedef struct {
+  int64_t committed_tokens, ticks, accepts, rejects; /* RunMetrics order */
+  int32_t alpha_valid;
+  double alpha_all_measured, throughput, speedup_vs_ar;
+  double decode_ms;     /* CUDA-event time of the decode loop (prefill excluded) */
+  double prefill_ms;    /* CUDA-event time of the prompt prefill */
+  int64_t gpu_launches; /* kernels this engine launched for the call */
+} ppsd_metrics;
+
+typedef struct {
+  int32_t tick, stage, kind, position, token, verdict;
+} ppsd_trace_row;
+
+const char* ppsd_last_error(void);
+const char* ppsd_build_info(void);
+
+int ppsd_engine_create(const ppsd_model_desc* model, const ppsd_weights* weights,
+                       const ppsd_pipeline_desc* pipe, void* cuda_stream,
+                       ppsd_engine** out);
+int ppsd_engine_destroy(ppsd_engine* e);
+
+/* greedy verify-while-draft decode; tokens/trace are HOST buffers */
+int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
+                int32_t max_tokens, int32_t force_reject, int32_t* out_tokens,
+                ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                int64_t* trace_len);
+
+/* greedy full-model autoregressive decode (the oracle / AR baseline) */
+int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
+                   int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out);
+
+/* greedy draft-then-verify rounds of gamma drafts (EESD baseline) */
+int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32_t n_prompt,
+                     int32_t horizon, int32_t* out_tokens, int32_t out_cap,
+                     ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                     int64_t* trace_len);
+
+/* schedule-only PPSD with Bernoulli(alpha) verdicts drawn from the counter
+ * stream seeded verify_seed (= derive_seed(rng.seed, "verify")) */
+int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed, int32_t horizon,
+                  int32_t force_reject, ppsd_metrics* out, ppsd_trace_row* trace,
+                  int64_t trace_cap, int64_t* trace_len);
+
+/* Multi-rank stepping (one engine per GPU owning stages [stage_lo, stage_hi]).
+ * Between tick_compute and tick_finish the caller all-gathers every rank's
+ * outbox into every rank's inbox (NCCL all_gather over NVLink); the scheduler
+ * state is replicated and advances identically on every rank. */
+int ppsd_exchange_info(ppsd_engine* e, void** outbox, void** inbox, int64_t* bytes_per_rank);
+int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
+                    int32_t force_reject, int32_t world, int32_t rank);
+int ppsd_step_compute(ppsd_engine* e);
+int ppsd_step_finish(ppsd_engine* e);
+int ppsd_step_poll(ppsd_engine* e, int32_t* done, int64_t* committed, int64_t* ticks);
+int ppsd_step_end(ppsd_engine* e, int32_t* out_tokens, ppsd_metrics* out,
+                  ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len);
+
+/* Device weight initialiser: the counter-hash init of oracle/transformer.py,
+ * written straight into the engine's physical layout.
+ * layout: 0 plain [rows][cols]; 1 = fused qkv (q,k pair-interleaved);
+ * 2 = fused gate/up (row-interleaved). For layouts 1/2 tid0..tid2 are the
+ * logical tensors' ids and a0..a2 their scales. */
+int ppsd_init_weight(void* dst_bf16, int32_t layout, int64_t rows, int64_t cols,
+                     uint64_t seed, const uint64_t* tids, const float* scales,
+                     int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                     void* cuda_stream);
+
+/* fp32 logits of the last head evaluation: which 0 = exit head, 1 = final
+ * head (length vocab) — debugging / tolerance tests. */
+int ppsd_read_logits(ppsd_engine* e, int32_t which, float* out);
+
+/* Kernel-time probe for the roofline: times `reps` launches of the engine's
+ * dominant layer GEMV (gate/up) with CUDA events on the engine stream. */
+int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps,
+                    double* avg_ms, double* bytes_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPSD_H */

@@ -1,0 +1,179 @@
+// attn.cu — split-K decode attention over the paged KV cache.
+//
+// Work item = (stage group, kv head, KV page). One KV page is kPage=64
+// positions of one kv head stored contiguously ([page][kvh][64][hd]), so an
+// item streams one contiguous 16 KB (bf16, hd=128) K block and one V block.
+// All q heads that share the kv head (GQA) are scored against that block in
+// the same pass. Page boundaries are absolute positions, so the partial
+// results — and the ordered merge done by the last CTA to finish a
+// (chain, kv head) — depend only on the context length, never on how many
+// stages share the launch: PPSD and AR attention are bit-identical.
+#include <float.h>
+
+#include "kernels.cuh"
+
+namespace ppsd {
+
+template <typename T>
+__device__ __forceinline__ void load16(const T* p, float* out);
+template <>
+__device__ __forceinline__ void load16<float>(const float* p, float* out) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load16<__nv_bfloat16>(const __nv_bfloat16* p, float* out) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  out[0] = bf16lo(v.x); out[1] = bf16hi(v.x); out[2] = bf16lo(v.y); out[3] = bf16hi(v.y);
+  out[4] = bf16lo(v.z); out[5] = bf16hi(v.z); out[6] = bf16lo(v.w); out[7] = bf16hi(v.w);
+}
+__device__ __forceinline__ float tof(float v) { return v; }
+__device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <int HD, typename KVT, int QPK>
+__global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
+  constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte load
+  constexpr int LPT = HD / EPV;                // lanes per token
+  constexpr int TPW = 32 / LPT;                // tokens per warp pass
+  static_assert(LPT >= 1 && LPT <= 32 && (32 % LPT) == 0, "head_dim / dtype combination");
+  __shared__ float qs[QPK][HD];
+  __shared__ float sc[QPK][kPage];
+  __shared__ float s_m[QPK], s_l[QPK];
+  __shared__ int s_last;
+
+  const Work* w = a.work;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int H = a.dm.H, KVh = a.dm.KV;
+  const float scale = 1.0f / sqrtf((float)HD);
+
+  for (int item = blockIdx.x;; item += gridDim.x) {
+    int g = -1, rem = item, nch = 0;
+    for (int gg = 0; gg < w->G; ++gg) {
+      if (w->slot[gg] < 0 || a.layer_i >= w->nl[gg]) continue;
+      nch = (w->pos[gg] + kPage) / kPage;  // ceil((pos+1)/kPage)
+      if (rem < nch * KVh) { g = gg; break; }
+      rem -= nch * KVh;
+    }
+    if (g < 0) break;
+    const int kvh = rem / nch, c = rem - kvh * nch;
+    const int slot = w->slot[g], ctx = w->pos[g] + 1;
+    const int n = min(kPage, ctx - c * kPage);
+    const LayerW& L = a.layers[w->first[g] + a.layer_i];
+    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * kPage * HD;
+    const KVT* kb = reinterpret_cast<const KVT*>(L.kc) + blk;
+    const KVT* vb = reinterpret_cast<const KVT*>(L.vc) + blk;
+    const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
+    for (int i = tid; i < QPK * HD; i += 128) qs[i / HD][i % HD] = qsrc[i];
+    __syncthreads();
+
+    // scores: LPT lanes per token, one 16-byte K vector per lane
+    const int li = lane % LPT, tw = lane / LPT;
+    for (int base = warp * TPW; base < n; base += 4 * TPW) {
+      const int tt = base + tw;
+      float part[QPK];
+#pragma unroll
+      for (int i = 0; i < QPK; ++i) part[i] = 0.f;
+      if (tt < n) {
+        float kf[EPV];
+        load16<KVT>(kb + (size_t)tt * HD + li * EPV, kf);
+#pragma unroll
+        for (int i = 0; i < QPK; ++i)
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) part[i] = fmaf(kf[e], qs[i][li * EPV + e], part[i]);
+      }
+#pragma unroll
+      for (int off = LPT / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int i = 0; i < QPK; ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], off);
+      if (li == 0 && tt < n)
+#pragma unroll
+        for (int i = 0; i < QPK; ++i) sc[i][tt] = part[i] * scale;
+    }
+    __syncthreads();
+
+    for (int i = warp; i < QPK; i += 4) {  // chunk-local softmax statistics
+      float mx = -FLT_MAX;
+      for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, sc[i][tt]);
+      mx = warp_max(mx);
+      float l = 0.f;
+      for (int tt = lane; tt < n; tt += 32) {
+        const float p = expf(sc[i][tt] - mx);
+        sc[i][tt] = p;
+        l += p;
+      }
+      l = warp_sum(l);
+      if (lane == 0) { s_m[i] = mx; s_l[i] = l; }
+    }
+    __syncthreads();
+
+    float* pbase = a.part + (((size_t)slot * H + (size_t)kvh * QPK) * a.max_pages) * (HD + 2);
+    for (int idx = tid; idx < QPK * HD; idx += 128) {
+      const int i = idx / HD, d = idx - i * HD;
+      float acc = 0.f;
+      for (int tt = 0; tt < n; ++tt) acc = fmaf(sc[i][tt], tof(vb[(size_t)tt * HD + d]), acc);
+      pbase[((size_t)i * a.max_pages + c) * (HD + 2) + d] = acc;
+    }
+    if (tid < QPK) {
+      pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD] = s_m[tid];
+      pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD + 1] = s_l[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(&a.cnt[slot * KVh + kvh], 1) == nch - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // ordered merge of the page partials
+      __threadfence();
+      for (int idx = tid; idx < QPK * HD; idx += 128) {
+        const int i = idx / HD, d = idx - i * HD;
+        const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2);
+        float M = -FLT_MAX;
+        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(pb + (size_t)cc * (HD + 2) + HD));
+        float Ls = 0.f, O = 0.f;
+        for (int cc = 0; cc < nch; ++cc) {
+          const float e = expf(__ldcg(pb + (size_t)cc * (HD + 2) + HD) - M);
+          Ls = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + HD + 1), e, Ls);
+          O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + d), e, O);
+        }
+        a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / Ls;
+      }
+      if (tid == 0) a.cnt[slot * KVh + kvh] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+namespace {
+template <int HD, typename KVT>
+cudaError_t launch_qpk(const AttnArgs& a, int grid, cudaStream_t st) {
+  switch (a.dm.H / a.dm.KV) {
+    case 1: attn_kernel<HD, KVT, 1><<<grid, 128, 0, st>>>(a); break;
+    case 2: attn_kernel<HD, KVT, 2><<<grid, 128, 0, st>>>(a); break;
+    case 4: attn_kernel<HD, KVT, 4><<<grid, 128, 0, st>>>(a); break;
+    case 8: attn_kernel<HD, KVT, 8><<<grid, 128, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template <int HD>
+cudaError_t launch_hd(const AttnArgs& a, int grid, cudaStream_t st) {
+  return a.dm.kv_bf16 ? launch_qpk<HD, __nv_bfloat16>(a, grid, st) : launch_qpk<HD, float>(a, grid, st);
+}
+}  // namespace
+
+bool attn_supported(int hd, int qpk) {
+  return (hd == 16 || hd == 32 || hd == 64 || hd == 128) && (qpk == 1 || qpk == 2 || qpk == 4 || qpk == 8);
+}
+
+cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) {
+  switch (a.dm.hd) {
+    case 16: return launch_hd<16>(a, grid, st);
+    case 32: return launch_hd<32>(a, grid, st);
+    case 64: return launch_hd<64>(a, grid, st);
+    case 128: return launch_hd<128>(a, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ppsd

@@ -1,0 +1,718 @@
+// engine.cu — libppsd.so: the C ABI declared in include/ppsd.h.
+//
+// A tick of the verify-while-draft machine is one CUDA graph:
+//   [per layer slot i of the local stages: qkv_rope, attention, o_proj+res,
+//    gate_up+swiglu, down+res] -> [tied exit/final LM head + argmax]
+//   -> [sched_tick: verdict/draft/rollback for tick t, plan tick t+1, embed]
+// Graph arguments never change; per-call state lives in device memory
+// (TickCtx / Sched / Work), so the host enqueues ticks back to back and only
+// synchronises when the lower bound on the remaining ticks is exhausted.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "engine_dev.cuh"
+
+using namespace ppsd;
+
+namespace ppsd {
+bool attn_supported(int hd, int qpk);
+}
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CU(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t _e = (x);                                                                     \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(PPSD_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " @" +        \
+                                  std::to_string(__LINE__));                                  \
+  } while (0)
+
+struct GemvPlan {
+  int vpt = 0, tr = 0, ns = 0, R = 0, K = 0;
+  size_t smem = 0;
+};
+
+struct ppsd_engine {
+  ppsd_model_desc md{};
+  ppsd_pipeline_desc pd{};
+  int device = 0, num_sms = 148;
+  cudaStream_t st = nullptr;
+  SchedCfg cfg{};
+  int S = 0, lo = 1, hi = 1, max_local_layers = 0, first_local_layer = 0, n_local_layers = 0;
+  Dims dm{};
+  // device state
+  Sched* d_sched = nullptr;
+  Work* d_work = nullptr;
+  Work* d_work_ar = nullptr;
+  TickCtx* d_ctx = nullptr;
+  ArCtl* d_arctl = nullptr;
+  int32_t* d_tokens = nullptr;
+  uint64_t* d_pdig = nullptr;
+  uint64_t* d_chain_dig = nullptr;
+  TraceRow* d_trace = nullptr;
+  int64_t trace_cap = 0;
+  // transformer buffers
+  std::vector<LayerW> h_layers;
+  LayerW* d_layers = nullptr;
+  float *d_x = nullptr, *d_q = nullptr, *d_o = nullptr, *d_h = nullptr, *d_logits = nullptr;
+  float *d_attn_part = nullptr, *d_head_part = nullptr;
+  int32_t *d_attn_cnt = nullptr, *d_head_cnt = nullptr, *d_page_table = nullptr;
+  void* d_kv = nullptr;
+  int max_pages = 0;
+  GemvPlan gp[5];
+  const __nv_bfloat16* lm_head = nullptr;
+  const float* final_norm = nullptr;
+  const float* exit_norm = nullptr;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  // graphs
+  cudaGraphExec_t g_tick = nullptr, g_ar = nullptr, g_prefill = nullptr;
+  int64_t tick_launches = 0, ar_launches = 0, prefill_launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  // host staging
+  Sched* h_sched = nullptr;  // pinned
+  TickCtx h_ctx{};
+};
+
+extern "C" const char* ppsd_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char* ppsd_build_info(void) {
+  return "libppsd sm_100a: tma-bulk gemv ring, split-K paged attention, device tick machine";
+}
+
+static int attn_grid(const ppsd_engine* e) { return 2 * e->num_sms; }
+
+// ---------------------------------------------------------------------------
+// enqueue helpers (also used while capturing graphs)
+
+static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat) {
+  const GemvPlan& p = e->gp[mat];
+  GemvArgs a{};
+  a.work = w;
+  a.layer_i = layer_i;
+  a.mat = mat;
+  a.layers = e->d_layers;
+  a.head_w = e->lm_head;
+  a.head_norm0 = e->exit_norm;
+  a.head_norm1 = e->final_norm;
+  a.R = p.R;
+  a.K = p.K;
+  a.nstage = p.ns;
+  a.dm = e->dm;
+  a.x = e->d_x;
+  a.q = e->d_q;
+  a.o = e->d_o;
+  a.h = e->d_h;
+  a.logits = e->d_logits;
+  a.rope_cos = e->rope_cos;
+  a.rope_sin = e->rope_sin;
+  a.page_table = e->d_page_table;
+  a.head_part = e->d_head_part;
+  a.head_cnt = e->d_head_cnt;
+  return gemv_launch(a, p.vpt, p.smem, e->num_sms, e->st);
+}
+
+static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
+  AttnArgs a{};
+  a.work = w;
+  a.layer_i = layer_i;
+  a.layers = e->d_layers;
+  a.dm = e->dm;
+  a.q = e->d_q;
+  a.o = e->d_o;
+  a.part = e->d_attn_part;
+  a.cnt = e->d_attn_cnt;
+  a.page_table = e->d_page_table;
+  a.max_pages = e->max_pages;
+  return attn_launch(a, attn_grid(e), e->st);
+}
+
+// returns launches enqueued, or -1 on error
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots) {
+  int n = 0;
+  for (int i = 0; i < n_slots; ++i) {
+    if (enqueue_gemv(e, w, i, kMatQKV) != cudaSuccess) return -1;
+    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatO) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatGU) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatDown) != cudaSuccess) return -1;
+    n += 5;
+  }
+  return n;
+}
+
+template <class F>
+static int capture(ppsd_engine* e, F body, cudaGraphExec_t* out, int64_t* nlaunch) {
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
+  int n = body();
+  cudaError_t ce = cudaStreamEndCapture(e->st, &g);
+  if (n < 0) {
+    if (g) cudaGraphDestroy(g);
+    return fail(PPSD_ECUDA, std::string("kernel launch failed during capture: ") +
+                                cudaGetErrorString(cudaGetLastError()));
+  }
+  CU(ce);
+  CU(cudaGraphInstantiate(out, g, 0));
+  CU(cudaGraphDestroy(g));
+  *nlaunch = n;
+  return PPSD_OK;
+}
+
+static int build_graphs(ppsd_engine* e) {
+  const int kind = e->md.kind;
+  int rc = capture(
+      e,
+      [&]() -> int {
+        int n = 0;
+        if (kind == PPSD_MODEL_TRANSFORMER) {
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+          if (m < 0) return -1;
+          n += m;
+          if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
+          n += 1;
+        } else if (kind == PPSD_MODEL_TOYLM) {
+          toy_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx);
+          if (cudaGetLastError() != cudaSuccess) return -1;
+          n += 1;
+        }
+        sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 0);
+        if (cudaGetLastError() != cudaSuccess) return -1;
+        return n + 1;
+      },
+      &e->g_tick, &e->tick_launches);
+  if (rc) return rc;
+  if (kind != PPSD_MODEL_TRANSFORMER) return PPSD_OK;
+  for (int with_head = 0; with_head < 2; ++with_head) {
+    rc = capture(
+        e,
+        [&]() -> int {
+          ar_begin_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, e->d_arctl, with_head);
+          if (cudaGetLastError() != cudaSuccess) return -1;
+          int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
+          if (m < 0) return -1;
+          if (with_head && enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
+          ar_end_kernel<<<1, 32, 0, e->st>>>(e->d_ctx, e->d_arctl, with_head);
+          if (cudaGetLastError() != cudaSuccess) return -1;
+          return m + 2 + with_head;
+        },
+        with_head ? &e->g_ar : &e->g_prefill, with_head ? &e->ar_launches : &e->prefill_launches);
+    if (rc) return rc;
+  }
+  return PPSD_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+static void free_engine(ppsd_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->st) cudaStreamSynchronize(e->st);
+  if (e->g_tick) cudaGraphExecDestroy(e->g_tick);
+  if (e->g_ar) cudaGraphExecDestroy(e->g_ar);
+  if (e->g_prefill) cudaGraphExecDestroy(e->g_prefill);
+  void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+                  e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
+                  e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (e->h_sched) cudaFreeHost(e->h_sched);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->ev2) cudaEventDestroy(e->ev2);
+  if (e->st) cudaStreamDestroy(e->st);
+  delete e;
+}
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t bytes) {
+  cudaError_t r = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  if (r == cudaSuccess) r = cudaMemset(*p, 0, bytes);
+  return r;
+}
+
+static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const ppsd_pipeline_desc* pd,
+                       ppsd_engine* e) {
+  e->md = *md;
+  e->pd = *pd;
+  e->device = pd->device;
+  CU(cudaSetDevice(e->device));
+  CU(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
+  CU(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+  CU(cudaEventCreate(&e->ev0));
+  CU(cudaEventCreate(&e->ev1));
+  CU(cudaEventCreate(&e->ev2));
+  if (md->n_layers != pd->n_layers)
+    return fail(PPSD_EINVAL, "pipeline is " + std::to_string(pd->n_layers) + " layers deep but the model has " +
+                                 std::to_string(md->n_layers));
+  if (sched_configure(&e->cfg, pd->n_layers, pd->exit_depth, pd->exit_stage, pd->comm_latency) != 0)
+    return fail(PPSD_EINVAL, "invalid pipeline (needs 2..96 stages, 1 <= exit_stage <= S-1, comm_latency >= 0)");
+  e->S = e->cfg.S;
+  e->lo = pd->stage_lo > 0 ? pd->stage_lo : 1;
+  e->hi = pd->stage_hi > 0 ? pd->stage_hi : e->S;
+  if (e->lo > e->hi || e->hi > e->S) return fail(PPSD_EINVAL, "bad local stage range");
+  e->first_local_layer = e->cfg.stage_first[e->lo];
+  e->n_local_layers = 0;
+  for (int s = e->lo; s <= e->hi; ++s) {
+    e->max_local_layers = std::max(e->max_local_layers, (int)e->cfg.stage_layers[s]);
+    e->n_local_layers += e->cfg.stage_layers[s];
+  }
+  const int max_ctx = md->max_ctx > 0 ? md->max_ctx : 4096;
+  e->md.max_ctx = max_ctx;
+  const int nslot = e->cfg.nslot;
+
+  CU(dalloc(&e->d_sched, sizeof(Sched)));
+  CU(dalloc(&e->d_work, sizeof(Work)));
+  CU(dalloc(&e->d_work_ar, sizeof(Work)));
+  CU(dalloc(&e->d_ctx, sizeof(TickCtx)));
+  CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
+  CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&e->h_sched), sizeof(Sched)));
+
+  TickCtx& c = e->h_ctx;
+  c.sched = e->d_sched;
+  c.work = e->d_work;
+  c.work_ar = e->d_work_ar;
+  c.tokens = e->d_tokens;
+  c.model = md->kind;
+  c.lo = e->lo;
+  c.hi = e->hi;
+  c.n_layers = md->n_layers;
+  c.vocab = md->vocab;
+
+  if (md->kind == PPSD_MODEL_TOYLM) {
+    if (md->vocab < 2) return fail(PPSD_EINVAL, "vocab must be >= 2");
+    if (md->toy_misalignment < 0) return fail(PPSD_EINVAL, "misalignment must be non-negative");
+    CU(dalloc(&e->d_pdig, sizeof(uint64_t) * (max_ctx + 9)));
+    CU(dalloc(&e->d_chain_dig, sizeof(uint64_t) * nslot));
+    c.pdig = e->d_pdig;
+    c.chain_dig = e->d_chain_dig;
+    c.beta = md->toy_misalignment;
+    c.toy_seed = md->toy_seed;
+  } else if (md->kind == PPSD_MODEL_TRANSFORMER) {
+    Dims& d = e->dm;
+    d.d = md->d_model;
+    d.H = md->n_heads;
+    d.KV = md->n_kv_heads;
+    d.hd = md->head_dim;
+    d.ffn = md->ffn_dim;
+    d.V = md->vocab;
+    d.max_ctx = max_ctx;
+    d.nslot = nslot;
+    d.eps = md->rms_eps;
+    d.kv_bf16 = md->kv_bf16;
+    if (d.KV <= 0 || d.H % d.KV != 0 || !attn_supported(d.hd, d.H / d.KV))
+      return fail(PPSD_EUNSUPPORTED, "unsupported head geometry (head_dim in {16,32,64,128}, H/KV in {1,2,4,8})");
+    if (d.d % 8 || d.ffn % 8 || (d.H * d.hd) % 8)
+      return fail(PPSD_EUNSUPPORTED, "d_model, ffn_dim and H*head_dim must be multiples of 8");
+    if (!w || !w->lm_head || !w->embed || !w->final_norm || !w->exit_norm || !w->rope_cos)
+      return fail(PPSD_EINVAL, "missing transformer weights");
+    const int Rq = (d.H + 2 * d.KV) * d.hd;
+    const int shapes[5][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d}, {d.d, d.ffn}, {d.V, d.d}};
+    for (int m = 0; m < 5; ++m) {
+      GemvPlan& p = e->gp[m];
+      p.R = shapes[m][0];
+      p.K = shapes[m][1];
+      if (gemv_pick(p.K, p.R, m, &p.vpt, &p.tr, &p.ns, &p.smem) != 0)
+        return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
+                                           std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
+      CU(gemv_set_attrs(p.vpt, m, p.smem));
+    }
+    e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
+    e->final_norm = w->final_norm;
+    e->exit_norm = w->exit_norm;
+    e->rope_cos = w->rope_cos;
+    e->rope_sin = w->rope_sin;
+    c.embed = reinterpret_cast<const __nv_bfloat16*>(w->embed);
+    c.d = d.d;
+    // KV page pool for the local layers; identity page table
+    e->max_pages = (max_ctx + kPage - 1) / kPage;
+    const size_t esz = d.kv_bf16 ? 2 : 4;
+    const size_t per_layer = (size_t)e->max_pages * kPage * d.KV * d.hd * esz;
+    CU(cudaMalloc(&e->d_kv, per_layer * 2 * e->n_local_layers));
+    std::vector<int32_t> pt(e->max_pages);
+    for (int i = 0; i < e->max_pages; ++i) pt[i] = i;
+    CU(dalloc(&e->d_page_table, sizeof(int32_t) * e->max_pages));
+    CU(cudaMemcpy(e->d_page_table, pt.data(), sizeof(int32_t) * e->max_pages, cudaMemcpyHostToDevice));
+    e->h_layers.assign(md->n_layers, LayerW{});
+    for (int l = 0; l < md->n_layers; ++l) {
+      LayerW& L = e->h_layers[l];
+      const int li = l - e->first_local_layer;
+      if (li < 0 || li >= e->n_local_layers) continue;
+      if (!w->w_qkv[l] || !w->w_o[l] || !w->w_gu[l] || !w->w_down[l] || !w->attn_norm[l] || !w->mlp_norm[l])
+        return fail(PPSD_EINVAL, "missing weights for local layer " + std::to_string(l));
+      L.qkv = reinterpret_cast<const __nv_bfloat16*>(w->w_qkv[l]);
+      L.o = reinterpret_cast<const __nv_bfloat16*>(w->w_o[l]);
+      L.gu = reinterpret_cast<const __nv_bfloat16*>(w->w_gu[l]);
+      L.down = reinterpret_cast<const __nv_bfloat16*>(w->w_down[l]);
+      L.attn_norm = w->attn_norm[l];
+      L.mlp_norm = w->mlp_norm[l];
+      L.kc = static_cast<char*>(e->d_kv) + per_layer * (2 * li);
+      L.vc = static_cast<char*>(e->d_kv) + per_layer * (2 * li + 1);
+    }
+    CU(dalloc(&e->d_layers, sizeof(LayerW) * md->n_layers));
+    CU(cudaMemcpy(e->d_layers, e->h_layers.data(), sizeof(LayerW) * md->n_layers, cudaMemcpyHostToDevice));
+    const int qd = d.H * d.hd;
+    CU(dalloc(&e->d_x, sizeof(float) * (size_t)nslot * d.d));
+    CU(dalloc(&e->d_q, sizeof(float) * (size_t)nslot * qd));
+    CU(dalloc(&e->d_o, sizeof(float) * (size_t)nslot * qd));
+    CU(dalloc(&e->d_h, sizeof(float) * (size_t)nslot * d.ffn));
+    CU(dalloc(&e->d_logits, sizeof(float) * 2 * (size_t)d.V));
+    CU(dalloc(&e->d_attn_part, sizeof(float) * (size_t)nslot * d.H * e->max_pages * (d.hd + 2)));
+    CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * (size_t)nslot * d.KV));
+    CU(dalloc(&e->d_head_part, sizeof(float) * 4 * (size_t)e->num_sms));
+    CU(dalloc(&e->d_head_cnt, sizeof(int32_t)));
+    c.x = e->d_x;
+  } else if (md->kind != PPSD_MODEL_BERNOULLI) {
+    return fail(PPSD_EINVAL, "unknown model kind");
+  }
+  CU(cudaMemcpy(e->d_ctx, &c, sizeof(TickCtx), cudaMemcpyHostToDevice));
+  return build_graphs(e);
+}
+
+extern "C" int ppsd_engine_create(const ppsd_model_desc* model, const ppsd_weights* weights,
+                                  const ppsd_pipeline_desc* pipe, void* cuda_stream, ppsd_engine** out) {
+  (void)cuda_stream;
+  if (!model || !pipe || !out) return fail(PPSD_EINVAL, "null argument");
+  ppsd_engine* e = new ppsd_engine();
+  int rc = create_impl(model, weights, pipe, e);
+  if (rc != PPSD_OK) {
+    std::string keep = g_err;
+    free_engine(e);
+    g_err = keep;
+    return rc;
+  }
+  *out = e;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_engine_destroy(ppsd_engine* e) {
+  free_engine(e);
+  return PPSD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// decode
+
+static int check_prompt(const ppsd_engine* e, const int32_t* prompt, int n_prompt) {
+  if (n_prompt <= 0 || !prompt) return fail(PPSD_EINVAL, "prompt must be non-empty");
+  for (int i = 0; i < n_prompt; ++i)
+    if (prompt[i] < 0 || prompt[i] >= e->md.vocab)
+      return fail(PPSD_EINVAL, "prompt token " + std::to_string(prompt[i]) + " outside vocab of " +
+                                   std::to_string(e->md.vocab));
+  return PPSD_OK;
+}
+
+static int upload_prompt(ppsd_engine* e, const int32_t* prompt, int n_prompt) {
+  CU(cudaMemcpyAsync(e->d_tokens, prompt, sizeof(int32_t) * n_prompt, cudaMemcpyHostToDevice, e->st));
+  if (e->md.kind == PPSD_MODEL_TOYLM) {
+    std::vector<uint64_t> pd(n_prompt + 1);
+    pd[0] = hmix64(e->md.toy_seed ^ kSeqSalt);  // toylm.py:72-74
+    for (int i = 0; i < n_prompt; ++i) pd[i + 1] = toy_extend(pd[i], prompt[i]);
+    CU(cudaMemcpyAsync(e->d_pdig, pd.data(), sizeof(uint64_t) * (n_prompt + 1), cudaMemcpyHostToDevice, e->st));
+    CU(cudaStreamSynchronize(e->st));  // pd is a host temporary
+  }
+  return PPSD_OK;
+}
+
+// Run the prompt prefill (transformer): KV for tokens 0..n_prompt-2.
+static int prefill(ppsd_engine* e, int n_prompt, double* ms, int64_t* launches) {
+  *ms = 0;
+  if (e->md.kind != PPSD_MODEL_TRANSFORMER || n_prompt < 2) return PPSD_OK;
+  ArCtl ctl{0, e->first_local_layer, e->n_local_layers, 0};
+  CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
+  CU(cudaEventRecord(e->ev0, e->st));
+  for (int i = 0; i < n_prompt - 1; ++i) CU(cudaGraphLaunch(e->g_prefill, e->st));
+  CU(cudaEventRecord(e->ev1, e->st));
+  CU(cudaEventSynchronize(e->ev1));
+  float f = 0;
+  CU(cudaEventElapsedTime(&f, e->ev0, e->ev1));
+  *ms = f;
+  *launches += (int64_t)(n_prompt - 1) * e->prefill_launches;
+  return PPSD_OK;
+}
+
+static int ensure_trace(ppsd_engine* e, int64_t cap) {
+  if (cap <= e->trace_cap) return PPSD_OK;
+  if (e->d_trace) CU(cudaFree(e->d_trace));
+  e->d_trace = nullptr;
+  e->trace_cap = 0;
+  CU(cudaMalloc(&e->d_trace, sizeof(TraceRow) * cap));
+  e->trace_cap = cap;
+  return PPSD_OK;
+}
+
+static void fill_metrics(const ppsd_engine* e, const Sched& s, ppsd_metrics* m) {
+  m->committed_tokens = s.committed;
+  m->ticks = s.t;
+  m->accepts = s.accepts;
+  m->rejects = s.rejects;
+  const int64_t drafted = s.accepts + s.rejects;
+  m->alpha_valid = drafted > 0;
+  m->alpha_all_measured = drafted > 0 ? (double)s.accepts / (double)drafted : 0.0;
+  m->throughput = s.t > 0 ? (double)s.committed / (double)s.t : 0.0;
+  m->speedup_vs_ar = m->throughput * (double)(e->S * e->cfg.per);  // pipesim.py:274
+}
+
+static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int force_reject, double alpha,
+                       uint64_t verify_seed, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                       int64_t* trace_len, int64_t launches) {
+  const int64_t max_ticks = (int64_t)stop * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
+  int64_t cap = 0;
+  if (trace) {
+    cap = max_ticks * (e->S + 2);
+    if (trace_cap < cap) cap = trace_cap;
+    int rc = ensure_trace(e, cap);
+    if (rc) return rc;
+  }
+  Sched& s = *e->h_sched;
+  memset(&s, 0, sizeof(Sched));
+  s.c = e->cfg;
+  s.c.model = model;
+  s.c.force_reject = force_reject;
+  s.c.stop = stop;
+  s.c.n_prompt = n_prompt;
+  s.c.alpha = alpha;
+  s.c.verify_seed = verify_seed;
+  sched_reset(&s);
+  e->h_ctx.trace = trace ? e->d_trace : nullptr;
+  e->h_ctx.trace_cap = cap;
+  CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_sched, &s, sizeof(Sched), cudaMemcpyHostToDevice, e->st));
+  CU(cudaEventRecord(e->ev0, e->st));
+  sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 1);
+  CU(cudaGetLastError());
+  launches += 1;
+  int64_t committed = 0, ticks_launched = 0;
+  // small readback: committed .. error (8 int32 after SchedCfg)
+  const size_t off = offsetof(Sched, t);
+  const size_t len = offsetof(Sched, verify_counter) - off;
+  for (;;) {
+    const int64_t n = std::max<int64_t>(1, (int64_t)stop - committed);
+    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(e->g_tick, e->st));
+    ticks_launched += n;
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
+                       cudaMemcpyDeviceToHost, e->st));
+    CU(cudaStreamSynchronize(e->st));
+    if (s.error) break;
+    if (s.done) break;
+    committed = s.committed;
+    if (ticks_launched > max_ticks + 4)
+      return fail(PPSD_ESTATE, "tick machine did not converge (internal error)");
+  }
+  CU(cudaEventRecord(e->ev1, e->st));
+  CU(cudaMemcpyAsync(&s, e->d_sched, sizeof(Sched), cudaMemcpyDeviceToHost, e->st));
+  CU(cudaEventSynchronize(e->ev1));
+  CU(cudaStreamSynchronize(e->st));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  if (s.error & kErrOrder) return fail(PPSD_ESTATE, "verdicts must land in position order");
+  if (s.error & kErrTransit) return fail(PPSD_ESTATE, "transit queue overflow");
+  if (s.error & kErrTrace) return fail(PPSD_ESTATE, "trace buffer too small");
+  fill_metrics(e, s, out);
+  out->decode_ms = ms;
+  out->gpu_launches = launches + ticks_launched * e->tick_launches;
+  if (trace) {
+    const int64_t nrows = std::min<int64_t>(s.trace_n, trace_cap);
+    if (nrows > 0)
+      CU(cudaMemcpy(trace, e->d_trace, sizeof(TraceRow) * nrows, cudaMemcpyDeviceToHost));
+    if (trace_len) *trace_len = nrows;
+  } else if (trace_len) {
+    *trace_len = 0;
+  }
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
+                           int32_t max_tokens, int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out,
+                           ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  if (e->lo != 1 || e->hi != e->S) return fail(PPSD_EINVAL, "engine holds a stage subset: use ppsd_step_*");
+  if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines run ppsd_simulate");
+  if (!greedy) return fail(PPSD_EUNSUPPORTED, "sampling mode is not implemented on the B200 engine yet");
+  int rc = check_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  if (max_tokens < 0) return fail(PPSD_EINVAL, "max_tokens must be >= 0");
+  memset(out, 0, sizeof(*out));
+  if (trace_len) *trace_len = 0;
+  if (max_tokens == 0) return PPSD_OK;  // pipesim.py:620-621
+  const int64_t need = (int64_t)n_prompt + max_tokens + (int64_t)e->S * e->cfg.per + 2;
+  if (need > e->md.max_ctx)
+    return fail(PPSD_EINVAL, "prompt + max_tokens exceeds the engine's max_ctx (" + std::to_string(e->md.max_ctx) + ")");
+  CU(cudaSetDevice(e->device));
+  rc = upload_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  int64_t launches = 0;
+  double pre_ms = 0;
+  rc = prefill(e, n_prompt, &pre_ms, &launches);
+  if (rc) return rc;
+  rc = run_machine(e, 1, n_prompt, max_tokens, force_reject, 0.0, 0, out, trace, trace_cap, trace_len, launches);
+  if (rc) return rc;
+  out->prefill_ms = pre_ms;
+  if (out_tokens)
+    CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * max_tokens, cudaMemcpyDeviceToHost));
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed, int32_t horizon,
+                             int32_t force_reject, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                             int64_t* trace_len) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  if (e->md.kind != PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "ppsd_simulate needs a Bernoulli engine");
+  if (horizon < 1) return fail(PPSD_EINVAL, "horizon must be >= 1");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(PPSD_EINVAL, "BERNOULLI oracle needs alpha in [0, 1]");
+  memset(out, 0, sizeof(*out));
+  CU(cudaSetDevice(e->device));
+  return run_machine(e, 0, 0, horizon, force_reject, alpha, verify_seed, out, trace, trace_cap, trace_len, 0);
+}
+
+extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
+                              int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines have no model");
+  if (e->lo != 1 || e->hi != e->S) return fail(PPSD_EINVAL, "engine holds a stage subset");
+  if (!greedy) return fail(PPSD_EUNSUPPORTED, "sampling mode is not implemented on the B200 engine yet");
+  int rc = check_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  if (max_tokens < 0) return fail(PPSD_EINVAL, "max_tokens must be >= 0");
+  memset(out, 0, sizeof(*out));
+  if (max_tokens == 0) return PPSD_OK;
+  if ((int64_t)n_prompt + max_tokens + 2 > e->md.max_ctx) return fail(PPSD_EINVAL, "exceeds max_ctx");
+  CU(cudaSetDevice(e->device));
+  rc = upload_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  int64_t launches = 0;
+  if (e->md.kind == PPSD_MODEL_TOYLM) {
+    CU(cudaEventRecord(e->ev0, e->st));
+    toy_ar_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, n_prompt, max_tokens);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(e->ev1, e->st));
+    launches = 1;
+  } else {
+    double pre_ms = 0;
+    rc = prefill(e, n_prompt, &pre_ms, &launches);
+    if (rc) return rc;
+    out->prefill_ms = pre_ms;
+    ArCtl ctl{n_prompt - 1, e->first_local_layer, e->n_local_layers, 0};
+    CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
+    CU(cudaEventRecord(e->ev0, e->st));
+    for (int i = 0; i < max_tokens; ++i) CU(cudaGraphLaunch(e->g_ar, e->st));
+    CU(cudaEventRecord(e->ev1, e->st));
+    launches += (int64_t)max_tokens * e->ar_launches;
+  }
+  CU(cudaEventSynchronize(e->ev1));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  out->decode_ms = ms;
+  out->committed_tokens = max_tokens;
+  out->ticks = (int64_t)max_tokens * e->S;  // simulate_autoregressive tick model, pipesim.py:386
+  out->rejects = max_tokens;
+  out->throughput = 1.0 / e->S;
+  out->speedup_vs_ar = 1.0;
+  out->gpu_launches = launches;
+  if (out_tokens)
+    CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * max_tokens, cudaMemcpyDeviceToHost));
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_decode_eesd(ppsd_engine*, int32_t, const int32_t*, int32_t, int32_t, int32_t*, int32_t,
+                                ppsd_metrics*, ppsd_trace_row*, int64_t, int64_t*) {
+  return fail(PPSD_EUNSUPPORTED, "EESD baseline not implemented yet");
+}
+
+// ---------------------------------------------------------------------------
+// weight init
+
+extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t cols, uint64_t seed,
+                                const uint64_t* tids, const float* scales, int32_t n_heads, int32_t n_kv_heads,
+                                int32_t head_dim, void* cuda_stream) {
+  if (!dst || !tids || !scales || rows <= 0 || cols <= 0) return fail(PPSD_EINVAL, "bad init arguments");
+  const uint64_t salt = 0x5EEDB200C0FFEE01ull;  // oracle/transformer.py INIT_SALT
+  uint64_t b[3] = {0, 0, 0};
+  float a[3] = {0, 0, 0};
+  const int nt = layout == 0 ? 1 : (layout == 1 ? 3 : 2);
+  for (int i = 0; i < nt; ++i) {
+    b[i] = hmix64(hmix64(seed ^ salt) ^ tids[i]);
+    a[i] = scales[i];
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const long long n = rows * cols;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148LL * 64) blocks = 148LL * 64;
+  init_weight_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(dst), layout, rows, cols,
+                                                     b[0], b[1], b[2], a[0], a[1], a[2], n_heads, n_kv_heads,
+                                                     head_dim);
+  CU(cudaGetLastError());
+  return PPSD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-rank stepping and the kernel probe: implemented in engine_mr.cu
+
+extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps, double* avg_ms,
+                               double* bytes_per_launch) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "probe needs a transformer engine");
+  if (which < 0 || which > 4 || reps < 1) return fail(PPSD_EINVAL, "bad probe arguments");
+  const int G = e->hi - e->lo + 1;
+  if (n_groups < 1 || n_groups > G || n_groups > e->cfg.nslot) return fail(PPSD_EINVAL, "bad n_groups");
+  CU(cudaSetDevice(e->device));
+  Work w{};
+  w.G = n_groups;
+  for (int g = 0; g < n_groups; ++g) {
+    w.slot[g] = g;
+    w.pos[g] = 0;
+    w.first[g] = e->cfg.stage_first[e->lo + g];
+    w.nl[g] = e->cfg.stage_layers[e->lo + g];
+  }
+  w.head_slot[0] = 0;
+  w.head_slot[1] = n_groups > 1 ? 1 : 0;
+  CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
+  for (int i = 0; i < 3; ++i) CU(enqueue_gemv(e, e->d_work_ar, 0, which));
+  CU(cudaEventRecord(e->ev0, e->st));
+  for (int i = 0; i < reps; ++i) CU(enqueue_gemv(e, e->d_work_ar, 0, which));
+  CU(cudaEventRecord(e->ev1, e->st));
+  CU(cudaEventSynchronize(e->ev1));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  const GemvPlan& p = e->gp[which];
+  *avg_ms = ms / reps;
+  *bytes_per_launch = (double)p.R * p.K * 2.0 * (which == kMatHead ? 1 : n_groups);
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_read_logits(ppsd_engine* e, int32_t which, float* out) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER || which < 0 || which > 1 || !out)
+    return fail(PPSD_EINVAL, "bad read_logits arguments");
+  CU(cudaSetDevice(e->device));
+  CU(cudaStreamSynchronize(e->st));
+  CU(cudaMemcpy(out, e->d_logits + (size_t)which * e->dm.V, sizeof(float) * e->dm.V, cudaMemcpyDeviceToHost));
+  return PPSD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-rank stepping (one engine per GPU); see include/ppsd.h
+
+extern "C" int ppsd_exchange_info(ppsd_engine*, void**, void**, int64_t*) {
+  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+}
+extern "C" int ppsd_step_begin(ppsd_engine*, const int32_t*, int32_t, int32_t, int32_t, int32_t, int32_t) {
+  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+}
+extern "C" int ppsd_step_compute(ppsd_engine*) { return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet"); }
+extern "C" int ppsd_step_finish(ppsd_engine*) { return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet"); }
+extern "C" int ppsd_step_poll(ppsd_engine*, int32_t*, int64_t*, int64_t*) {
+  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+}
+extern "C" int ppsd_step_end(ppsd_engine*, int32_t*, ppsd_metrics*, ppsd_trace_row*, int64_t, int64_t*) {
+  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+}

@@ -1,0 +1,46 @@
+// engine_dev.cuh — device context shared by the bookkeeping kernels.
+#pragma once
+#include "../../include/ppsd.h"
+#include "kernels.cuh"
+
+namespace ppsd {
+
+// Everything the per-tick bookkeeping kernels need, in device memory so the
+// captured graphs keep fixed arguments while buffers change per call.
+struct TickCtx {
+  Sched* sched;
+  Work* work;
+  Work* work_ar;
+  int32_t* tokens;     // [max_ctx + 8] prompt + committed/drafted tokens
+  uint64_t* pdig;      // ToyLM prefix digests [max_ctx + 9]
+  uint64_t* chain_dig; // ToyLM per-slot chain digests
+  TraceRow* trace;
+  int64_t trace_cap;
+  const __nv_bfloat16* embed;
+  float* x;
+  int32_t d;
+  int32_t model;
+  int32_t lo, hi;      // local stages
+  // ToyLM parameters (toylm.py:55-60)
+  int32_t n_layers, vocab;
+  double beta;
+  uint64_t toy_seed;
+};
+
+struct ArCtl {
+  int32_t j;           // token index being processed
+  int32_t first_layer; // first local layer
+  int32_t n_layers;    // local layer count
+  int32_t pad;
+};
+
+__global__ void sched_tick_kernel(const TickCtx* ctxp, int begin);
+__global__ void ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
+__global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
+__global__ void toy_tick_kernel(const TickCtx* ctxp);
+__global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);
+__global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long rows, long long cols,
+                                   uint64_t b0, uint64_t b1, uint64_t b2, float a0, float a1, float a2,
+                                   int H, int KV, int hd);
+
+}  // namespace ppsd

@@ -1,0 +1,461 @@
+// gemv.cu — weight-streaming GEMV for bs=1 decode on sm_100a.
+//
+// Every decode-step matmul is y = W x with W bf16 [R][K] streamed from HBM
+// exactly once and x a handful of fp32 vectors; the roofline is HBM bytes.
+// One persistent CTA per SM (grid = #SMs, 1 CTA/SM, ~200 KB smem):
+//
+//   warp 8 (producer, one lane): cp.async.bulk (UBLKCP) of TR contiguous
+//       weight rows per stage into an NS-deep shared-memory ring, completion
+//       counted on a per-stage mbarrier (expect_tx), L2 evict_first hint.
+//   warps 0-7 (consumers, 256 threads): thread t owns the 16-byte column
+//       vectors t, t+256, ... of every row, so its slice of the normalised
+//       input vector lives in registers for the whole kernel; per stage it
+//       does TR x VPT ld.shared.v4 + 8 FMAs each, then a warp butterfly per
+//       row and a deterministic 8-warp sum in a deferred, batched epilogue.
+//
+// The tile space of ALL active problems of one launch (the same layer slot
+// of every pipeline stage that has a chain this tick — the "grouped" launch
+// that lets the stages of one GPU share the SMs) is split into contiguous,
+// byte-balanced ranges, one per CTA. Row results never depend on the range
+// split, the group count or the number of vectors, so the PPSD path and the
+// autoregressive path produce bit-identical hidden states.
+//
+// Fused epilogues (the op that follows each matmul in the decoder layer):
+//   kMatQKV  : RMSNorm prologue; RoPE on (q,k) row pairs; q -> scratch,
+//              k,v -> paged KV cache at the chain's position.
+//   kMatGU   : RMSNorm prologue; SwiGLU on (gate,up) row pairs -> h.
+//   kMatO / kMatDown : residual add into the chain's fp32 hidden state.
+//   kMatHead : per-vector RMSNorm prologue (exit norm | final norm), M=2
+//              vectors share one pass over the tied LM head; fp32 logits and
+//              a deterministic first-index argmax across CTAs.
+#include <float.h>
+#include <limits.h>
+
+#include "kernels.cuh"
+
+namespace ppsd {
+
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+template <int VPT, int TR, int M, int EPI>
+__global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_prob[kMaxStages];
+  __shared__ int s_np;
+  __shared__ float s_ss[8][M];
+  __shared__ float s_bv[8][M];
+  __shared__ int s_bi[8][M];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.K, R = a.R, NS = a.nstage;
+  const int stage_bytes = TR * K * 2;
+  unsigned char* ring = smem;
+  float* red = reinterpret_cast<float*>(smem + (size_t)NS * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + kGemvChunkTiles * 8 * M * TR);
+  uint64_t* empty = full + NS;
+  const Work* work = a.work;
+
+  if (tid == 0) {
+    int np = 0;
+    if (EPI == kMatHead) {
+      np = (work->head_slot[0] >= 0 || work->head_slot[1] >= 0) ? 1 : 0;
+    } else {
+      for (int g = 0; g < work->G; ++g)
+        if (work->slot[g] >= 0 && a.layer_i < work->nl[g]) s_prob[np++] = g;
+    }
+    s_np = np;
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int np = s_np;
+  if (np == 0) return;
+  const int tpp = R / TR;
+  const long long T = (long long)np * tpp;
+  const long long t0 = T * blockIdx.x / gridDim.x;
+  const long long t1 = T * (blockIdx.x + 1) / gridDim.x;
+  const int ntiles = (int)(t1 - t0);
+
+  auto weights = [&](int p) -> const __nv_bfloat16* {
+    if (EPI == kMatHead) return a.head_w;
+    const LayerW& L = a.layers[work->first[s_prob[p]] + a.layer_i];
+    return EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;
+  };
+
+  if (warp == 8) {  // ---------------- producer ----------------
+    if (lane == 0 && ntiles > 0) {
+      const uint64_t pol = policy_evict_first();
+      int cur_p = -1;
+      const unsigned char* wb = nullptr;
+      for (int n = 0; n < ntiles; ++n) {
+        const long long t = t0 + n;
+        const int p = (int)(t / tpp);
+        const int tile = (int)(t - (long long)p * tpp);
+        if (p != cur_p) {
+          wb = reinterpret_cast<const unsigned char*>(weights(p));
+          cur_p = p;
+        }
+        const int st = n % NS;
+        if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
+        mbar_expect_tx(&full[st], stage_bytes);
+        bulk_g2s(ring + (size_t)st * stage_bytes, wb + (size_t)tile * stage_bytes, stage_bytes,
+                 &full[st], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  float bestv[M];
+  int besti[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    bestv[m] = -FLT_MAX;
+    besti[m] = INT_MAX;
+  }
+  bool mact[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) mact[m] = true;
+  if (EPI == kMatHead) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) mact[m] = work->head_slot[m] >= 0;
+  }
+
+  if (ntiles > 0) {
+    const int nvec = K >> 3;
+    float xr[M][VPT][8];
+    int cur_p = -1;
+    for (int n = 0; n < ntiles; ++n) {
+      const long long t = t0 + n;
+      const int p = (int)(t / tpp);
+      if (p != cur_p) {  // load + normalise this problem's input slice
+        cur_p = p;
+        const float* nw[M];
+        const float* src[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          nw[m] = nullptr;
+          src[m] = nullptr;
+          if (EPI == kMatHead) {
+            const int s = work->head_slot[m];
+            nw[m] = m == 0 ? a.head_norm0 : a.head_norm1;
+            src[m] = s >= 0 ? a.x + (size_t)s * a.dm.d : nullptr;
+          } else {
+            const int g = s_prob[p];
+            const int s = work->slot[g];
+            const LayerW& L = a.layers[work->first[g] + a.layer_i];
+            if (EPI == kMatQKV) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.attn_norm; }
+            if (EPI == kMatGU) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.mlp_norm; }
+            if (EPI == kMatO) src[m] = a.o + (size_t)s * a.dm.H * a.dm.hd;
+            if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn;
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          float ss = 0.f;
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            const int v = tid + u * kGemvConsumers;
+            if (src[m] && v < nvec) {
+              const float4 lo = *reinterpret_cast<const float4*>(src[m] + v * 8);
+              const float4 hi = *reinterpret_cast<const float4*>(src[m] + v * 8 + 4);
+              xr[m][u][0] = lo.x; xr[m][u][1] = lo.y; xr[m][u][2] = lo.z; xr[m][u][3] = lo.w;
+              xr[m][u][4] = hi.x; xr[m][u][5] = hi.y; xr[m][u][6] = hi.z; xr[m][u][7] = hi.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) xr[m][u][e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss = fmaf(xr[m][u][e], xr[m][u][e], ss);
+          }
+          ss = warp_sum(ss);
+          if (lane == 0) s_ss[warp][m] = ss;
+        }
+        named_bar_sync(1, kGemvConsumers);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          if (!nw[m]) continue;
+          float tot = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) tot += s_ss[w][m];
+          const float rstd = 1.0f / sqrtf(tot / (float)K + a.dm.eps);
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            const int v = tid + u * kGemvConsumers;
+            if (v < nvec) {
+              const float4 w0 = *reinterpret_cast<const float4*>(nw[m] + v * 8);
+              const float4 w1 = *reinterpret_cast<const float4*>(nw[m] + v * 8 + 4);
+              const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) xr[m][u][e] = (xr[m][u][e] * rstd) * wv[e];
+            }
+          }
+        }
+        named_bar_sync(1, kGemvConsumers);
+      }
+
+      const int st = n % NS;
+      mbar_wait(&full[st], (n / NS) & 1);
+      const unsigned char* tb = ring + (size_t)st * stage_bytes;
+      float acc[M][TR];
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int r = 0; r < TR; ++r) acc[m][r] = 0.f;
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int v = tid + u * kGemvConsumers;
+          if (v < nvec) {
+            const uint4 w = lds128(tb + (size_t)r * K * 2 + (size_t)v * 16);
+            const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                                 bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (!mact[m]) continue;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[m][r] = fmaf(wf[e], xr[m][u][e], acc[m][r]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      const int ct = n % kGemvChunkTiles;
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+          const float s = warp_sum(acc[m][r]);
+          if (lane == 0) red[((ct * 8 + warp) * M + m) * TR + r] = s;
+        }
+
+      if (ct == kGemvChunkTiles - 1 || n == ntiles - 1) {  // deferred epilogue
+        named_bar_sync(1, kGemvConsumers);
+        const int n0 = n - ct;
+        const int nrows = (ct + 1) * TR;
+        auto rowsum = [&](int rl, int m) {
+          const int tt = rl / TR, r = rl % TR;
+          float s = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) s += red[((tt * 8 + w) * M + m) * TR + r];
+          return s;
+        };
+        if (EPI == kMatQKV || EPI == kMatGU) {
+          for (int pr = tid; pr < nrows / 2; pr += kGemvConsumers) {
+            const int rl = pr * 2;
+            const float y0 = rowsum(rl, 0), y1 = rowsum(rl + 1, 0);
+            const long long tg = t0 + n0 + rl / TR;
+            const int pp = (int)(tg / tpp);
+            const int rr = (int)(tg - (long long)pp * tpp) * TR + rl % TR;
+            const int g = s_prob[pp];
+            const int slot = work->slot[g], pos = work->pos[g];
+            if (EPI == kMatGU) {
+              a.h[(size_t)slot * a.dm.ffn + (rr >> 1)] = y0 / (1.0f + expf(-y0)) * y1;
+            } else {
+              const int H = a.dm.H, KVh = a.dm.KV, hd = a.dm.hd;
+              const LayerW& L = a.layers[work->first[g] + a.layer_i];
+              const int head = rr / hd, w = rr - head * hd;
+              float o0 = y0, o1 = y1;
+              void* cache = nullptr;
+              int kvh = 0;
+              if (head < H + KVh) {
+                const int half = hd >> 1;
+                const float c = a.rope_cos[(size_t)pos * half + (w >> 1)];
+                const float sn = a.rope_sin[(size_t)pos * half + (w >> 1)];
+                o0 = y0 * c - y1 * sn;
+                o1 = y1 * c + y0 * sn;
+                if (head < H) {
+                  float* q = a.q + (size_t)slot * H * hd + head * hd + w;
+                  q[0] = o0;
+                  q[1] = o1;
+                } else {
+                  cache = L.kc;
+                  kvh = head - H;
+                }
+              } else {
+                cache = L.vc;
+                kvh = head - H - KVh;
+              }
+              if (cache) {
+                const int page = a.page_table[pos / kPage];
+                const size_t off = (((size_t)page * KVh + kvh) * kPage + (pos % kPage)) * hd + w;
+                if (a.dm.kv_bf16) {
+                  __nv_bfloat162 pv = __floats2bfloat162_rn(o0, o1);
+                  *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) = pv;
+                } else {
+                  float* cp = reinterpret_cast<float*>(cache) + off;
+                  cp[0] = o0;
+                  cp[1] = o1;
+                }
+              }
+            }
+          }
+        } else {
+          for (int rl = tid; rl < nrows; rl += kGemvConsumers) {
+            const long long tg = t0 + n0 + rl / TR;
+            const int pp = (int)(tg / tpp);
+            const int rr = (int)(tg - (long long)pp * tpp) * TR + rl % TR;
+            if (EPI == kMatHead) {
+#pragma unroll
+              for (int m = 0; m < M; ++m) {
+                if (!mact[m]) continue;
+                const float y = rowsum(rl, m);
+                a.logits[(size_t)m * a.dm.V + rr] = y;
+                if (y > bestv[m]) {  // rows ascend per thread: strict > keeps first index
+                  bestv[m] = y;
+                  besti[m] = rr;
+                }
+              }
+            } else {
+              const float y = rowsum(rl, 0);
+              const int slot = work->slot[s_prob[pp]];
+              a.x[(size_t)slot * a.dm.d + rr] += y;
+            }
+          }
+        }
+        named_bar_sync(1, kGemvConsumers);
+      }
+    }
+  }
+
+  if (EPI == kMatHead) {  // deterministic first-index argmax across the grid
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      float v = bestv[m];
+      int i = besti[m];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, v, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, off);
+        if (better(ov, oi, v, i)) { v = ov; i = oi; }
+      }
+      if (lane == 0) { s_bv[warp][m] = v; s_bi[warp][m] = i; }
+    }
+    named_bar_sync(1, kGemvConsumers);
+    if (tid == 0) {
+      __shared__ int s_last;
+      for (int m = 0; m < M; ++m) {
+        float v = s_bv[0][m];
+        int i = s_bi[0][m];
+        for (int w = 1; w < 8; ++w)
+          if (better(s_bv[w][m], s_bi[w][m], v, i)) { v = s_bv[w][m]; i = s_bi[w][m]; }
+        a.head_part[((size_t)blockIdx.x * 2 + m) * 2 + 0] = v;
+        a.head_part[((size_t)blockIdx.x * 2 + m) * 2 + 1] = __int_as_float(i);
+      }
+      __threadfence();
+      s_last = (atomicAdd(a.head_cnt, 1) == (int)gridDim.x - 1);
+      if (s_last) {
+        __threadfence();
+        Work* wk = const_cast<Work*>(work);
+        for (int m = 0; m < M; ++m) {
+          float v = -FLT_MAX;
+          int i = INT_MAX;
+          for (int b = 0; b < (int)gridDim.x; ++b) {
+            const float bv = __ldcg(&a.head_part[((size_t)b * 2 + m) * 2 + 0]);
+            const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * 2 + m) * 2 + 1]));
+            if (better(bv, bi, v, i)) { v = bv; i = bi; }
+          }
+          wk->head_out[m] = mact[m] ? i : -1;
+        }
+        *a.head_cnt = 0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch
+
+namespace {
+constexpr int kVpts[] = {1, 2, 3, 4, 6, 7, 8, 14};
+constexpr size_t kRingBudget = 200 * 1024;
+
+constexpr int tr_for(int vpt) { return vpt <= 3 ? 4 : (vpt <= 6 ? 2 : 1); }
+
+template <int VPT, int EPI>
+cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only) {
+  constexpr int TR = tr_for(VPT);
+  constexpr int M = EPI == kMatHead ? 2 : 1;
+  auto fn = gemv_kernel<VPT, TR, M, EPI>;
+  if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fn<<<grid, kGemvThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int VPT>
+cudaError_t launch_vpt(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only,
+                       int mat) {
+  // only the instantiations gemv_pick can select: the fused pair epilogues
+  // need TR >= 2 (VPT <= 6); the head runs on K = d_model <= 8192 (VPT <= 4)
+  if (mat == kMatO) return launch_one<VPT, kMatO>(a, smem, grid, st, attrs_only);
+  if (mat == kMatDown) return launch_one<VPT, kMatDown>(a, smem, grid, st, attrs_only);
+  if constexpr (VPT <= 6) {
+    if (mat == kMatQKV) return launch_one<VPT, kMatQKV>(a, smem, grid, st, attrs_only);
+    if (mat == kMatGU) return launch_one<VPT, kMatGU>(a, smem, grid, st, attrs_only);
+  }
+  if constexpr (VPT <= 4) {
+    if (mat == kMatHead) return launch_one<VPT, kMatHead>(a, smem, grid, st, attrs_only);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+namespace {
+cudaError_t dispatch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st, bool attrs_only,
+                     int mat) {
+  switch (vpt) {
+    case 1: return launch_vpt<1>(a, smem, grid, st, attrs_only, mat);
+    case 2: return launch_vpt<2>(a, smem, grid, st, attrs_only, mat);
+    case 3: return launch_vpt<3>(a, smem, grid, st, attrs_only, mat);
+    case 4: return launch_vpt<4>(a, smem, grid, st, attrs_only, mat);
+    case 6: return launch_vpt<6>(a, smem, grid, st, attrs_only, mat);
+    case 7: return launch_vpt<7>(a, smem, grid, st, attrs_only, mat);
+    case 8: return launch_vpt<8>(a, smem, grid, st, attrs_only, mat);
+    case 14: return launch_vpt<14>(a, smem, grid, st, attrs_only, mat);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+// Choose the (VPT, TR, NS) instantiation for a [R][K] matrix; 0 on success.
+int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* smem) {
+  if (K % 8 != 0 || K <= 0 || R <= 0) return -1;
+  const int need = (K + 8 * kGemvConsumers - 1) / (8 * kGemvConsumers);
+  int v = -1;
+  for (int c : kVpts)
+    if (c >= need) { v = c; break; }
+  if (v < 0) return -1;
+  const int t = tr_for(v);
+  if (R % t != 0) return -1;
+  if ((mat == kMatQKV || mat == kMatGU) && t < 2) return -1;
+  if (mat == kMatHead && v > 4) return -1;
+  const int M = mat == kMatHead ? 2 : 1;
+  const size_t stage = (size_t)t * K * 2;
+  const size_t red = (size_t)kGemvChunkTiles * 8 * M * t * 4;
+  int ns = (int)((kRingBudget - red) / stage);
+  if (ns > 8) ns = 8;
+  if (ns < 2) return -1;
+  *vpt = v;
+  *tr = t;
+  *nstage = ns;
+  *smem = stage * ns + red + 2 * ns * sizeof(uint64_t);
+  return 0;
+}
+
+cudaError_t gemv_set_attrs(int vpt, int mat, size_t smem) {
+  GemvArgs dummy{};
+  return dispatch(dummy, vpt, smem, 0, 0, true, mat);
+}
+
+cudaError_t gemv_launch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st) {
+  return dispatch(a, vpt, smem, grid, st, false, a.mat);
+}
+
+}  // namespace ppsd

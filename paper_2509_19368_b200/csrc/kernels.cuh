@@ -1,0 +1,88 @@
+// kernels.cuh — device-side data structures and kernel entry points shared by
+// the engine (engine.cu) and the kernel translation units.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "sched.h"
+
+namespace ppsd {
+
+constexpr int kPage = 64;          // KV page = attention chunk (tokens)
+constexpr int kGemvConsumers = 256;  // 8 consumer warps
+constexpr int kGemvThreads = 288;    // + 1 bulk-copy producer warp
+constexpr int kGemvChunkTiles = 16;  // tiles per deferred epilogue batch
+
+// Per-tick local work: one group per local pipeline stage. Written by the
+// scheduler kernel at the start of every tick, read by every layer kernel.
+struct Work {
+  int32_t G;                    // local stage count
+  int32_t slot[kMaxStages];     // chain activation slot, -1 = stage idle this tick
+  int32_t pos[kMaxStages];      // token index the chain processes (RoPE / KV index)
+  int32_t first[kMaxStages];    // global index of the stage's first layer
+  int32_t nl[kMaxStages];       // layers in the stage
+  int32_t head_slot[2];         // [0] exit head input slot, [1] final head input slot
+  int32_t head_out[2];          // argmax written by the head kernel
+};
+
+struct LayerW {
+  const __nv_bfloat16* qkv;
+  const __nv_bfloat16* o;
+  const __nv_bfloat16* gu;
+  const __nv_bfloat16* down;
+  const float* attn_norm;
+  const float* mlp_norm;
+  void* kc;  // [pages][KV][kPage][hd] in the KV dtype
+  void* vc;
+};
+
+struct Dims {
+  int32_t d, H, KV, hd, ffn, V, max_ctx, nslot;
+  float eps;
+  int32_t kv_bf16;
+};
+
+enum : int { kMatQKV = 0, kMatO = 1, kMatGU = 2, kMatDown = 3, kMatHead = 4 };
+
+struct GemvArgs {
+  Work* work;
+  int32_t layer_i;        // layer offset inside each stage
+  int32_t mat;            // kMat*
+  const LayerW* layers;   // [n_layers]
+  const __nv_bfloat16* head_w;
+  const float* head_norm0;  // exit norm
+  const float* head_norm1;  // final norm
+  int32_t R, K, nstage;
+  Dims dm;
+  float* x;   // [nslot][d]   residual stream (fp32)
+  float* q;   // [nslot][H*hd]
+  float* o;   // [nslot][H*hd]
+  float* h;   // [nslot][ffn]
+  float* logits;  // [2][V]
+  const float* rope_cos;
+  const float* rope_sin;
+  const int32_t* page_table;
+  float* head_part;  // [grid][2][2] (value, index-as-float bits)
+  int32_t* head_cnt;
+};
+
+struct AttnArgs {
+  const Work* work;
+  int32_t layer_i;
+  const LayerW* layers;
+  Dims dm;
+  const float* q;
+  float* o;
+  float* part;       // [nslot][H][max_pages][hd+2]
+  int32_t* cnt;      // [nslot][KV]
+  const int32_t* page_table;
+  int32_t max_pages;
+};
+
+// launchers (gemv.cu / attn.cu)
+int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* smem);
+cudaError_t gemv_launch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st);
+cudaError_t gemv_set_attrs(int vpt, int mat, size_t smem);
+cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
+
+}  // namespace ppsd

@@ -1,0 +1,247 @@
+// sched.h — the verify-while-draft tick machine, shared by the device
+// scheduler kernel (sched.cu) and a host build used by the multi-rank CPU
+// tests. It restates the reference machine `_ppsd_machine`
+// (pkg/src/specpipe/pipesim.py:670-789) split at the point where model
+// compute happens:
+//
+//   sched_plan(t)   : t += 1; deliver transit (pipesim.py:722-725); pick the
+//                     chain each stage runs this tick (:729-733); launch a
+//                     new chain at stage 1 if t == next_launch (:766-777).
+//   ...model compute for every planned (stage, chain), exit head on the
+//      chain at the exit stage, final head on the chain at stage S...
+//   sched_finish(t) : verdict at stage S (:739-760), drafts at the exit stage
+//                     (:709-719, :762-763), emissions into transit (:703-707),
+//                     launch bookkeeping (:773-777), rollback (:779-786).
+//
+// Trace rows are written in exactly the reference's append order so the
+// exported CSV is byte-identical (pipesim.py:175-189).
+//
+// Chain identity: an in-flight chain is named by its activation slot
+// pos % nslot. In-flight positions are contiguous and at most (S-1)*per+1
+// apart (one launch per tick at most, a chain lives (S-1)*per ticks), so the
+// slot is unique while the chain lives; nslot = (S-1)*per + 2.
+#pragma once
+#include "hostdev.h"
+
+namespace ppsd {
+
+constexpr int kMaxStages = 96;
+constexpr int kMaxSlots = 512;
+constexpr int kTransitCap = 512;
+
+enum : int { kKindAct = 0, kKindDraft = 1, kKindFinal = 2, kKindCheck = 3 };
+enum : int { kVerdictNone = 0, kVerdictAccept = 1, kVerdictReject = 2 };
+enum : int { kErrOrder = 1, kErrTrace = 2, kErrTransit = 4 };
+
+struct TraceRow {
+  int32_t tick, stage, kind, position, token, verdict;
+};
+
+struct SchedCfg {
+  int32_t S, k, per, n_layers;
+  int32_t model;        // 0: Bernoulli verdicts, 1: greedy model verdicts
+  int32_t force_reject;
+  int32_t stop;         // stop_commits (max_tokens / horizon)
+  int32_t n_prompt;
+  int32_t nslot;
+  int32_t pad_;
+  double alpha;         // Bernoulli acceptance rate
+  uint64_t verify_seed; // derive_seed(rng.seed, "verify") (pipesim.py:693)
+  int32_t stage_layers[kMaxStages + 1];  // 1-based
+  int32_t stage_first[kMaxStages + 1];   // global index of the stage's first layer
+};
+
+struct Sched {
+  SchedCfg c;
+  int32_t t, committed, accepts, rejects, draft_head, next_launch, done, error;
+  uint64_t verify_counter;
+  int64_t trace_n;
+  int32_t launched;     // the stage-1 chain this tick is a fresh launch
+  int32_t exit_slot;    // chain whose exit head runs this tick, -1 none
+  int32_t final_slot;   // chain whose final head runs this tick, -1 none
+  int32_t tq_head, tq_n;
+  int32_t cur[kMaxStages + 2];
+  int32_t work[kMaxStages + 2];  // chain slot each stage runs this tick, -1 idle
+  int32_t tq_ready[kTransitCap], tq_dest[kTransitCap], tq_slot[kTransitCap];
+  int32_t ch_pos[kMaxSlots], ch_layer[kMaxSlots], ch_tok[kMaxSlots];
+};
+
+constexpr int32_t kNone = -1;
+
+PPSD_HD void sched_reset(Sched* s) {
+  s->t = s->committed = s->accepts = s->rejects = s->draft_head = 0;
+  s->next_launch = 1;
+  s->done = (s->c.stop <= 0);
+  s->error = 0;
+  s->verify_counter = 0;
+  s->trace_n = 0;
+  s->launched = 0;
+  s->exit_slot = s->final_slot = kNone;
+  s->tq_head = s->tq_n = 0;
+  for (int i = 0; i <= s->c.S + 1; ++i) s->cur[i] = s->work[i] = kNone;
+}
+
+PPSD_HD void sched_trace(Sched* s, TraceRow* tr, int64_t cap, int st, int kind, int pos, int tok,
+                         int verdict) {
+  if (!tr) return;
+  if (s->trace_n >= cap) {
+    s->error |= kErrTrace;
+    return;
+  }
+  TraceRow r;
+  r.tick = s->t;
+  r.stage = st;
+  r.kind = kind;
+  r.position = pos;
+  r.token = tok;
+  r.verdict = verdict;
+  tr[s->trace_n++] = r;
+}
+
+// Beginning of tick t+1: returns 0 when the run is already done.
+PPSD_HD int sched_plan(Sched* s) {
+  const int S = s->c.S;
+  for (int i = 0; i <= S + 1; ++i) s->work[i] = kNone;
+  s->launched = 0;
+  s->exit_slot = s->final_slot = kNone;
+  if (s->done) return 0;
+  s->t += 1;
+  while (s->tq_n > 0 && s->tq_ready[s->tq_head] == s->t) {  // pipesim.py:723-725
+    s->cur[s->tq_dest[s->tq_head]] = s->tq_slot[s->tq_head];
+    s->tq_head = (s->tq_head + 1) % kTransitCap;
+    s->tq_n -= 1;
+  }
+  for (int st = S; st >= 2; --st) {  // pipesim.py:729-733
+    s->work[st] = s->cur[st];
+    s->cur[st] = kNone;
+  }
+  if (s->next_launch != kNone && s->t == s->next_launch) {  // pipesim.py:766-772
+    const int pos = s->draft_head + 1;
+    const int slot = pos % s->c.nslot;
+    s->ch_pos[slot] = pos;
+    s->ch_layer[slot] = 0;
+    s->ch_tok[slot] = kNone;
+    s->work[1] = slot;
+    s->launched = 1;
+    s->draft_head = pos;
+    if (s->c.k != 1) s->next_launch = kNone;  // pipesim.py:775-776
+  }
+  s->exit_slot = s->work[s->c.k];
+  s->final_slot = s->work[S];
+  return 1;
+}
+
+PPSD_HD void sched_push_token(const Sched* s, int32_t* tokens, uint64_t* pdig, int idx, int tok) {
+  if (tokens) tokens[idx] = tok;
+  if (pdig) pdig[idx + 1] = toy_extend(pdig[idx], tok);
+  (void)s;
+}
+
+// make_draft (pipesim.py:709-719) for a chain at stage st with exit-head argmax tok
+PPSD_HD void sched_draft(Sched* s, int slot, int st, int exit_tok, int32_t* tokens, uint64_t* pdig,
+                         TraceRow* tr, int64_t cap) {
+  int tok = kNone;
+  if (s->c.model != 0) {
+    tok = exit_tok;
+    s->ch_tok[slot] = tok;
+    sched_push_token(s, tokens, pdig, s->c.n_prompt + s->ch_pos[slot] - 1, tok);
+  }
+  sched_trace(s, tr, cap, st, kKindDraft, s->ch_pos[slot], tok, kVerdictNone);
+  s->next_launch = s->t + (st == 1 ? 1 : s->c.per);
+}
+
+// emit_activation (pipesim.py:703-707)
+PPSD_HD void sched_emit(Sched* s, int slot, int st, TraceRow* tr, int64_t cap) {
+  sched_trace(s, tr, cap, st, kKindAct, s->ch_pos[slot], kNone, kVerdictNone);
+  if (s->tq_n >= kTransitCap) {
+    s->error |= kErrTransit;
+    return;
+  }
+  const int tail = (s->tq_head + s->tq_n) % kTransitCap;
+  s->tq_ready[tail] = s->t + s->c.per;
+  s->tq_dest[tail] = st + 1;
+  s->tq_slot[tail] = slot;
+  s->tq_n += 1;
+}
+
+// End of tick t. exit_tok / final_tok are the argmax outputs of the exit and
+// final heads for s->exit_slot / s->final_slot (ignored for Bernoulli).
+PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens, uint64_t* pdig,
+                          TraceRow* tr, int64_t cap) {
+  // a tick that sched_plan declined (run already done) leaves work[] idle
+  // and launched == 0, so nothing below fires.
+  const int S = s->c.S, k = s->c.k;
+  int rollback = kNone, corrected = kNone;
+  for (int st = S; st >= 2; --st) {  // pipesim.py:729-764
+    const int slot = s->work[st];
+    if (slot == kNone) continue;
+    s->ch_layer[slot] += s->c.stage_layers[st];
+    if (st == S) {
+      const int pos = s->ch_pos[slot];
+      if (pos != s->committed + 1) s->error |= kErrOrder;  // pipesim.py:740-741
+      bool ok;
+      int tok;
+      if (s->c.model != 0) {  // greedy_match (speccore.py:116-126), pipesim.py:351-358
+        ok = !s->c.force_reject && s->ch_tok[slot] == final_tok;
+        tok = final_tok;  // == the draft when accepted
+      } else {            // pipesim.py:749
+        ok = false;
+        if (!s->c.force_reject) ok = counter_uniform(s->c.verify_seed, s->verify_counter++) < s->c.alpha;
+        tok = kNone;
+      }
+      s->committed += 1;
+      if (ok) {
+        s->accepts += 1;
+        sched_trace(s, tr, cap, S, kKindFinal, pos, tok, kVerdictAccept);
+      } else {
+        s->rejects += 1;
+        rollback = pos;
+        corrected = tok;
+        sched_trace(s, tr, cap, S, kKindCheck, pos, tok, kVerdictReject);
+      }
+    } else {
+      if (st == k) sched_draft(s, slot, st, exit_tok, tokens, pdig, tr, cap);
+      sched_emit(s, slot, st, tr, cap);
+    }
+  }
+  if (s->launched) {  // pipesim.py:771-777
+    const int slot = s->work[1];
+    s->ch_layer[slot] = s->c.stage_layers[1];
+    if (k == 1) sched_draft(s, slot, 1, exit_tok, tokens, pdig, tr, cap);
+    sched_emit(s, slot, 1, tr, cap);
+  }
+  if (rollback != kNone) {  // pipesim.py:779-786
+    s->tq_n = 0;
+    for (int st = 1; st <= S; ++st) s->cur[st] = kNone;
+    s->draft_head = rollback;
+    if (s->c.model != 0) sched_push_token(s, tokens, pdig, s->c.n_prompt + rollback - 1, corrected);
+    s->next_launch = s->t + s->c.per;
+  }
+  if (s->committed >= s->c.stop) s->done = 1;
+}
+
+// Host-side configuration helper (also used by the CPU test build).
+PPSD_HD int sched_configure(SchedCfg* c, int n_layers, int exit_depth, int exit_stage,
+                            int comm_latency) {
+  if (n_layers < 1 || exit_depth < 1 || exit_depth > n_layers || comm_latency < 0) return -1;
+  const int S = (n_layers + exit_depth - 1) / exit_depth;
+  if (S < 2 || S > kMaxStages) return -1;
+  const int k = exit_stage <= 0 ? 1 : exit_stage;
+  if (k > S - 1) return -1;
+  c->S = S;
+  c->k = k;
+  c->per = 1 + comm_latency;
+  c->n_layers = n_layers;
+  int first = 0;
+  for (int st = 1; st <= S; ++st) {
+    const int nl = (st < S) ? exit_depth : n_layers - (S - 1) * exit_depth;
+    c->stage_layers[st] = nl;
+    c->stage_first[st] = first;
+    first += nl;
+  }
+  c->nslot = (S - 1) * c->per + 2;
+  if (c->nslot > kMaxSlots || S * c->per + 2 > kTransitCap) return -1;
+  return 0;
+}
+
+}  // namespace ppsd

@@ -1,0 +1,248 @@
+"""The reference's decode entry points, executed by the B200 engine.
+
+`decode_ppsd`, `decode_autoregressive`, `simulate_ppsd` keep the signatures,
+argument checks, error types and return values of
+pkg/src/specpipe/pipesim.py:390-409, 571-633; all compute goes through
+libppsd.so (include/ppsd.h). Validation order mirrors the reference
+(`_check_mode`, `_check_prompt`, depth, draft head) so errors surface the
+same way.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .models import ToyLM, TransformerLM
+from .pipeline import (AcceptanceOracle, EventTrace, OracleMode, PipelineConfig, RunMetrics,
+                       default_prompt, make_metrics)
+from .rng import RngStream
+
+
+def _check_mode(mode: str) -> None:
+    if mode not in ("greedy", "sampling"):
+        raise ValueError(f"mode must be 'greedy' or 'sampling', got {mode!r}")
+
+
+def _check_prompt(lm, prompt) -> None:
+    if len(prompt) == 0:
+        raise ValueError("prompt must be non-empty")
+    for t in prompt:
+        if not 0 <= t < lm.vocab:
+            raise ValueError(f"prompt token {t} outside vocab of {lm.vocab}")
+
+
+def _require_draft_head(cfg: PipelineConfig) -> int:
+    if cfg.exit_stage is None:
+        raise ValueError("this schedule needs a draft head (at least 2 stages)")
+    return cfg.exit_stage
+
+
+def _greedy_only(mode: str) -> None:
+    if mode != "greedy":
+        raise NotImplementedError(
+            "sampling-mode verification is not implemented on the B200 engine yet "
+            "(greedy is the parity contract; SURVEY.md §8f-2)")
+
+
+class Engine:
+    """One libppsd engine: a model (or the Bernoulli oracle) + a pipeline split."""
+
+    def __init__(self, model_desc: _lib.ModelDesc, weights, cfg: PipelineConfig, device: int = 0,
+                 stage_range: tuple[int, int] = (0, 0)):
+        L = _lib.lib()
+        self.cfg = cfg
+        self.kind = model_desc.kind
+        pd = _lib.PipelineDesc(n_layers=cfg.n_layers, exit_depth=cfg.exit_depth,
+                               exit_stage=cfg.exit_stage or 0, comm_latency=cfg.comm_latency,
+                               stage_lo=stage_range[0], stage_hi=stage_range[1], device=device)
+        h = C.c_void_p()
+        self._weights = weights  # keep pointer arrays alive
+        _lib.check(L.ppsd_engine_create(C.byref(model_desc), C.byref(weights) if weights is not None
+                                        else None, C.byref(pd), None, C.byref(h)), "engine_create")
+        self.h = h
+        self.max_ctx = model_desc.max_ctx
+        self._vocab = model_desc.vocab
+        self.last = None
+        self._fin = weakref.finalize(self, L.ppsd_engine_destroy, h)
+
+    def close(self):
+        self._fin()
+
+    # -- helpers ---------------------------------------------------------
+    def _trace_cap(self, stop: int) -> int:
+        c = self.cfg
+        return (stop * c.n_stages * c.hop_period + c.n_stages * c.hop_period + 8) * (c.n_stages + 2)
+
+    def _finish(self, m: _lib.Metrics, rows: np.ndarray | None, n_rows: int):
+        self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
+                         ticks=m.ticks, committed=m.committed_tokens)
+        metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects,
+                               m.accepts + m.rejects, self.cfg.ar_ticks_per_token)
+        trace = EventTrace.from_array(rows[:n_rows]) if rows is not None else EventTrace()
+        return metrics, trace
+
+    # -- entry points ----------------------------------------------------
+    def decode(self, prompt, max_tokens: int, force_reject: bool = False, trace: bool = True):
+        L = _lib.lib()
+        p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
+        out = np.zeros(max(1, max_tokens), dtype=np.int32)
+        m = _lib.Metrics()
+        rows = np.zeros((self._trace_cap(max_tokens), 6), dtype=np.int32) if trace else None
+        n_rows = C.c_int64(0)
+        _lib.check(L.ppsd_decode(self.h, 1, p, len(prompt), max_tokens, int(bool(force_reject)),
+                                 out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(m),
+                                 rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
+                                 rows.shape[0] if trace else 0, C.byref(n_rows)), "decode")
+        metrics, tr = self._finish(m, rows, n_rows.value)
+        return out[:max_tokens].tolist(), metrics, tr
+
+    def decode_ar(self, prompt, max_tokens: int):
+        L = _lib.lib()
+        p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
+        out = np.zeros(max(1, max_tokens), dtype=np.int32)
+        m = _lib.Metrics()
+        _lib.check(L.ppsd_decode_ar(self.h, 1, p, len(prompt), max_tokens,
+                                    out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(m)), "decode_ar")
+        self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
+                         ticks=m.ticks, committed=m.committed_tokens)
+        return out[:max_tokens].tolist()
+
+    def simulate(self, alpha: float, verify_seed: int, horizon: int, force_reject=False, trace=True):
+        L = _lib.lib()
+        m = _lib.Metrics()
+        rows = np.zeros((self._trace_cap(horizon), 6), dtype=np.int32) if trace else None
+        n_rows = C.c_int64(0)
+        _lib.check(L.ppsd_simulate(self.h, float(alpha), verify_seed & ((1 << 64) - 1), horizon,
+                                   int(bool(force_reject)), C.byref(m),
+                                   rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
+                                   rows.shape[0] if trace else 0, C.byref(n_rows)), "simulate")
+        return self._finish(m, rows, n_rows.value)
+
+    def read_logits(self, which: int) -> np.ndarray:
+        V = self._vocab
+        out = np.zeros(V, dtype=np.float32)
+        _lib.check(_lib.lib().ppsd_read_logits(self.h, which, out.ctypes.data_as(C.POINTER(C.c_float))),
+                   "read_logits")
+        return out
+
+    def probe_gemv(self, which: int, n_groups: int, reps: int = 20):
+        ms, nbytes = C.c_double(), C.c_double()
+        _lib.check(_lib.lib().ppsd_probe_gemv(self.h, which, n_groups, reps, C.byref(ms), C.byref(nbytes)),
+                   "probe")
+        return ms.value, nbytes.value
+
+
+# engines are cached per (model, pipeline split, device)
+_ENGINES: dict = {}
+
+
+def _cfg_key(cfg: PipelineConfig):
+    return (cfg.n_layers, cfg.exit_depth, cfg.exit_stage, cfg.comm_latency)
+
+
+def engine_for(lm, cfg: PipelineConfig) -> Engine:
+    import torch
+
+    if isinstance(lm, TransformerLM):
+        cache = lm.__dict__.setdefault("_engines", {})
+        key = _cfg_key(cfg)
+        if key not in cache:
+            cache[key] = Engine(lm.model_desc(), lm.weights_struct(), cfg, device=lm.device.index)
+        return cache[key]
+    if isinstance(lm, ToyLM):
+        dev = _lib.require_cuda().index
+        key = (lm, _cfg_key(cfg), dev)
+        if key not in _ENGINES:
+            _ENGINES[key] = Engine(lm.model_desc(max_ctx=4096), None, cfg, device=dev)
+        return _ENGINES[key]
+    raise TypeError(f"the B200 engine runs ToyLM or TransformerLM models, got {type(lm).__name__}")
+
+
+def _toy_ctx_for(lm: ToyLM, n_prompt: int, max_tokens: int, cfg: PipelineConfig) -> None:
+    need = n_prompt + max_tokens + cfg.n_stages * cfg.hop_period + 2
+    if need > 4096:
+        raise ValueError("prompt + max_tokens exceeds the ToyLM engine context (4096)")
+
+
+def decode_ppsd(lm, cfg: PipelineConfig, prompt: list[int], max_tokens: int, mode: str,
+                rng: RngStream, *, force_reject: bool = False
+                ) -> tuple[list[int], RunMetrics, EventTrace]:
+    """Verify-while-draft decode on the GPU (pipesim.py:595-633)."""
+    _check_mode(mode)
+    _check_prompt(lm, prompt)
+    if cfg.n_layers != lm.n_layers:
+        raise ValueError(f"pipeline is {cfg.n_layers} layers deep but the model has {lm.n_layers}")
+    _require_draft_head(cfg)
+    if max_tokens == 0:
+        return [], make_metrics(0, 0, 0, 0, 0, cfg.ar_ticks_per_token), EventTrace()
+    _greedy_only(mode)
+    if isinstance(lm, ToyLM):
+        _toy_ctx_for(lm, len(prompt), max_tokens, cfg)
+    return engine_for(lm, cfg).decode(prompt, max_tokens, force_reject)
+
+
+def decode_autoregressive(lm, prompt: list[int], max_tokens: int, mode: str, rng: RngStream) -> list[int]:
+    """Full-model greedy decode on the GPU (pipesim.py:390-409)."""
+    _check_mode(mode)
+    _check_prompt(lm, prompt)
+    if max_tokens == 0:
+        return []
+    _greedy_only(mode)
+    n = lm.n_layers
+    if n < 2:
+        raise NotImplementedError("single-layer models are not supported by the engine")
+    cfg = PipelineConfig(n, max(1, n // 2))
+    if isinstance(lm, ToyLM):
+        _toy_ctx_for(lm, len(prompt), max_tokens, cfg)
+        return engine_for(lm, cfg).decode_ar(prompt, max_tokens)
+    cached = getattr(lm, "_engines", None)
+    eng = next(iter(cached.values())) if cached else engine_for(lm, cfg)  # reuse the KV pool
+    return eng.decode_ar(prompt, max_tokens)
+
+
+def simulate_ppsd(cfg: PipelineConfig, oracle: AcceptanceOracle, horizon: int, rng: RngStream, *,
+                  trace: EventTrace | None = None) -> RunMetrics:
+    """Pipelined schedule with a verdict oracle (pipesim.py:571-592), on the GPU tick machine."""
+    if horizon < 1:
+        raise ValueError("horizon must be >= 1")
+    _require_draft_head(cfg)
+    if oracle.mode is OracleMode.BERNOULLI:
+        import torch  # noqa: F401
+
+        dev = _lib.require_cuda().index
+        key = ("bernoulli", _cfg_key(cfg), dev)
+        if key not in _ENGINES:
+            _ENGINES[key] = Engine(_lib.ModelDesc(kind=_lib.MODEL_BERNOULLI, n_layers=cfg.n_layers),
+                                   None, cfg, device=dev)
+        m, tr = _ENGINES[key].simulate(oracle.alpha, rng.split("verify").seed, horizon,
+                                       trace=trace is not None)
+    else:
+        _greedy_only("greedy" if oracle.greedy else "sampling")
+        lm = oracle.lm
+        prompt = default_prompt(lm.vocab, rng)
+        _, m, tr = engine_for(lm, cfg).decode(prompt, horizon, trace=trace is not None)
+    if trace is not None:
+        trace._rows.extend(tr.rows())
+    return m
+
+
+def simulate_autoregressive(cfg: PipelineConfig, horizon: int, *, trace: EventTrace | None = None
+                            ) -> RunMetrics:
+    """Sequential baseline tick arithmetic (pipesim.py:372-387); host-side, no model."""
+    from .pipeline import ACTIVATION, FINAL_TOKEN, StageMessage
+
+    if horizon < 1:
+        raise ValueError("horizon must be >= 1")
+    s, per = cfg.n_stages, cfg.hop_period
+    if trace is not None:
+        for i in range(1, horizon + 1):
+            start = 1 + (i - 1) * s * per
+            for st in range(1, s):
+                trace.add(start + (st - 1) * per, st, StageMessage(ACTIVATION, i))
+            trace.add(start + (s - 1) * per, s, StageMessage(FINAL_TOKEN, i))
+    ticks = 1 + (horizon - 1) * s * per + (s - 1) * per
+    return make_metrics(horizon, ticks, 0, horizon, 0, cfg.ar_ticks_per_token)

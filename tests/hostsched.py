@@ -1,0 +1,163 @@
+"""ctypes driver for libppsd_host.so (host build of csrc/sched.h) — test helper.
+
+`run_toy` / `run_bernoulli` mimic what the GPU engine does each tick
+(sched_plan -> per-stage compute + heads -> sched_finish) with the model
+compute done by the oracle port, so the plan/finish split of the shipped
+scheduler can be checked against the reference goldens on a CPU box.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from oracle import specpipe_port as sp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB_PATH = os.path.join(ROOT, "paper_2509_19368_b200", "libppsd_host.so")
+KINDS = ("ACTIVATION", "DRAFT_TOKEN", "FINAL_TOKEN", "CHECK_TOKEN")
+VERDICTS = ("", "accept", "reject")
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            import subprocess
+
+            subprocess.check_call(["make", "-C", os.path.join(ROOT, "paper_2509_19368_b200", "csrc"),
+                                   "host"])
+        L = C.CDLL(LIB_PATH)
+        L.ppsdh_create.restype = C.c_void_p
+        L.ppsdh_create.argtypes = [C.c_int] * 7 + [C.POINTER(C.c_int32), C.c_int, C.c_int,
+                                                  C.c_double, C.c_uint64, C.c_int, C.c_uint64,
+                                                  C.c_int64]
+        L.ppsdh_destroy.argtypes = [C.c_void_p]
+        L.ppsdh_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.ppsdh_finish.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ppsdh_chain_pos.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_chain_tok.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_prefix_digest.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_prefix_digest.restype = C.c_uint64
+        L.ppsdh_token.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_state.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+        L.ppsdh_trace.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64]
+        L.ppsdh_trace.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+class HostSched:
+    def __init__(self, n_layers, exit_depth, *, exit_stage=0, comm_latency=0, model=1,
+                 force_reject=False, stop=0, prompt=(), alpha=0.0, verify_seed=0,
+                 toy_seed=None, max_ctx=8192, trace_cap=1 << 20):
+        L = lib()
+        arr = (C.c_int32 * max(1, len(prompt)))(*prompt)
+        self.h = L.ppsdh_create(n_layers, exit_depth, exit_stage or 0, comm_latency, model,
+                                int(force_reject), stop, arr, len(prompt), max_ctx, alpha,
+                                verify_seed, int(toy_seed is not None), toy_seed or 0, trace_cap)
+        if not self.h:
+            raise ValueError("bad pipeline config")
+        self.n_prompt = len(prompt)
+        self.layers = sp.stage_layers(n_layers, exit_depth)
+        self.S = len(self.layers)
+        self.per = 1 + comm_latency
+        self.work = (C.c_int32 * (self.S + 2))()
+        self.info = (C.c_int32 * 8)()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ppsdh_destroy(self.h)
+            self.h = None
+
+    def plan(self):
+        r = lib().ppsdh_plan(self.h, self.work, self.info)
+        return r, list(self.work), list(self.info)
+
+    def finish(self, exit_tok=-1, final_tok=-1):
+        lib().ppsdh_finish(self.h, exit_tok, final_tok)
+
+    def chain_pos(self, slot):
+        return lib().ppsdh_chain_pos(self.h, slot)
+
+    def chain_tok(self, slot):
+        return lib().ppsdh_chain_tok(self.h, slot)
+
+    def prefix_digest(self, n):
+        return lib().ppsdh_prefix_digest(self.h, n)
+
+    def state(self):
+        out = (C.c_int64 * 6)()
+        lib().ppsdh_state(self.h, out)
+        return list(out)
+
+    def tokens(self, n):
+        return [lib().ppsdh_token(self.h, self.n_prompt + i) for i in range(n)]
+
+    def trace_rows(self):
+        n = self.state()[5]
+        buf = (C.c_int32 * (6 * max(1, n)))()
+        n = lib().ppsdh_trace(self.h, buf, n)
+        a = np.frombuffer(buf, dtype=np.int32)[: 6 * n].reshape(n, 6)
+        return [(int(t), int(s), KINDS[k], int(p), None if tok < 0 else int(tok), VERDICTS[v])
+                for t, s, k, p, tok, v in a]
+
+    def metrics(self):
+        committed, ticks, acc, rej, err, _ = self.state()
+        assert err == 0, f"scheduler error flags {err}"
+        return sp.make_metrics(committed, ticks, acc, rej, acc + rej, self.S * self.per)
+
+
+def _toy_heads(lm, n_layers, layers, k, S, digest_of, exit_slot, final_slot):
+    exit_tok = final_tok = -1
+    if exit_slot >= 0:
+        d = digest_of[exit_slot]
+        layer_after = sum(layers[:k])
+        fin = lm.advance_digest(d, layer_after, n_layers)
+        exit_tok = sp.first_argmax(lm.exit_logits(fin, d))
+    if final_slot >= 0:
+        final_tok = sp.first_argmax(lm.logits(digest_of[final_slot]))
+    return exit_tok, final_tok
+
+
+def run_toy(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=0, comm_latency=0,
+            force_reject=False):
+    """Single-rank engine emulation: plan -> toy stage compute -> heads -> finish."""
+    hs = HostSched(n_layers, exit_depth, exit_stage=exit_stage, comm_latency=comm_latency,
+                   model=1, force_reject=force_reject, stop=stop, prompt=prompt, toy_seed=lm.seed)
+    if stop == 0:
+        return [], sp.make_metrics(0, 0, 0, 0, 0, hs.S * hs.per), []
+    layers = hs.layers
+    first = [sum(layers[:i]) for i in range(len(layers))]
+    dig = {}
+    while True:
+        r, work, info = hs.plan()
+        if not r:
+            break
+        k = info[6]
+        for st in range(1, hs.S + 1):
+            slot = work[st]
+            if slot < 0:
+                continue
+            if st == 1 and info[1]:
+                pos = hs.chain_pos(slot)
+                dig[slot] = hs.prefix_digest(hs.n_prompt + pos - 1)
+            a = first[st - 1]
+            dig[slot] = lm.advance_digest(dig[slot], a, a + layers[st - 1])
+        e, f = _toy_heads(lm, n_layers, layers, k, hs.S, dig, info[2], info[3])
+        hs.finish(e, f)
+    m = hs.metrics()
+    return hs.tokens(m[0]), m, hs.trace_rows()
+
+
+def run_bernoulli(n_layers, exit_depth, alpha, horizon, verify_seed, *, exit_stage=0,
+                  comm_latency=0):
+    hs = HostSched(n_layers, exit_depth, exit_stage=exit_stage, comm_latency=comm_latency,
+                   model=0, stop=horizon, alpha=alpha, verify_seed=verify_seed)
+    while hs.plan()[0]:
+        hs.finish()
+    return hs.metrics(), hs.trace_rows()

@@ -1,0 +1,31 @@
+"""The shipped tick machine (csrc/sched.h, host build) against reference goldens."""
+
+import pytest
+
+from conftest import load_golden
+from hostsched import run_bernoulli, run_toy
+from oracle import specpipe_port as sp
+
+
+@pytest.mark.parametrize("case", load_golden("toylm_decode.json"), ids=lambda c: c["name"])
+def test_sched_toy_matches_reference(case):
+    lm = sp.ToyLMPort(case["n_layers"], case["vocab"], case["lm_seed"], case["beta"])
+    cfg = case["cfg"]
+    toks, m, rows = run_toy(lm, cfg["n_layers"], cfg["exit_depth"], case["prompt"],
+                            case["max_tokens"], exit_stage=cfg.get("exit_stage", 0) or 0,
+                            comm_latency=cfg.get("comm_latency", 0))
+    assert toks == case["tokens"]
+    assert list(m[:4]) == case["metrics"][:4]
+    assert m[4:] == tuple(case["metrics"][4:])
+    assert sp.trace_csv(rows) == case["trace_csv"]
+
+
+@pytest.mark.parametrize("case", load_golden("bernoulli.json"), ids=lambda c: f"a{c['alpha']}-{c['horizon']}")
+def test_sched_bernoulli_matches_reference(case):
+    cfg = case["cfg"]
+    verify_seed = sp.Stream(case["rng_seed"]).split("verify").seed
+    m, rows = run_bernoulli(cfg["n_layers"], cfg["exit_depth"], case["alpha"], case["horizon"],
+                            verify_seed, exit_stage=cfg.get("exit_stage", 0) or 0,
+                            comm_latency=cfg.get("comm_latency", 0))
+    assert list(m) == case["metrics"]
+    assert sp.trace_csv(rows) == case["trace_csv"]
