@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
   __shared__ float s_m[QPK], s_l[QPK];
   __shared__ int s_last;
 
+  pdl_wait();  // q / KV rows come from the preceding QKV kernel
+  pdl_trigger();
   const Work* w = a.work;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = a.dm.H, KVh = a.dm.KV;
@@ -148,13 +150,12 @@ namespace {
 template <int HD, typename KVT>
 cudaError_t launch_qpk(const AttnArgs& a, int grid, cudaStream_t st) {
   switch (a.dm.H / a.dm.KV) {
-    case 1: attn_kernel<HD, KVT, 1><<<grid, 128, 0, st>>>(a); break;
-    case 2: attn_kernel<HD, KVT, 2><<<grid, 128, 0, st>>>(a); break;
-    case 4: attn_kernel<HD, KVT, 4><<<grid, 128, 0, st>>>(a); break;
-    case 8: attn_kernel<HD, KVT, 8><<<grid, 128, 0, st>>>(a); break;
+    case 1: return launch_pdl(attn_kernel<HD, KVT, 1>, dim3(grid), dim3(128), 0, st, a);
+    case 2: return launch_pdl(attn_kernel<HD, KVT, 2>, dim3(grid), dim3(128), 0, st, a);
+    case 4: return launch_pdl(attn_kernel<HD, KVT, 4>, dim3(grid), dim3(128), 0, st, a);
+    case 8: return launch_pdl(attn_kernel<HD, KVT, 8>, dim3(grid), dim3(128), 0, st, a);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 template <int HD>
 cudaError_t launch_hd(const AttnArgs& a, int grid, cudaStream_t st) {

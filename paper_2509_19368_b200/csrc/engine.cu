@@ -8,6 +8,7 @@
 // (TickCtx / Sched / Work), so the host enqueues ticks back to back and only
 // synchronises when the lower bound on the remaining ticks is exhausted.
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -24,6 +25,9 @@ bool attn_supported(int hd, int qpk);
 }
 
 static thread_local std::string g_err;
+namespace ppsd {
+bool g_pdl = true;
+}
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -100,6 +104,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat) {
   GemvArgs a{};
   a.work = w;
   a.layer_i = layer_i;
+  a.desc_early = !(mat == kMatQKV && layer_i == 0);  // first kernel after the scheduler
   a.mat = mat;
   a.layers = e->d_layers;
   a.head_w = e->lm_head;
@@ -182,12 +187,13 @@ static int build_graphs(ppsd_engine* e) {
           if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
           n += 1;
         } else if (kind == PPSD_MODEL_TOYLM) {
-          toy_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx);
-          if (cudaGetLastError() != cudaSuccess) return -1;
+          if (launch_pdl(toy_tick_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx) != cudaSuccess)
+            return -1;
           n += 1;
         }
-        sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 0);
-        if (cudaGetLastError() != cudaSuccess) return -1;
+        if (launch_pdl(sched_tick_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
+            cudaSuccess)
+          return -1;
         return n + 1;
       },
       &e->g_tick, &e->tick_launches);
@@ -197,13 +203,15 @@ static int build_graphs(ppsd_engine* e) {
     rc = capture(
         e,
         [&]() -> int {
-          ar_begin_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, e->d_arctl, with_head);
-          if (cudaGetLastError() != cudaSuccess) return -1;
+          if (launch_pdl(ar_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl,
+                         with_head) != cudaSuccess)
+            return -1;
           int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
           if (m < 0) return -1;
           if (with_head && enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
-          ar_end_kernel<<<1, 32, 0, e->st>>>(e->d_ctx, e->d_arctl, with_head);
-          if (cudaGetLastError() != cudaSuccess) return -1;
+          if (launch_pdl(ar_end_kernel, dim3(1), dim3(32), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl,
+                         with_head) != cudaSuccess)
+            return -1;
           return m + 2 + with_head;
         },
         with_head ? &e->g_ar : &e->g_prefill, with_head ? &e->ar_launches : &e->prefill_launches);
@@ -245,6 +253,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
                        ppsd_engine* e) {
   e->md = *md;
   e->pd = *pd;
+  if (const char* v = getenv("PPSD_PDL")) ppsd::g_pdl = atoi(v) != 0;
   e->device = pd->device;
   CU(cudaSetDevice(e->device));
   CU(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));

@@ -2,30 +2,38 @@
 //
 // Every decode-step matmul is y = W x with W bf16 [R][K] streamed from HBM
 // exactly once and x a handful of fp32 vectors; the roofline is HBM bytes.
-// One persistent CTA per SM (grid = #SMs, 1 CTA/SM, ~200 KB smem):
+// One persistent CTA per SM (grid = #SMs, ~200 KB smem):
 //
 //   warp 8 (producer, one lane): cp.async.bulk (UBLKCP) of TR contiguous
-//       weight rows per stage into an NS-deep shared-memory ring, completion
-//       counted on a per-stage mbarrier (expect_tx), L2 evict_first hint.
+//       weight rows (48-96 KB per copy — measured: the per-SM bulk-copy
+//       engine needs few, large copies in flight) into an NS-deep smem ring,
+//       completion counted on per-stage mbarriers (expect_tx), L2 evict_first.
 //   warps 0-7 (consumers, 256 threads): thread t owns the 16-byte column
-//       vectors t, t+256, ... of every row, so its slice of the normalised
-//       input vector lives in registers for the whole kernel; per stage it
-//       does TR x VPT ld.shared.v4 + 8 FMAs each, then a warp butterfly per
-//       row and a deterministic 8-warp sum in a deferred, batched epilogue.
+//       vectors t, t+256, ... of every row; its slice of the normalised input
+//       vector lives in registers for the whole kernel. Per stage it issues
+//       all TR x VPT ld.shared.v4 at once, releases the stage back to the
+//       producer immediately (early release keeps the ring full), then does
+//       the FMAs and ONE transpose-butterfly that reduces all M x TR row
+//       partials of the warp in N-1+5-log2(N) shuffles.
 //
-// The tile space of ALL active problems of one launch (the same layer slot
-// of every pipeline stage that has a chain this tick — the "grouped" launch
-// that lets the stages of one GPU share the SMs) is split into contiguous,
-// byte-balanced ranges, one per CTA. Row results never depend on the range
-// split, the group count or the number of vectors, so the PPSD path and the
-// autoregressive path produce bit-identical hidden states.
+// Programmatic dependent launch: the producer starts streaming weights
+// before the previous kernel of the step has finished (weights never depend
+// on it); consumers wait (griddepcontrol.wait) before touching activations.
+// The per-tick work descriptor is read early except by the first layer
+// kernel after the scheduler (desc_early == 0).
+//
+// The tile space of ALL active problems of one launch (the same layer slot of
+// every pipeline stage with a chain this tick — the grouped launch through
+// which the stages on one GPU share the SMs) is split into contiguous ranges,
+// one per CTA. Row results never depend on the split, the group count or M,
+// so PPSD and autoregressive decoding produce bit-identical hidden states.
 //
 // Fused epilogues (the op that follows each matmul in the decoder layer):
 //   kMatQKV  : RMSNorm prologue; RoPE on (q,k) row pairs; q -> scratch,
 //              k,v -> paged KV cache at the chain's position.
 //   kMatGU   : RMSNorm prologue; SwiGLU on (gate,up) row pairs -> h.
 //   kMatO / kMatDown : residual add into the chain's fp32 hidden state.
-//   kMatHead : per-vector RMSNorm prologue (exit norm | final norm), M=2
+//   kMatHead : per-vector RMSNorm prologue (exit norm | final norm); M=2
 //              vectors share one pass over the tied LM head; fp32 logits and
 //              a deterministic first-index argmax across CTAs.
 #include <float.h>
@@ -39,8 +47,41 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
 
+constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Reduce N per-lane values across the warp. Afterwards lane L holds the
+// warp total of value index L >> (5 - log2 N). Fixed shuffle tree: the
+// result is deterministic.
+template <int N>
+__device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
+  static_assert((N & (N - 1)) == 0 && N <= 32, "N must be a power of two <= 32");
+  int cnt = N;
+  int off = 16;
+#pragma unroll
+  for (int step = 0; step < ilog2(N); ++step) {
+    const int half = cnt >> 1;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      if (i < half) {
+        const float keep = upper ? v[i + half] : v[i];
+        const float send = upper ? v[i] : v[i + half];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    cnt = half;
+    off >>= 1;
+  }
+  float s = v[0];
+#pragma unroll
+  for (int o = 16 >> ilog2(N); o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 template <int VPT, int TR, int M, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
+  constexpr int NV = M * TR;  // row partials per thread per stage
+  constexpr int CHT = (128 / TR) < 1 ? 1 : (128 / TR);  // tiles per deferred epilogue
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_prob[kMaxStages];
   __shared__ int s_np;
@@ -53,10 +94,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   const int stage_bytes = TR * K * 2;
   unsigned char* ring = smem;
   float* red = reinterpret_cast<float*>(smem + (size_t)NS * stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + kGemvChunkTiles * 8 * M * TR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + CHT * 8 * NV);
   uint64_t* empty = full + NS;
   const Work* work = a.work;
 
+  if (!a.desc_early) pdl_wait();
   if (tid == 0) {
     int np = 0;
     if (EPI == kMatHead) {
@@ -74,18 +116,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
   __syncthreads();
   const int np = s_np;
-  if (np == 0) return;
+  if (np == 0) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
   const int tpp = R / TR;
   const long long T = (long long)np * tpp;
   const long long t0 = T * blockIdx.x / gridDim.x;
   const long long t1 = T * (blockIdx.x + 1) / gridDim.x;
   const int ntiles = (int)(t1 - t0);
-
-  auto weights = [&](int p) -> const __nv_bfloat16* {
-    if (EPI == kMatHead) return a.head_w;
-    const LayerW& L = a.layers[work->first[s_prob[p]] + a.layer_i];
-    return EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;
-  };
 
   if (warp == 8) {  // ---------------- producer ----------------
     if (lane == 0 && ntiles > 0) {
@@ -97,7 +137,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         const int p = (int)(t / tpp);
         const int tile = (int)(t - (long long)p * tpp);
         if (p != cur_p) {
-          wb = reinterpret_cast<const unsigned char*>(weights(p));
+          const __nv_bfloat16* w;
+          if (EPI == kMatHead) {
+            w = a.head_w;
+          } else {
+            const LayerW& L = a.layers[work->first[s_prob[p]] + a.layer_i];
+            w = EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;
+          }
+          wb = reinterpret_cast<const unsigned char*>(w);
           cur_p = p;
         }
         const int st = n % NS;
@@ -111,19 +158,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
 
   // ---------------- consumers ----------------
+  pdl_wait();     // activations of the previous kernel are visible from here on
+  pdl_trigger();  // ...so the next kernel may start streaming its weights
   float bestv[M];
   int besti[M];
+  bool mact[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     bestv[m] = -FLT_MAX;
     besti[m] = INT_MAX;
-  }
-  bool mact[M];
-#pragma unroll
-  for (int m = 0; m < M; ++m) mact[m] = true;
-  if (EPI == kMatHead) {
-#pragma unroll
-    for (int m = 0; m < M; ++m) mact[m] = work->head_slot[m] >= 0;
+    mact[m] = EPI == kMatHead ? work->head_slot[m] >= 0 : true;
   }
 
   if (ntiles > 0) {
@@ -199,44 +243,44 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         named_bar_sync(1, kGemvConsumers);
       }
 
+      // ---- stage: all shared loads first, release the slot, then math ----
       const int st = n % NS;
       mbar_wait(&full[st], (n / NS) & 1);
       const unsigned char* tb = ring + (size_t)st * stage_bytes;
-      float acc[M][TR];
+      uint4 wv[TR][VPT];
 #pragma unroll
-      for (int m = 0; m < M; ++m)
+      for (int r = 0; r < TR; ++r)
 #pragma unroll
-        for (int r = 0; r < TR; ++r) acc[m][r] = 0.f;
+        for (int u = 0; u < VPT; ++u) {
+          const int v = tid + u * kGemvConsumers;
+          wv[r][u] = v < nvec ? lds128(tb + (size_t)r * K * 2 + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      float acc[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
 #pragma unroll
       for (int r = 0; r < TR; ++r) {
 #pragma unroll
         for (int u = 0; u < VPT; ++u) {
-          const int v = tid + u * kGemvConsumers;
-          if (v < nvec) {
-            const uint4 w = lds128(tb + (size_t)r * K * 2 + (size_t)v * 16);
-            const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
-                                 bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+          const uint4 w = wv[r][u];
+          const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                               bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
-              if (!mact[m]) continue;
+          for (int m = 0; m < M; ++m) {
+            if (!mact[m]) continue;
 #pragma unroll
-              for (int e = 0; e < 8; ++e) acc[m][r] = fmaf(wf[e], xr[m][u][e], acc[m][r]);
-            }
+            for (int e = 0; e < 8; ++e) acc[m * TR + r] = fmaf(wf[e], xr[m][u][e], acc[m * TR + r]);
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      const int ct = n % kGemvChunkTiles;
-#pragma unroll
-      for (int m = 0; m < M; ++m)
-#pragma unroll
-        for (int r = 0; r < TR; ++r) {
-          const float s = warp_sum(acc[m][r]);
-          if (lane == 0) red[((ct * 8 + warp) * M + m) * TR + r] = s;
-        }
+      const int ct = n % CHT;
+      const float s = transpose_reduce<NV>(acc, lane);
+      constexpr int kShift = 5 - ilog2(NV);
+      if ((lane & ((1 << kShift) - 1)) == 0) red[(ct * 8 + warp) * NV + (lane >> kShift)] = s;
 
-      if (ct == kGemvChunkTiles - 1 || n == ntiles - 1) {  // deferred epilogue
+      if (ct == CHT - 1 || n == ntiles - 1) {  // deferred epilogue over CHT tiles
         named_bar_sync(1, kGemvConsumers);
         const int n0 = n - ct;
         const int nrows = (ct + 1) * TR;
@@ -244,7 +288,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           const int tt = rl / TR, r = rl % TR;
           float s = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) s += red[((tt * 8 + w) * M + m) * TR + r];
+          for (int w = 0; w < 8; ++w) s += red[(tt * 8 + w) * NV + m * TR + r];
           return s;
         };
         if (EPI == kMatQKV || EPI == kMatGU) {
@@ -287,8 +331,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
                 const int page = a.page_table[pos / kPage];
                 const size_t off = (((size_t)page * KVh + kvh) * kPage + (pos % kPage)) * hd + w;
                 if (a.dm.kv_bf16) {
-                  __nv_bfloat162 pv = __floats2bfloat162_rn(o0, o1);
-                  *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) = pv;
+                  *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) =
+                      __floats2bfloat162_rn(o0, o1);
                 } else {
                   float* cp = reinterpret_cast<float*>(cache) + off;
                   cp[0] = o0;
@@ -340,7 +384,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     named_bar_sync(1, kGemvConsumers);
     if (tid == 0) {
-      __shared__ int s_last;
       for (int m = 0; m < M; ++m) {
         float v = s_bv[0][m];
         int i = s_bi[0][m];
@@ -350,8 +393,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         a.head_part[((size_t)blockIdx.x * 2 + m) * 2 + 1] = __int_as_float(i);
       }
       __threadfence();
-      s_last = (atomicAdd(a.head_cnt, 1) == (int)gridDim.x - 1);
-      if (s_last) {
+      if (atomicAdd(a.head_cnt, 1) == (int)gridDim.x - 1) {
         __threadfence();
         Work* wk = const_cast<Work*>(work);
         for (int m = 0; m < M; ++m) {
@@ -375,9 +417,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 
 namespace {
 constexpr int kVpts[] = {1, 2, 3, 4, 6, 7, 8, 14};
-constexpr size_t kRingBudget = 200 * 1024;
+constexpr size_t kRingBudget = 212 * 1024;
 
-constexpr int tr_for(int vpt) { return vpt <= 3 ? 4 : (vpt <= 6 ? 2 : 1); }
+// rows per stage: ~64-96 KB bulk copies (tools/stream_bench.cu)
+constexpr int tr_for(int vpt) {
+  return vpt == 1 ? 16 : vpt <= 3 ? 8 : vpt <= 6 ? 4 : vpt <= 8 ? 2 : 1;
+}
 
 template <int VPT, int EPI>
 cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only) {
@@ -385,18 +430,17 @@ cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st
   constexpr int M = EPI == kMatHead ? 2 : 1;
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fn<<<grid, kGemvThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(fn, dim3(grid), dim3(kGemvThreads), smem, st, a);
 }
 
 template <int VPT>
 cudaError_t launch_vpt(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only,
                        int mat) {
   // only the instantiations gemv_pick can select: the fused pair epilogues
-  // need TR >= 2 (VPT <= 6); the head runs on K = d_model <= 8192 (VPT <= 4)
+  // need TR >= 2; the head runs on K = d_model <= 8192 (VPT <= 4)
   if (mat == kMatO) return launch_one<VPT, kMatO>(a, smem, grid, st, attrs_only);
   if (mat == kMatDown) return launch_one<VPT, kMatDown>(a, smem, grid, st, attrs_only);
-  if constexpr (VPT <= 6) {
+  if constexpr (tr_for(VPT) >= 2) {
     if (mat == kMatQKV) return launch_one<VPT, kMatQKV>(a, smem, grid, st, attrs_only);
     if (mat == kMatGU) return launch_one<VPT, kMatGU>(a, smem, grid, st, attrs_only);
   }
@@ -406,8 +450,6 @@ cudaError_t launch_vpt(const GemvArgs& a, size_t smem, int grid, cudaStream_t st
   return cudaErrorInvalidValue;
 }
 
-}  // namespace
-namespace {
 cudaError_t dispatch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st, bool attrs_only,
                      int mat) {
   switch (vpt) {
@@ -437,10 +479,11 @@ int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* sme
   if ((mat == kMatQKV || mat == kMatGU) && t < 2) return -1;
   if (mat == kMatHead && v > 4) return -1;
   const int M = mat == kMatHead ? 2 : 1;
+  const int cht = 128 / t < 1 ? 1 : 128 / t;
   const size_t stage = (size_t)t * K * 2;
-  const size_t red = (size_t)kGemvChunkTiles * 8 * M * t * 4;
+  const size_t red = (size_t)cht * 8 * M * t * 4;
   int ns = (int)((kRingBudget - red) / stage);
-  if (ns > 8) ns = 8;
+  if (ns > 6) ns = 6;
   if (ns < 2) return -1;
   *vpt = v;
   *tr = t;

@@ -47,6 +47,7 @@ enum : int { kMatQKV = 0, kMatO = 1, kMatGU = 2, kMatDown = 3, kMatHead = 4 };
 struct GemvArgs {
   Work* work;
   int32_t layer_i;        // layer offset inside each stage
+  int32_t desc_early;     // 1: the work descriptor was written >= 2 kernels ago
   int32_t mat;            // kMat*
   const LayerW* layers;   // [n_layers]
   const __nv_bfloat16* head_w;
@@ -78,6 +79,27 @@ struct AttnArgs {
   const int32_t* page_table;
   int32_t max_pages;
 };
+
+// Programmatic dependent launch (PDL): every kernel of a decode step is
+// launched with programmatic stream serialization so it can be scheduled
+// while its predecessor drains; kernels order their own accesses with
+// griddepcontrol.wait / launch_dependents. Disable with PPSD_PDL=0.
+extern bool g_pdl;
+
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, args...);
+}
 
 // launchers (gemv.cu / attn.cu)
 int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* smem);

@@ -24,6 +24,8 @@ __device__ void embed_row(const TickCtx& c, int slot, int tok) {
 __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, int begin) {
   __shared__ __align__(16) Sched s;
   __shared__ int s_launch_slot, s_launch_pos;
+  pdl_wait();  // head results of this tick
+  pdl_trigger();
   const TickCtx c = *ctxp;
   copy_words(&s, c.sched, sizeof(Sched));
   __syncthreads();
@@ -61,6 +63,8 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
 
 // ---- autoregressive / prefill control (decode_autoregressive, pipesim.py:390-409)
 __global__ void __launch_bounds__(256) ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head) {
+  pdl_wait();
+  pdl_trigger();
   const TickCtx c = *ctxp;
   const int j = ctl->j;
   if (threadIdx.x == 0) {
@@ -77,6 +81,8 @@ __global__ void __launch_bounds__(256) ar_begin_kernel(const TickCtx* ctxp, ArCt
 }
 
 __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head) {
+  pdl_wait();
+  pdl_trigger();
   const TickCtx c = *ctxp;
   if (threadIdx.x == 0) {
     const int j = ctl->j;

@@ -61,6 +61,8 @@ __device__ int block_argmax(int V, F f) {
 
 // One tick of stage compute for every local stage plus both heads.
 __global__ void __launch_bounds__(256) toy_tick_kernel(const TickCtx* ctxp) {
+  pdl_wait();
+  pdl_trigger();
   const TickCtx c = *ctxp;
   Work* w = c.work;
   __shared__ uint64_t s_dig[kMaxStages];
