@@ -142,13 +142,21 @@ int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed, int32_t ho
                   int32_t force_reject, ppsd_metrics* out, ppsd_trace_row* trace,
                   int64_t trace_cap, int64_t* trace_len);
 
-/* Multi-rank stepping (one engine per GPU owning stages [stage_lo, stage_hi]).
- * Between tick_compute and tick_finish the caller all-gathers every rank's
- * outbox into every rank's inbox (NCCL all_gather over NVLink); the scheduler
- * state is replicated and advances identically on every rank. */
-int ppsd_exchange_info(ppsd_engine* e, void** outbox, void** inbox, int64_t* bytes_per_rank);
+/* Multi-rank stepping: one engine per GPU owning stages [stage_lo, stage_hi]
+ * of the pipeline. The scheduler is replicated on every rank
+ * and advances identically; per tick the caller all-gathers every rank's
+ * outbox (kBoxHeader int32 words + d fp32, ppsd_exchange_info) into every
+ * rank's inbox (world boxes) — NCCL all_gather on the engine stream — between
+ * ppsd_step_compute and ppsd_step_finish. The prompt prefill is pipelined the
+ * same way: ppsd_prefill_steps() rounds of {ppsd_prefill_compute, exchange}.
+ * stage_owner[st] (st = 1..S, index 0 unused) is the rank owning stage st.
+ * outbox / inbox are device buffers owned by the caller. */
+int ppsd_exchange_info(ppsd_engine* e, int64_t* outbox_bytes, void** cuda_stream);
 int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
-                    int32_t force_reject, int32_t world, int32_t rank);
+                    int32_t force_reject, const int32_t* stage_owner, int32_t world, int32_t rank,
+                    void* outbox, void* inbox);
+int ppsd_prefill_steps(ppsd_engine* e, int32_t* n_steps);
+int ppsd_prefill_compute(ppsd_engine* e);
 int ppsd_step_compute(ppsd_engine* e);
 int ppsd_step_finish(ppsd_engine* e);
 int ppsd_step_poll(ppsd_engine* e, int32_t* done, int64_t* committed, int64_t* ticks);

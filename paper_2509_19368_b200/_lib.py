@@ -80,10 +80,11 @@ EXPORTS = {
     "ppsd_simulate": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_int32,
                                 C.POINTER(Metrics), C.POINTER(TraceRowC), C.c_int64,
                                 C.POINTER(C.c_int64)]),
-    "ppsd_exchange_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
-                                     C.POINTER(C.c_int64)]),
+    "ppsd_exchange_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]),
     "ppsd_step_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32,
-                                  C.c_int32, C.c_int32]),
+                                  C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ppsd_prefill_steps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "ppsd_prefill_compute": (C.c_int, [C.c_void_p]),
     "ppsd_step_compute": (C.c_int, [C.c_void_p]),
     "ppsd_step_finish": (C.c_int, [C.c_void_p]),
     "ppsd_step_poll": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),

@@ -1,13 +1,15 @@
 // attn.cu — split-K decode attention over the paged KV cache.
 //
-// Work item = (stage group, kv head, KV page). One KV page is kPage=64
-// positions of one kv head stored contiguously ([page][kvh][64][hd]), so an
-// item streams one contiguous 16 KB (bf16, hd=128) K block and one V block.
-// All q heads that share the kv head (GQA) are scored against that block in
-// the same pass. Page boundaries are absolute positions, so the partial
-// results — and the ordered merge done by the last CTA to finish a
-// (chain, kv head) — depend only on the context length, never on how many
-// stages share the launch: PPSD and AR attention are bit-identical.
+// Work item = (stage group, kv head, KV page). A KV page is kPage=64
+// positions of one kv head stored contiguously ([page][kvh][64][hd]); an item
+// pulls its K block and V block into shared memory with two 1-D bulk copies
+// (UBLKCP, one mbarrier) — one DRAM round trip per item instead of a chain of
+// dependent loads — then scores every q head that shares the kv head (GQA)
+// against the block, takes a chunk-local softmax and accumulates V from smem.
+// Page boundaries are absolute positions, so the partial results, and the
+// ordered merge done by the last CTA to finish a (chain, kv head), depend
+// only on the context length — never on how many pipeline stages share the
+// launch: PPSD and AR attention are bit-identical.
 #include <float.h>
 
 #include "kernels.cuh"
@@ -15,39 +17,51 @@
 namespace ppsd {
 
 template <typename T>
-__device__ __forceinline__ void load16(const T* p, float* out);
+__device__ __forceinline__ void unpack16(const uint4& v, float* out);
 template <>
-__device__ __forceinline__ void load16<float>(const float* p, float* out) {
-  const float4 v = *reinterpret_cast<const float4*>(p);
-  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+__device__ __forceinline__ void unpack16<float>(const uint4& v, float* out) {
+  out[0] = __uint_as_float(v.x); out[1] = __uint_as_float(v.y);
+  out[2] = __uint_as_float(v.z); out[3] = __uint_as_float(v.w);
 }
 template <>
-__device__ __forceinline__ void load16<__nv_bfloat16>(const __nv_bfloat16* p, float* out) {
-  const uint4 v = *reinterpret_cast<const uint4*>(p);
+__device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& v, float* out) {
   out[0] = bf16lo(v.x); out[1] = bf16hi(v.x); out[2] = bf16lo(v.y); out[3] = bf16hi(v.y);
   out[4] = bf16lo(v.z); out[5] = bf16hi(v.z); out[6] = bf16lo(v.w); out[7] = bf16hi(v.w);
 }
 __device__ __forceinline__ float tof(float v) { return v; }
 __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
 
+constexpr int kAttnThreads = 128;
+
 template <int HD, typename KVT, int QPK>
-__global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
-  constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte load
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
+  constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte vector
   constexpr int LPT = HD / EPV;                // lanes per token
   constexpr int TPW = 32 / LPT;                // tokens per warp pass
+  constexpr int BLK = kPage * HD;              // elements per K (or V) page block
   static_assert(LPT >= 1 && LPT <= 32 && (32 % LPT) == 0, "head_dim / dtype combination");
+  extern __shared__ __align__(128) unsigned char smem[];
+  KVT* ks = reinterpret_cast<KVT*>(smem);
+  KVT* vs = ks + BLK;
   __shared__ float qs[QPK][HD];
   __shared__ float sc[QPK][kPage];
   __shared__ float s_m[QPK], s_l[QPK];
   __shared__ int s_last;
+  __shared__ __align__(8) uint64_t bar;
 
-  pdl_wait();  // q / KV rows come from the preceding QKV kernel
-  pdl_trigger();
   const Work* w = a.work;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int H = a.dm.H, KVh = a.dm.KV;
   const float scale = 1.0f / sqrtf((float)HD);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  pdl_wait();  // q / KV rows come from the preceding QKV kernel
+  pdl_trigger();
+  __syncthreads();
 
+  uint32_t phase = 0;
   for (int item = blockIdx.x;; item += gridDim.x) {
     int g = -1, rem = item, nch = 0;
     for (int gg = 0; gg < w->G; ++gg) {
@@ -61,12 +75,18 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
     const int slot = w->slot[g], ctx = w->pos[g] + 1;
     const int n = min(kPage, ctx - c * kPage);
     const LayerW& L = a.layers[w->first[g] + a.layer_i];
-    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * kPage * HD;
-    const KVT* kb = reinterpret_cast<const KVT*>(L.kc) + blk;
-    const KVT* vb = reinterpret_cast<const KVT*>(L.vc) + blk;
+    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
+      mbar_expect_tx(&bar, 2 * bytes);
+      bulk_g2s(ks, reinterpret_cast<const KVT*>(L.kc) + blk, bytes, &bar);
+      bulk_g2s(vs, reinterpret_cast<const KVT*>(L.vc) + blk, bytes, &bar);
+    }
     const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
-    for (int i = tid; i < QPK * HD; i += 128) qs[i / HD][i % HD] = qsrc[i];
+    for (int i = tid; i < QPK * HD; i += kAttnThreads) qs[i / HD][i % HD] = qsrc[i];
     __syncthreads();
+    mbar_wait(&bar, phase);
+    phase ^= 1;
 
     // scores: LPT lanes per token, one 16-byte K vector per lane
     const int li = lane % LPT, tw = lane / LPT;
@@ -77,7 +97,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
       for (int i = 0; i < QPK; ++i) part[i] = 0.f;
       if (tt < n) {
         float kf[EPV];
-        load16<KVT>(kb + (size_t)tt * HD + li * EPV, kf);
+        unpack16<KVT>(lds128(ks + (size_t)tt * HD + li * EPV), kf);
 #pragma unroll
         for (int i = 0; i < QPK; ++i)
 #pragma unroll
@@ -109,10 +129,11 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
     __syncthreads();
 
     float* pbase = a.part + (((size_t)slot * H + (size_t)kvh * QPK) * a.max_pages) * (HD + 2);
-    for (int idx = tid; idx < QPK * HD; idx += 128) {
+    for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
       const int i = idx / HD, d = idx - i * HD;
       float acc = 0.f;
-      for (int tt = 0; tt < n; ++tt) acc = fmaf(sc[i][tt], tof(vb[(size_t)tt * HD + d]), acc);
+#pragma unroll 8
+      for (int tt = 0; tt < n; ++tt) acc = fmaf(sc[i][tt], tof(vs[(size_t)tt * HD + d]), acc);
       pbase[((size_t)i * a.max_pages + c) * (HD + 2) + d] = acc;
     }
     if (tid < QPK) {
@@ -127,7 +148,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
     __syncthreads();
     if (s_last) {  // ordered merge of the page partials
       __threadfence();
-      for (int idx = tid; idx < QPK * HD; idx += 128) {
+      for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
         const int i = idx / HD, d = idx - i * HD;
         const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2);
         float M = -FLT_MAX;
@@ -147,19 +168,37 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnArgs a) {
 }
 
 namespace {
+template <int HD, typename KVT, int QPK>
+cudaError_t launch_k(const AttnArgs& a, int grid, cudaStream_t st, bool attrs) {
+  const size_t smem = 2 * (size_t)kPage * HD * sizeof(KVT);
+  if (attrs)
+    return cudaFuncSetAttribute(attn_kernel<HD, KVT, QPK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+  return launch_pdl(attn_kernel<HD, KVT, QPK>, dim3(grid), dim3(kAttnThreads), smem, st, a);
+}
 template <int HD, typename KVT>
-cudaError_t launch_qpk(const AttnArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_qpk(const AttnArgs& a, int grid, cudaStream_t st, bool attrs) {
   switch (a.dm.H / a.dm.KV) {
-    case 1: return launch_pdl(attn_kernel<HD, KVT, 1>, dim3(grid), dim3(128), 0, st, a);
-    case 2: return launch_pdl(attn_kernel<HD, KVT, 2>, dim3(grid), dim3(128), 0, st, a);
-    case 4: return launch_pdl(attn_kernel<HD, KVT, 4>, dim3(grid), dim3(128), 0, st, a);
-    case 8: return launch_pdl(attn_kernel<HD, KVT, 8>, dim3(grid), dim3(128), 0, st, a);
-    default: return cudaErrorInvalidValue;
+    case 1: return launch_k<HD, KVT, 1>(a, grid, st, attrs);
+    case 2: return launch_k<HD, KVT, 2>(a, grid, st, attrs);
+    case 4: return launch_k<HD, KVT, 4>(a, grid, st, attrs);
+    case 8: return launch_k<HD, KVT, 8>(a, grid, st, attrs);
   }
+  return cudaErrorInvalidValue;
 }
 template <int HD>
-cudaError_t launch_hd(const AttnArgs& a, int grid, cudaStream_t st) {
-  return a.dm.kv_bf16 ? launch_qpk<HD, __nv_bfloat16>(a, grid, st) : launch_qpk<HD, float>(a, grid, st);
+cudaError_t launch_hd(const AttnArgs& a, int grid, cudaStream_t st, bool attrs) {
+  return a.dm.kv_bf16 ? launch_qpk<HD, __nv_bfloat16>(a, grid, st, attrs)
+                      : launch_qpk<HD, float>(a, grid, st, attrs);
+}
+cudaError_t dispatch(const AttnArgs& a, int grid, cudaStream_t st, bool attrs) {
+  switch (a.dm.hd) {
+    case 16: return launch_hd<16>(a, grid, st, attrs);
+    case 32: return launch_hd<32>(a, grid, st, attrs);
+    case 64: return launch_hd<64>(a, grid, st, attrs);
+    case 128: return launch_hd<128>(a, grid, st, attrs);
+  }
+  return cudaErrorInvalidValue;
 }
 }  // namespace
 
@@ -167,14 +206,8 @@ bool attn_supported(int hd, int qpk) {
   return (hd == 16 || hd == 32 || hd == 64 || hd == 128) && (qpk == 1 || qpk == 2 || qpk == 4 || qpk == 8);
 }
 
-cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) {
-  switch (a.dm.hd) {
-    case 16: return launch_hd<16>(a, grid, st);
-    case 32: return launch_hd<32>(a, grid, st);
-    case 64: return launch_hd<64>(a, grid, st);
-    case 128: return launch_hd<128>(a, grid, st);
-  }
-  return cudaErrorInvalidValue;
-}
+cudaError_t attn_set_attrs(const AttnArgs& a) { return dispatch(a, 0, 0, true); }
+
+cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) { return dispatch(a, grid, st, false); }
 
 }  // namespace ppsd

@@ -81,6 +81,10 @@ struct ppsd_engine {
   const float* rope_sin = nullptr;
   // graphs
   cudaGraphExec_t g_tick = nullptr, g_ar = nullptr, g_prefill = nullptr;
+  cudaGraphExec_t g_compute = nullptr, g_finish = nullptr, g_mr_prefill = nullptr;  // multi-rank
+  int64_t compute_launches = 0, finish_launches = 0, mr_prefill_launches = 0;
+  int mr_world = 0, mr_rank = 0, mr_stop = 0, mr_n_prompt = 0;
+  int64_t mr_launches = 0, mr_ticks_launched = 0;
   int64_t tick_launches = 0, ar_launches = 0, prefill_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   // host staging
@@ -94,7 +98,7 @@ extern "C" const char* ppsd_build_info(void) {
   return "libppsd sm_100a: tma-bulk gemv ring, split-K paged attention, device tick machine";
 }
 
-static int attn_grid(const ppsd_engine* e) { return 2 * e->num_sms; }
+static int attn_grid(const ppsd_engine* e) { return 4 * e->num_sms; }
 
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
@@ -229,6 +233,9 @@ static void free_engine(ppsd_engine* e) {
   if (e->g_tick) cudaGraphExecDestroy(e->g_tick);
   if (e->g_ar) cudaGraphExecDestroy(e->g_ar);
   if (e->g_prefill) cudaGraphExecDestroy(e->g_prefill);
+  if (e->g_compute) cudaGraphExecDestroy(e->g_compute);
+  if (e->g_finish) cudaGraphExecDestroy(e->g_finish);
+  if (e->g_mr_prefill) cudaGraphExecDestroy(e->g_mr_prefill);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv};
@@ -298,6 +305,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.hi = e->hi;
   c.n_layers = md->n_layers;
   c.vocab = md->vocab;
+  c.model_stages = e->cfg.S;
 
   if (md->kind == PPSD_MODEL_TOYLM) {
     if (md->vocab < 2) return fail(PPSD_EINVAL, "vocab must be >= 2");
@@ -324,7 +332,9 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       return fail(PPSD_EUNSUPPORTED, "unsupported head geometry (head_dim in {16,32,64,128}, H/KV in {1,2,4,8})");
     if (d.d % 8 || d.ffn % 8 || (d.H * d.hd) % 8)
       return fail(PPSD_EUNSUPPORTED, "d_model, ffn_dim and H*head_dim must be multiples of 8");
-    if (!w || !w->lm_head || !w->embed || !w->final_norm || !w->exit_norm || !w->rope_cos)
+    const bool need_head = (e->cfg.k >= e->lo && e->cfg.k <= e->hi) || e->hi == e->S;
+    if (!w || !w->final_norm || !w->exit_norm || !w->rope_cos || (e->lo == 1 && !w->embed) ||
+        (need_head && !w->lm_head))
       return fail(PPSD_EINVAL, "missing transformer weights");
     const int Rq = (d.H + 2 * d.KV) * d.hd;
     const int shapes[5][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d}, {d.d, d.ffn}, {d.V, d.d}};
@@ -336,6 +346,11 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
                                            std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
       CU(gemv_set_attrs(p.vpt, m, p.smem));
+    }
+    {
+      AttnArgs aa{};
+      aa.dm = d;
+      CU(attn_set_attrs(aa));
     }
     e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
     e->final_norm = w->final_norm;
@@ -495,6 +510,8 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   s.c.verify_seed = verify_seed;
   sched_reset(&s);
   e->h_ctx.trace = trace ? e->d_trace : nullptr;
+  e->h_ctx.inbox = nullptr;  // single-rank run
+  e->h_ctx.outbox = nullptr;
   e->h_ctx.trace_cap = cap;
   CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
   CU(cudaMemcpyAsync(e->d_sched, &s, sizeof(Sched), cudaMemcpyHostToDevice, e->st));
@@ -710,18 +727,191 @@ extern "C" int ppsd_read_logits(ppsd_engine* e, int32_t which, float* out) {
 
 // ---------------------------------------------------------------------------
 // multi-rank stepping (one engine per GPU); see include/ppsd.h
+//
+// Per tick: step_compute = [layers of the local stages, local heads, pack
+// outbox]; the caller all-gathers every rank's outbox into every inbox
+// (NCCL over NVLink); step_finish = [sched_tick: unpack the arriving
+// activation + the owners' head results, verdict/draft/rollback, plan].
+// Every rank runs the identical scheduler, so ranks agree on every tick
+// without any other message.
 
-extern "C" int ppsd_exchange_info(ppsd_engine*, void**, void**, int64_t*) {
-  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+static int build_mr_graphs(ppsd_engine* e) {
+  if (e->g_compute) return PPSD_OK;
+  int rc = capture(
+      e,
+      [&]() -> int {
+        int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+        if (m < 0) return -1;
+        if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
+        if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
+            cudaSuccess)
+          return -1;
+        return m + 2;
+      },
+      &e->g_compute, &e->compute_launches);
+  if (rc) return rc;
+  rc = capture(
+      e,
+      [&]() -> int {
+        if (launch_pdl(sched_tick_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
+            cudaSuccess)
+          return -1;
+        return 1;
+      },
+      &e->g_finish, &e->finish_launches);
+  if (rc) return rc;
+  return capture(
+      e,
+      [&]() -> int {
+        if (launch_pdl(mr_prefill_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
+                       e->d_arctl) != cudaSuccess)
+          return -1;
+        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
+        if (m < 0) return -1;
+        if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 1) !=
+            cudaSuccess)
+          return -1;
+        return m + 2;
+      },
+      &e->g_mr_prefill, &e->mr_prefill_launches);
 }
-extern "C" int ppsd_step_begin(ppsd_engine*, const int32_t*, int32_t, int32_t, int32_t, int32_t, int32_t) {
-  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+
+extern "C" int ppsd_exchange_info(ppsd_engine* e, int64_t* outbox_bytes, void** cuda_stream) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "multi-rank needs a transformer engine");
+  if (outbox_bytes) *outbox_bytes = (int64_t)(kBoxHeader + e->dm.d) * 4;
+  if (cuda_stream) *cuda_stream = e->st;
+  return PPSD_OK;
 }
-extern "C" int ppsd_step_compute(ppsd_engine*) { return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet"); }
-extern "C" int ppsd_step_finish(ppsd_engine*) { return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet"); }
-extern "C" int ppsd_step_poll(ppsd_engine*, int32_t*, int64_t*, int64_t*) {
-  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+
+extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
+                               int32_t force_reject, const int32_t* stage_owner, int32_t world, int32_t rank,
+                               void* outbox, void* inbox) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "multi-rank needs a transformer engine");
+  if (!stage_owner || world < 1 || rank < 0 || rank >= world || !outbox || !inbox)
+    return fail(PPSD_EINVAL, "bad multi-rank arguments");
+  for (int st = e->lo; st <= e->hi; ++st)
+    if (stage_owner[st] != rank) return fail(PPSD_EINVAL, "stage_owner disagrees with the engine's stage range");
+  int rc = check_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  if (max_tokens < 1) return fail(PPSD_EINVAL, "max_tokens must be >= 1 for stepping");
+  if ((int64_t)n_prompt + max_tokens + (int64_t)e->S * e->cfg.per + 2 > e->md.max_ctx)
+    return fail(PPSD_EINVAL, "prompt + max_tokens exceeds the engine's max_ctx");
+  CU(cudaSetDevice(e->device));
+  rc = build_mr_graphs(e);
+  if (rc) return rc;
+  rc = upload_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  const int64_t max_ticks = (int64_t)max_tokens * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
+  rc = ensure_trace(e, max_ticks * (e->S + 2));
+  if (rc) return rc;
+  TickCtx& c = e->h_ctx;
+  c.trace = e->d_trace;
+  c.trace_cap = e->trace_cap;
+  c.outbox = reinterpret_cast<float*>(outbox);
+  c.inbox = reinterpret_cast<const float*>(inbox);
+  c.box_words = kBoxHeader + e->dm.d;
+  c.rank = rank;
+  c.world = world;
+  c.owner_k = stage_owner[e->cfg.k];
+  c.owner_S = stage_owner[e->S];
+  c.owner_prev = e->lo > 1 ? stage_owner[e->lo - 1] : -1;
+  c.n_prompt = n_prompt;
+  Sched& s = *e->h_sched;
+  memset(&s, 0, sizeof(Sched));
+  s.c = e->cfg;
+  s.c.model = 1;
+  s.c.force_reject = force_reject;
+  s.c.stop = max_tokens;
+  s.c.n_prompt = n_prompt;
+  sched_reset(&s);
+  ArCtl ctl{0, e->first_local_layer, e->n_local_layers, 0};
+  CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_ctx, &c, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_sched, &s, sizeof(Sched), cudaMemcpyHostToDevice, e->st));
+  sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 1);  // plan tick 1 (+ embed on rank 0)
+  CU(cudaGetLastError());
+  e->mr_world = world;
+  e->mr_rank = rank;
+  e->mr_stop = max_tokens;
+  e->mr_n_prompt = n_prompt;
+  e->mr_launches = 1;
+  e->mr_ticks_launched = 0;
+  CU(cudaEventRecord(e->ev0, e->st));
+  return PPSD_OK;
 }
-extern "C" int ppsd_step_end(ppsd_engine*, int32_t*, ppsd_metrics*, ppsd_trace_row*, int64_t, int64_t*) {
-  return fail(PPSD_EUNSUPPORTED, "multi-rank stepping not built yet");
+
+extern "C" int ppsd_prefill_steps(ppsd_engine* e, int32_t* n_steps) {
+  if (!e || !n_steps) return fail(PPSD_EINVAL, "null argument");
+  *n_steps = e->mr_n_prompt >= 2 ? (e->mr_n_prompt - 1) + (e->mr_world - 1) : 0;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_prefill_compute(ppsd_engine* e) {
+  if (!e || !e->g_mr_prefill) return fail(PPSD_ESTATE, "call ppsd_step_begin first");
+  CU(cudaGraphLaunch(e->g_mr_prefill, e->st));
+  e->mr_launches += e->mr_prefill_launches;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_step_compute(ppsd_engine* e) {
+  if (!e || !e->g_compute) return fail(PPSD_ESTATE, "call ppsd_step_begin first");
+  if (e->mr_ticks_launched == 0) CU(cudaEventRecord(e->ev2, e->st));  // decode starts (prefill done)
+  CU(cudaGraphLaunch(e->g_compute, e->st));
+  e->mr_launches += e->compute_launches;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_step_finish(ppsd_engine* e) {
+  if (!e || !e->g_finish) return fail(PPSD_ESTATE, "call ppsd_step_begin first");
+  CU(cudaGraphLaunch(e->g_finish, e->st));
+  e->mr_launches += e->finish_launches;
+  e->mr_ticks_launched += 1;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_step_poll(ppsd_engine* e, int32_t* done, int64_t* committed, int64_t* ticks) {
+  if (!e) return fail(PPSD_EINVAL, "null argument");
+  Sched& s = *e->h_sched;
+  const size_t off = offsetof(Sched, t);
+  const size_t len = offsetof(Sched, verify_counter) - off;
+  CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
+                     cudaMemcpyDeviceToHost, e->st));
+  CU(cudaStreamSynchronize(e->st));
+  if (s.error) return fail(PPSD_ESTATE, "scheduler error flags " + std::to_string(s.error));
+  if (done) *done = s.done;
+  if (committed) *committed = s.committed;
+  if (ticks) *ticks = s.t;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_step_end(ppsd_engine* e, int32_t* out_tokens, ppsd_metrics* out, ppsd_trace_row* trace,
+                             int64_t trace_cap, int64_t* trace_len) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  CU(cudaEventRecord(e->ev1, e->st));
+  Sched& s = *e->h_sched;
+  CU(cudaMemcpyAsync(&s, e->d_sched, sizeof(Sched), cudaMemcpyDeviceToHost, e->st));
+  CU(cudaStreamSynchronize(e->st));
+  if (!s.done) return fail(PPSD_ESTATE, "decode not finished");
+  if (s.error) return fail(PPSD_ESTATE, "scheduler error flags " + std::to_string(s.error));
+  float ms = 0, pre = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev2, e->ev1));
+  CU(cudaEventElapsedTime(&pre, e->ev0, e->ev2));
+  memset(out, 0, sizeof(*out));
+  fill_metrics(e, s, out);
+  out->decode_ms = ms;    // decode ticks on this rank's stream (CUDA events)
+  out->prefill_ms = pre;  // pipelined prefill steps
+  out->gpu_launches = e->mr_launches;
+  if (out_tokens)
+    CU(cudaMemcpy(out_tokens, e->d_tokens + e->mr_n_prompt, sizeof(int32_t) * e->mr_stop, cudaMemcpyDeviceToHost));
+  if (trace) {
+    const int64_t n = std::min<int64_t>(s.trace_n, trace_cap);
+    if (n > 0) CU(cudaMemcpy(trace, e->d_trace, sizeof(TraceRow) * n, cudaMemcpyDeviceToHost));
+    if (trace_len) *trace_len = n;
+  } else if (trace_len) {
+    *trace_len = 0;
+  }
+  e->h_ctx.inbox = nullptr;
+  e->h_ctx.outbox = nullptr;
+  CU(cudaMemcpy(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice));
+  return PPSD_OK;
 }

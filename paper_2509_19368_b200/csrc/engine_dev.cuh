@@ -25,7 +25,19 @@ struct TickCtx {
   int32_t n_layers, vocab;
   double beta;
   uint64_t toy_seed;
+  // multi-rank exchange (null / 0 on a single-rank engine). A box is
+  // kBoxHeader int32 words {exit_tok, final_tok, act_slot, act_pos} followed by
+  // the d fp32 activation leaving this rank's last local stage.
+  float* outbox;
+  const float* inbox;   // world boxes, all-gathered by the caller
+  int32_t box_words;
+  int32_t rank, world;
+  int32_t owner_k, owner_S, owner_prev;  // ranks owning the exit stage, stage S, stage lo-1
+  int32_t n_prompt;
+  int32_t model_stages;  // S
 };
+
+constexpr int kBoxHeader = 4;
 
 struct ArCtl {
   int32_t j;           // token index being processed
@@ -38,6 +50,8 @@ __global__ void sched_tick_kernel(const TickCtx* ctxp, int begin);
 __global__ void ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void toy_tick_kernel(const TickCtx* ctxp);
+__global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
+__global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);
 __global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long rows, long long cols,
                                    uint64_t b0, uint64_t b1, uint64_t b2, float a0, float a1, float a2,

@@ -106,5 +106,6 @@ int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* sme
 cudaError_t gemv_launch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st);
 cudaError_t gemv_set_attrs(int vpt, int mat, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
+cudaError_t attn_set_attrs(const AttnArgs& a);
 
 }  // namespace ppsd

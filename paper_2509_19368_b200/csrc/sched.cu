@@ -8,17 +8,52 @@
 
 namespace ppsd {
 
+// block copy with all loads of a thread issued before its stores (one
+// memory round trip instead of a dependent chain per element)
 __device__ void copy_words(void* dst, const void* src, int bytes) {
-  const int n = bytes / 4;
-  const int* s = reinterpret_cast<const int*>(src);
-  int* d = reinterpret_cast<int*>(dst);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = s[i];
+  const int n16 = bytes / 16;
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  constexpr int U = 4;
+  for (int base = 0; base < n16; base += U * blockDim.x) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i < n16) v[u] = s[i];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i < n16) d[i] = v[u];
+    }
+  }
+  const int tail = bytes - n16 * 16;  // Sched is 4-byte aligned
+  if ((int)threadIdx.x < tail / 4)
+    reinterpret_cast<int*>(dst)[n16 * 4 + threadIdx.x] = reinterpret_cast<const int*>(src)[n16 * 4 + threadIdx.x];
 }
 
 __device__ void embed_row(const TickCtx& c, int slot, int tok) {
-  const __nv_bfloat16* row = c.embed + (size_t)tok * c.d;
-  float* x = c.x + (size_t)slot * c.d;
-  for (int i = threadIdx.x; i < c.d; i += blockDim.x) x[i] = __bfloat162float(row[i]);
+  const uint4* row = reinterpret_cast<const uint4*>(c.embed + (size_t)tok * c.d);  // 8 bf16 per vector
+  float4* x = reinterpret_cast<float4*>(c.x + (size_t)slot * c.d);
+  const int nv = c.d / 8;
+  constexpr int U = 4;
+  for (int base = 0; base < nv; base += U * blockDim.x) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i < nv) v[u] = row[i];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i < nv) {
+        x[2 * i] = make_float4(bf16lo(v[u].x), bf16hi(v[u].x), bf16lo(v[u].y), bf16hi(v[u].y));
+        x[2 * i + 1] = make_float4(bf16lo(v[u].z), bf16hi(v[u].z), bf16lo(v[u].w), bf16hi(v[u].w));
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, int begin) {
@@ -29,9 +64,22 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
   const TickCtx c = *ctxp;
   copy_words(&s, c.sched, sizeof(Sched));
   __syncthreads();
+  if (!begin && c.inbox && c.owner_prev >= 0) {
+    // the chain stage lo-1 (another rank) ran this tick arrives with its activation
+    const int prev = s.work[c.lo - 1];
+    if (prev >= 0) {
+      const float* box = c.inbox + (size_t)c.owner_prev * c.box_words;
+      float* x = c.x + (size_t)prev * c.d;
+      for (int i = threadIdx.x; i < c.d; i += blockDim.x) x[i] = box[kBoxHeader + i];
+    }
+  }
   if (threadIdx.x == 0) {
-    if (!begin) sched_finish(&s, c.work->head_out[0], c.work->head_out[1], c.tokens, c.pdig,
-                             c.trace, c.trace_cap);
+    int exit_tok = c.work->head_out[0], final_tok = c.work->head_out[1];
+    if (c.inbox) {  // replicated scheduler: head results come from their owners' boxes
+      exit_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_k * c.box_words)[0];
+      final_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_S * c.box_words)[1];
+    }
+    if (!begin) sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap);
     sched_plan(&s);
     Work* w = c.work;
     w->G = c.hi - c.lo + 1;
@@ -59,6 +107,57 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
     }
   }
   copy_words(c.sched, &s, sizeof(Sched));
+}
+
+// Multi-rank: publish this rank's head results and the activation leaving
+// its last local stage (decode tick), or the prefill activation.
+__global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, int prefill) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  int32_t* hdr = reinterpret_cast<int32_t*>(c.outbox);
+  const Work* w = prefill ? c.work_ar : c.work;
+  const int slot = w->slot[w->G - 1];
+  const bool send = slot >= 0 && (prefill || c.hi < c.model_stages);
+  if (threadIdx.x == 0) {
+    hdr[0] = w->head_slot[0] >= 0 ? w->head_out[0] : -1;
+    hdr[1] = w->head_slot[1] >= 0 ? w->head_out[1] : -1;
+    hdr[2] = send ? slot : -1;
+    hdr[3] = send ? w->pos[w->G - 1] : -1;
+  }
+  if (send) {
+    const float* x = c.x + (size_t)slot * c.d;
+    for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.outbox[kBoxHeader + i] = x[i];
+  }
+}
+
+// Multi-rank pipelined prefill: at step p rank r runs its layers on prompt
+// token p - r; its input is the embedding (rank 0) or rank r-1's box.
+__global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  const int p = ctl->j;
+  const int j = p - c.rank;
+  const bool active = j >= 0 && j < c.n_prompt - 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Work* w = c.work_ar;
+    w->G = 1;
+    w->slot[0] = active ? 0 : -1;
+    w->pos[0] = active ? j : 0;
+    w->first[0] = ctl->first_layer;
+    w->nl[0] = ctl->n_layers;
+    w->head_slot[0] = w->head_slot[1] = -1;
+    ctl->j = p + 1;
+  }
+  if (!active) return;
+  if (c.rank == 0) {
+    embed_row(c, 0, c.tokens[j]);
+  } else {
+    const float* box = c.inbox + (size_t)(c.rank - 1) * c.box_words;
+    for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.x[i] = box[kBoxHeader + i];
+  }
 }
 
 // ---- autoregressive / prefill control (decode_autoregressive, pipesim.py:390-409)
