@@ -130,11 +130,21 @@ int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n
 int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
                    int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out);
 
-/* greedy draft-then-verify rounds of gamma drafts (EESD baseline) */
+/* greedy draft-then-verify rounds of gamma drafts (EESD baseline,
+ * simulate_eesd with a greedy model oracle, pipesim.py:435-551): gamma
+ * one-token drafts through the first exit_stage*exit_depth layers, one batched
+ * verify of the gamma+1 positions, acceptance scan, bonus / truncate. Returns
+ * the committed tokens (up to out_cap; the last round may overshoot horizon). */
 int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32_t n_prompt,
                      int32_t horizon, int32_t* out_tokens, int32_t out_cap,
                      ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
                      int64_t* trace_len);
+
+/* simulate_eesd with AcceptanceOracle.bernoulli (verify_seed =
+ * derive_seed(rng.seed, "verify"), pipesim.py:467) */
+int ppsd_simulate_eesd(ppsd_engine* e, int32_t gamma, double alpha, uint64_t verify_seed,
+                       int32_t horizon, ppsd_metrics* out, ppsd_trace_row* trace,
+                       int64_t trace_cap, int64_t* trace_len);
 
 /* schedule-only PPSD with Bernoulli(alpha) verdicts drawn from the counter
  * stream seeded verify_seed (= derive_seed(rng.seed, "verify")) */

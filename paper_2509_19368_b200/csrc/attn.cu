@@ -63,16 +63,20 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
 
   uint32_t phase = 0;
   for (int item = blockIdx.x;; item += gridDim.x) {
-    int g = -1, rem = item, nch = 0;
-    for (int gg = 0; gg < w->G; ++gg) {
+    // items: (group, vector, kv head, page); vector v of group g sits at
+    // slot[g]+v and position pos[g]+v (batched prefill / EESD verify)
+    int g = -1, vv = 0, rem = item, nch = 0;
+    for (int gg = 0; gg < w->G && g < 0; ++gg) {
       if (w->slot[gg] < 0 || a.layer_i >= w->nl[gg]) continue;
-      nch = (w->pos[gg] + kPage) / kPage;  // ceil((pos+1)/kPage)
-      if (rem < nch * KVh) { g = gg; break; }
-      rem -= nch * KVh;
+      for (int v = 0; v < w->nv[gg]; ++v) {
+        nch = (w->pos[gg] + v + kPage) / kPage;  // ceil((pos+1)/kPage)
+        if (rem < nch * KVh) { g = gg; vv = v; break; }
+        rem -= nch * KVh;
+      }
     }
     if (g < 0) break;
     const int kvh = rem / nch, c = rem - kvh * nch;
-    const int slot = w->slot[g], ctx = w->pos[g] + 1;
+    const int slot = w->slot[g] + vv, ctx = w->pos[g] + vv + 1;
     const int n = min(kPage, ctx - c * kPage);
     const LayerW& L = a.layers[w->first[g] + a.layer_i];
     const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;

@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -42,7 +43,7 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 struct GemvPlan {
-  int vpt = 0, tr = 0, ns = 0, R = 0, K = 0;
+  int vpt = 0, tr = 0, m = 1, ns = 0, R = 0, K = 0;
   size_t smem = 0;
 };
 
@@ -73,7 +74,9 @@ struct ppsd_engine {
   int32_t *d_attn_cnt = nullptr, *d_head_cnt = nullptr, *d_page_table = nullptr;
   void* d_kv = nullptr;
   int max_pages = 0;
-  GemvPlan gp[5];
+  GemvPlan gp[kNumMats];   // decode tick: one vector per weight pass (head: exit + final)
+  GemvPlan gpb[kNumMats];  // batched prefill / EESD verify: up to 4 vectors per pass
+  int nbuf = 0;            // activation slots (>= nslot, >= kMaxVec)
   const __nv_bfloat16* lm_head = nullptr;
   const float* final_norm = nullptr;
   const float* exit_norm = nullptr;
@@ -82,6 +85,8 @@ struct ppsd_engine {
   // graphs
   cudaGraphExec_t g_tick = nullptr, g_ar = nullptr, g_prefill = nullptr;
   cudaGraphExec_t g_compute = nullptr, g_finish = nullptr, g_mr_prefill = nullptr;  // multi-rank
+  std::map<int, std::pair<cudaGraphExec_t, int64_t>> eesd_graphs;  // per gamma: round graph, launches
+  EesdState* d_eesd = nullptr;
   int64_t compute_launches = 0, finish_launches = 0, mr_prefill_launches = 0;
   int mr_world = 0, mr_rank = 0, mr_stop = 0, mr_n_prompt = 0;
   int64_t mr_launches = 0, mr_ticks_launched = 0;
@@ -103,8 +108,8 @@ static int attn_grid(const ppsd_engine* e) { return 4 * e->num_sms; }
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
 
-static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat) {
-  const GemvPlan& p = e->gp[mat];
+static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, bool batched = false) {
+  const GemvPlan& p = batched ? e->gpb[mat] : e->gp[mat];
   GemvArgs a{};
   a.work = w;
   a.layer_i = layer_i;
@@ -128,7 +133,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat) {
   a.page_table = e->d_page_table;
   a.head_part = e->d_head_part;
   a.head_cnt = e->d_head_cnt;
-  return gemv_launch(a, p.vpt, p.smem, e->num_sms, e->st);
+  return gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st);
 }
 
 static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
@@ -147,14 +152,14 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
 }
 
 // returns launches enqueued, or -1 on error
-static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots) {
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched = false) {
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
-    if (enqueue_gemv(e, w, i, kMatQKV) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatQKV, batched) != cudaSuccess) return -1;
     if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
-    if (enqueue_gemv(e, w, i, kMatO) != cudaSuccess) return -1;
-    if (enqueue_gemv(e, w, i, kMatGU) != cudaSuccess) return -1;
-    if (enqueue_gemv(e, w, i, kMatDown) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatO, batched) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatGU, batched) != cudaSuccess) return -1;
+    if (enqueue_gemv(e, w, i, kMatDown, batched) != cudaSuccess) return -1;
     n += 5;
   }
   return n;
@@ -203,24 +208,34 @@ static int build_graphs(ppsd_engine* e) {
       &e->g_tick, &e->tick_launches);
   if (rc) return rc;
   if (kind != PPSD_MODEL_TRANSFORMER) return PPSD_OK;
-  for (int with_head = 0; with_head < 2; ++with_head) {
-    rc = capture(
-        e,
-        [&]() -> int {
-          if (launch_pdl(ar_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl,
-                         with_head) != cudaSuccess)
-            return -1;
-          int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
-          if (m < 0) return -1;
-          if (with_head && enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
-          if (launch_pdl(ar_end_kernel, dim3(1), dim3(32), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl,
-                         with_head) != cudaSuccess)
-            return -1;
-          return m + 2 + with_head;
-        },
-        with_head ? &e->g_ar : &e->g_prefill, with_head ? &e->ar_launches : &e->prefill_launches);
-    if (rc) return rc;
-  }
+  rc = capture(  // autoregressive token step (decode_autoregressive)
+      e,
+      [&]() -> int {
+        if (launch_pdl(ar_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
+            cudaSuccess)
+          return -1;
+        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
+        if (m < 0) return -1;
+        if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
+        if (launch_pdl(ar_end_kernel, dim3(1), dim3(32), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
+            cudaSuccess)
+          return -1;
+        return m + 3;
+      },
+      &e->g_ar, &e->ar_launches);
+  if (rc) return rc;
+  rc = capture(  // batched prompt prefill: one chunk of up to kMaxVec tokens per launch
+      e,
+      [&]() -> int {
+        if (launch_pdl(prefill_chunk_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
+                       e->d_arctl) != cudaSuccess)
+          return -1;
+        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);
+        if (m < 0) return -1;
+        return m + 1;
+      },
+      &e->g_prefill, &e->prefill_launches);
+  if (rc) return rc;
   return PPSD_OK;
 }
 
@@ -236,6 +251,8 @@ static void free_engine(ppsd_engine* e) {
   if (e->g_compute) cudaGraphExecDestroy(e->g_compute);
   if (e->g_finish) cudaGraphExecDestroy(e->g_finish);
   if (e->g_mr_prefill) cudaGraphExecDestroy(e->g_mr_prefill);
+  for (auto& kv : e->eesd_graphs) cudaGraphExecDestroy(kv.second.first);
+  if (e->d_eesd) cudaFree(e->d_eesd);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv};
@@ -286,6 +303,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   const int max_ctx = md->max_ctx > 0 ? md->max_ctx : 4096;
   e->md.max_ctx = max_ctx;
   const int nslot = e->cfg.nslot;
+  e->nbuf = std::max(nslot, (int)kMaxVec);
 
   CU(dalloc(&e->d_sched, sizeof(Sched)));
   CU(dalloc(&e->d_work, sizeof(Work)));
@@ -293,6 +311,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   CU(dalloc(&e->d_ctx, sizeof(TickCtx)));
   CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
   CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
+  CU(dalloc(&e->d_eesd, sizeof(EesdState)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&e->h_sched), sizeof(Sched)));
 
   TickCtx& c = e->h_ctx;
@@ -306,6 +325,8 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.n_layers = md->n_layers;
   c.vocab = md->vocab;
   c.model_stages = e->cfg.S;
+  c.prefill_chunk = kMaxVec;
+  if (const char* v = getenv("PPSD_PREFILL_CHUNK")) c.prefill_chunk = std::min(std::max(atoi(v), 1), (int)kMaxVec);
 
   if (md->kind == PPSD_MODEL_TOYLM) {
     if (md->vocab < 2) return fail(PPSD_EINVAL, "vocab must be >= 2");
@@ -325,7 +346,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     d.ffn = md->ffn_dim;
     d.V = md->vocab;
     d.max_ctx = max_ctx;
-    d.nslot = nslot;
+    d.nslot = e->nbuf;
     d.eps = md->rms_eps;
     d.kv_bf16 = md->kv_bf16;
     if (d.KV <= 0 || d.H % d.KV != 0 || !attn_supported(d.hd, d.H / d.KV))
@@ -337,15 +358,19 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         (need_head && !w->lm_head))
       return fail(PPSD_EINVAL, "missing transformer weights");
     const int Rq = (d.H + 2 * d.KV) * d.hd;
-    const int shapes[5][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d}, {d.d, d.ffn}, {d.V, d.d}};
-    for (int m = 0; m < 5; ++m) {
-      GemvPlan& p = e->gp[m];
-      p.R = shapes[m][0];
-      p.K = shapes[m][1];
-      if (gemv_pick(p.K, p.R, m, &p.vpt, &p.tr, &p.ns, &p.smem) != 0)
-        return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
-                                           std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
-      CU(gemv_set_attrs(p.vpt, m, p.smem));
+    const int shapes[kNumMats][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d},
+                                     {d.d, d.ffn}, {d.V, d.d}, {d.V, d.d}};
+    for (int m = 0; m < kNumMats; ++m) {
+      for (int b = 0; b < 2; ++b) {
+        if ((m == kMatHead && b) || (m == kMatHeadV && !b)) continue;
+        GemvPlan& p = b ? e->gpb[m] : e->gp[m];
+        p.R = shapes[m][0];
+        p.K = shapes[m][1];
+        if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.smem) != 0)
+          return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
+                                             std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
+        CU(gemv_set_attrs(p.vpt, p.m, m, p.smem));
+      }
     }
     {
       AttnArgs aa{};
@@ -387,15 +412,16 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_layers, sizeof(LayerW) * md->n_layers));
     CU(cudaMemcpy(e->d_layers, e->h_layers.data(), sizeof(LayerW) * md->n_layers, cudaMemcpyHostToDevice));
     const int qd = d.H * d.hd;
-    CU(dalloc(&e->d_x, sizeof(float) * (size_t)nslot * d.d));
-    CU(dalloc(&e->d_q, sizeof(float) * (size_t)nslot * qd));
-    CU(dalloc(&e->d_o, sizeof(float) * (size_t)nslot * qd));
-    CU(dalloc(&e->d_h, sizeof(float) * (size_t)nslot * d.ffn));
-    CU(dalloc(&e->d_logits, sizeof(float) * 2 * (size_t)d.V));
-    CU(dalloc(&e->d_attn_part, sizeof(float) * (size_t)nslot * d.H * e->max_pages * (d.hd + 2)));
-    CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * (size_t)nslot * d.KV));
-    CU(dalloc(&e->d_head_part, sizeof(float) * 4 * (size_t)e->num_sms));
-    CU(dalloc(&e->d_head_cnt, sizeof(int32_t)));
+    const size_t nb = (size_t)e->nbuf;
+    CU(dalloc(&e->d_x, sizeof(float) * nb * d.d));
+    CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
+    CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
+    CU(dalloc(&e->d_h, sizeof(float) * nb * d.ffn));
+    CU(dalloc(&e->d_logits, sizeof(float) * kMaxVec * (size_t)d.V));
+    CU(dalloc(&e->d_attn_part, sizeof(float) * nb * d.H * e->max_pages * (d.hd + 2)));
+    CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * nb * d.KV));
+    CU(dalloc(&e->d_head_part, sizeof(float) * 2 * kMaxVec * (size_t)e->num_sms));
+    CU(dalloc(&e->d_head_cnt, sizeof(int32_t) * kMaxVec));
     c.x = e->d_x;
   } else if (md->kind != PPSD_MODEL_BERNOULLI) {
     return fail(PPSD_EINVAL, "unknown model kind");
@@ -453,16 +479,17 @@ static int upload_prompt(ppsd_engine* e, const int32_t* prompt, int n_prompt) {
 static int prefill(ppsd_engine* e, int n_prompt, double* ms, int64_t* launches) {
   *ms = 0;
   if (e->md.kind != PPSD_MODEL_TRANSFORMER || n_prompt < 2) return PPSD_OK;
-  ArCtl ctl{0, e->first_local_layer, e->n_local_layers, 0};
+  ArCtl ctl{0, e->first_local_layer, e->n_local_layers, n_prompt - 1};
   CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
   CU(cudaEventRecord(e->ev0, e->st));
-  for (int i = 0; i < n_prompt - 1; ++i) CU(cudaGraphLaunch(e->g_prefill, e->st));
+  const int chunks = (n_prompt - 1 + e->h_ctx.prefill_chunk - 1) / e->h_ctx.prefill_chunk;
+  for (int i = 0; i < chunks; ++i) CU(cudaGraphLaunch(e->g_prefill, e->st));
   CU(cudaEventRecord(e->ev1, e->st));
   CU(cudaEventSynchronize(e->ev1));
   float f = 0;
   CU(cudaEventElapsedTime(&f, e->ev0, e->ev1));
   *ms = f;
-  *launches += (int64_t)(n_prompt - 1) * e->prefill_launches;
+  *launches += (int64_t)chunks * e->prefill_launches;
   return PPSD_OK;
 }
 
@@ -651,9 +678,163 @@ extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* pro
   return PPSD_OK;
 }
 
-extern "C" int ppsd_decode_eesd(ppsd_engine*, int32_t, const int32_t*, int32_t, int32_t, int32_t*, int32_t,
-                                ppsd_metrics*, ppsd_trace_row*, int64_t, int64_t*) {
-  return fail(PPSD_EUNSUPPORTED, "EESD baseline not implemented yet");
+// ---------------------------------------------------------------------------
+// EESD draft-then-verify baseline (pipesim.py:435-551)
+
+static int eesd_graph(ppsd_engine* e, int gamma, cudaGraphExec_t* out, int64_t* nlaunch) {
+  auto it = e->eesd_graphs.find(gamma);
+  if (it != e->eesd_graphs.end()) {
+    *out = it->second.first;
+    *nlaunch = it->second.second;
+    return PPSD_OK;
+  }
+  const TickCtx* ctx = e->d_ctx;
+  EesdState* es = e->d_eesd;
+  const int exit_layer = e->cfg.stage_first[e->cfg.k + 1];
+  cudaGraphExec_t g = nullptr;
+  int64_t n = 0;
+  int rc = capture(
+      e,
+      [&]() -> int {
+        int cnt = 0;
+        if (e->md.kind != PPSD_MODEL_TRANSFORMER) {
+          if (launch_pdl(eesd_toy_round_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
+          return 1;
+        }
+        for (int h = 0; h < gamma; ++h) {  // gamma one-token drafts through the exit layers
+          if (launch_pdl(eesd_draft_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
+          const int m = enqueue_layers(e, e->d_work_ar, exit_layer);
+          if (m < 0) return -1;
+          if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
+          if (launch_pdl(eesd_draft_end_kernel, dim3(1), dim3(32), 0, e->st, ctx, es) != cudaSuccess) return -1;
+          cnt += m + 3;
+        }
+        if (launch_pdl(eesd_verify_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
+        const int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);  // batched verify
+        if (m < 0) return -1;
+        if (enqueue_gemv(e, e->d_work_ar, 0, kMatHeadV, true) != cudaSuccess) return -1;
+        if (launch_pdl(eesd_scan_kernel, dim3(1), dim3(32), 0, e->st, ctx, es) != cudaSuccess) return -1;
+        return cnt + m + 3;
+      },
+      &g, &n);
+  if (rc) return rc;
+  e->eesd_graphs[gamma] = {g, n};
+  *out = g;
+  *nlaunch = n;
+  return PPSD_OK;
+}
+
+static int run_eesd(ppsd_engine* e, int model, int gamma, const int32_t* prompt, int n_prompt, int horizon,
+                    double alpha, uint64_t verify_seed, int32_t* out_tokens, int32_t out_cap, ppsd_metrics* out,
+                    ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (e->lo != 1 || e->hi != e->S) return fail(PPSD_EINVAL, "engine holds a stage subset");
+  if (gamma < 1) return fail(PPSD_EINVAL, "gamma must be >= 1");
+  if (horizon < 1) return fail(PPSD_EINVAL, "horizon must be >= 1");
+  if (model && e->md.kind == PPSD_MODEL_TRANSFORMER && gamma + 1 > kMaxVec)
+    return fail(PPSD_EUNSUPPORTED, "gamma + 1 must be <= 16 for the batched verify");
+  if (model && (int64_t)n_prompt + horizon + gamma + 2 > e->md.max_ctx)
+    return fail(PPSD_EINVAL, "prompt + horizon exceeds the engine's max_ctx");
+  memset(out, 0, sizeof(*out));
+  CU(cudaSetDevice(e->device));
+  cudaGraphExec_t g;
+  int64_t per_round = 0;
+  int rc = eesd_graph(e, gamma, &g, &per_round);
+  if (rc) return rc;
+  int64_t launches = 0;
+  double pre_ms = 0;
+  if (model) {
+    rc = upload_prompt(e, prompt, n_prompt);
+    if (rc) return rc;
+    rc = prefill(e, n_prompt, &pre_ms, &launches);
+    if (rc) return rc;
+  }
+  const int rows_per_round = 2 * gamma + e->S + 1;
+  int64_t cap = (int64_t)horizon * rows_per_round + 8;
+  if (trace) {
+    if (trace_cap < cap) cap = trace_cap;
+    rc = ensure_trace(e, cap);
+    if (rc) return rc;
+  }
+  EesdState st{};
+  st.gamma = gamma;
+  st.k = e->cfg.k;
+  st.S = e->S;
+  st.per = e->cfg.per;
+  st.dt = st.k == 1 ? 1 : st.k * st.per;  // pipesim.py:456
+  st.n_prompt = n_prompt;
+  st.horizon = horizon;
+  st.n_layers = e->md.n_layers;
+  st.exit_layer = e->cfg.stage_first[st.k + 1];
+  st.model = model;
+  st.alpha = alpha;
+  st.verify_seed = verify_seed;
+  st.len = n_prompt;
+  e->h_ctx.trace = trace ? e->d_trace : nullptr;
+  e->h_ctx.trace_cap = cap;
+  e->h_ctx.inbox = nullptr;
+  e->h_ctx.outbox = nullptr;
+  CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_eesd, &st, sizeof(EesdState), cudaMemcpyHostToDevice, e->st));
+  CU(cudaEventRecord(e->ev0, e->st));
+  int64_t rounds = 0;
+  for (;;) {
+    const int64_t n = std::max<int64_t>(1, (horizon - st.committed + gamma) / (gamma + 1));
+    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(g, e->st));
+    rounds += n;
+    CU(cudaMemcpyAsync(&st, e->d_eesd, sizeof(EesdState), cudaMemcpyDeviceToHost, e->st));
+    CU(cudaStreamSynchronize(e->st));
+    if (st.error || st.done) break;
+    if (rounds > (int64_t)horizon + 4) return fail(PPSD_ESTATE, "EESD rounds did not converge");
+  }
+  CU(cudaEventRecord(e->ev1, e->st));
+  CU(cudaEventSynchronize(e->ev1));
+  if (st.error & kErrTrace) return fail(PPSD_ESTATE, "trace buffer too small");
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  out->committed_tokens = st.committed;
+  out->ticks = st.t;
+  out->accepts = st.accepts;
+  out->rejects = st.rejects;
+  out->alpha_valid = st.drafted > 0;
+  out->alpha_all_measured = st.drafted > 0 ? (double)st.accepts / st.drafted : 0.0;  // pipesim.py:272
+  out->throughput = st.t > 0 ? (double)st.committed / st.t : 0.0;
+  out->speedup_vs_ar = out->throughput * (double)(e->S * e->cfg.per);
+  out->decode_ms = ms;
+  out->prefill_ms = pre_ms;
+  out->gpu_launches = launches + rounds * per_round;
+  if (out_tokens && model) {
+    const int n = std::min<int>(out_cap, st.committed);
+    if (n > 0) CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  }
+  if (trace) {
+    const int64_t nr = std::min<int64_t>(st.trace_n, cap);
+    if (nr > 0) CU(cudaMemcpy(trace, e->d_trace, sizeof(TraceRow) * nr, cudaMemcpyDeviceToHost));
+    if (trace_len) *trace_len = nr;
+  } else if (trace_len) {
+    *trace_len = 0;
+  }
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32_t n_prompt,
+                                int32_t horizon, int32_t* out_tokens, int32_t out_cap, ppsd_metrics* out,
+                                ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines run ppsd_simulate_eesd");
+  int rc = check_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  return run_eesd(e, 1, gamma, prompt, n_prompt, horizon, 0.0, 0, out_tokens, out_cap, out, trace, trace_cap,
+                  trace_len);
+}
+
+extern "C" int ppsd_simulate_eesd(ppsd_engine* e, int32_t gamma, double alpha, uint64_t verify_seed,
+                                  int32_t horizon, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                                  int64_t* trace_len) {
+  if (!e || !out) return fail(PPSD_EINVAL, "null argument");
+  if (e->md.kind != PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "ppsd_simulate_eesd needs a Bernoulli engine");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(PPSD_EINVAL, "BERNOULLI oracle needs alpha in [0, 1]");
+  return run_eesd(e, 0, gamma, nullptr, 0, horizon, alpha, verify_seed, nullptr, 0, out, trace, trace_cap,
+                  trace_len);
 }
 
 // ---------------------------------------------------------------------------
@@ -688,13 +869,14 @@ extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t
 extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps, double* avg_ms,
                                double* bytes_per_launch) {
   if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "probe needs a transformer engine");
-  if (which < 0 || which > 4 || reps < 1) return fail(PPSD_EINVAL, "bad probe arguments");
+  if (which < 0 || which > kMatHead || reps < 1) return fail(PPSD_EINVAL, "bad probe arguments");
   const int G = e->hi - e->lo + 1;
   if (n_groups < 1 || n_groups > G || n_groups > e->cfg.nslot) return fail(PPSD_EINVAL, "bad n_groups");
   CU(cudaSetDevice(e->device));
   Work w{};
   w.G = n_groups;
   for (int g = 0; g < n_groups; ++g) {
+    w.nv[g] = 1;
     w.slot[g] = g;
     w.pos[g] = 0;
     w.first[g] = e->cfg.stage_first[e->lo + g];

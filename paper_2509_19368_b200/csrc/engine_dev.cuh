@@ -35,6 +35,7 @@ struct TickCtx {
   int32_t owner_k, owner_S, owner_prev;  // ranks owning the exit stage, stage S, stage lo-1
   int32_t n_prompt;
   int32_t model_stages;  // S
+  int32_t prefill_chunk; // prompt tokens per batched prefill launch (<= kMaxVec)
 };
 
 constexpr int kBoxHeader = 4;
@@ -43,7 +44,17 @@ struct ArCtl {
   int32_t j;           // token index being processed
   int32_t first_layer; // first local layer
   int32_t n_layers;    // local layer count
-  int32_t pad;
+  int32_t end;         // batched prefill: tokens [0, end) are processed
+};
+
+// Draft-then-verify (EESD) round machine, pkg/src/specpipe/pipesim.py:435-551.
+struct EesdState {
+  int32_t gamma, k, S, per, dt, n_prompt, horizon, n_layers, exit_layer, model;
+  double alpha;          // Bernoulli verdicts
+  uint64_t verify_seed;
+  uint64_t verify_counter;
+  int32_t t, committed, accepts, rejects, drafted, done, error, len;  // len = sequence length
+  int64_t trace_n;
 };
 
 __global__ void sched_tick_kernel(const TickCtx* ctxp, int begin);
@@ -53,6 +64,12 @@ __global__ void toy_tick_kernel(const TickCtx* ctxp);
 __global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
 __global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);
+__global__ void prefill_chunk_kernel(const TickCtx* ctxp, ArCtl* ctl);
+__global__ void eesd_draft_begin_kernel(const TickCtx* ctxp, EesdState* es);
+__global__ void eesd_draft_end_kernel(const TickCtx* ctxp, EesdState* es);
+__global__ void eesd_verify_begin_kernel(const TickCtx* ctxp, EesdState* es);
+__global__ void eesd_scan_kernel(const TickCtx* ctxp, EesdState* es);
+__global__ void eesd_toy_round_kernel(const TickCtx* ctxp, EesdState* es);
 __global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long rows, long long cols,
                                    uint64_t b0, uint64_t b1, uint64_t b2, float a0, float a1, float a2,
                                    int H, int KV, int hd);

@@ -80,10 +80,14 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
 
 template <int VPT, int TR, int M, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
-  constexpr int NV = M * TR;  // row partials per thread per stage
+  constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
+  constexpr bool kHeadV = EPI == kMatHeadV;  // final head on the vectors of group 0
+  constexpr bool kHead = kHead2 || kHeadV;
+  constexpr int NV = M * TR;                 // row partials per thread per stage
   constexpr int CHT = (128 / TR) < 1 ? 1 : (128 / TR);  // tiles per deferred epilogue
+  constexpr int kMaxProb = 128;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ int s_prob[kMaxStages];
+  __shared__ int s_pg[kMaxProb], s_pv[kMaxProb];  // problem = (group, first vector)
   __shared__ int s_np;
   __shared__ float s_ss[8][M];
   __shared__ float s_bv[8][M];
@@ -101,11 +105,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   if (!a.desc_early) pdl_wait();
   if (tid == 0) {
     int np = 0;
-    if (EPI == kMatHead) {
-      np = (work->head_slot[0] >= 0 || work->head_slot[1] >= 0) ? 1 : 0;
+    if (kHead2) {
+      if (work->head_slot[0] >= 0 || work->head_slot[1] >= 0) { s_pg[0] = -1; s_pv[0] = 0; np = 1; }
+    } else if (kHeadV) {
+      if (work->G >= 1 && work->slot[0] >= 0)
+        for (int v0 = 0; v0 < work->nv[0] && np < kMaxProb; v0 += M) { s_pg[np] = 0; s_pv[np++] = v0; }
     } else {
       for (int g = 0; g < work->G; ++g)
-        if (work->slot[g] >= 0 && a.layer_i < work->nl[g]) s_prob[np++] = g;
+        if (work->slot[g] >= 0 && a.layer_i < work->nl[g])
+          for (int v0 = 0; v0 < work->nv[g] && np < kMaxProb; v0 += M) { s_pg[np] = g; s_pv[np++] = v0; }
     }
     s_np = np;
     for (int i = 0; i < NS; ++i) {
@@ -122,9 +130,22 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     return;
   }
   const int tpp = R / TR;
-  const long long T = (long long)np * tpp;
-  const long long t0 = T * blockIdx.x / gridDim.x;
-  const long long t1 = T * (blockIdx.x + 1) / gridDim.x;
+  long long t0, t1;
+  int hv_p = 0, hv_c0 = 0, hv_c1 = 0;  // kHeadV: this CTA's problem and its CTA span
+  if (kHeadV) {
+    // CTAs are split between problems so no CTA spans two vector chunks
+    const int G = gridDim.x, b = blockIdx.x;
+    while (hv_p + 1 < np && (hv_p + 1) * G / np <= b) ++hv_p;
+    hv_c0 = hv_p * G / np;
+    hv_c1 = (hv_p + 1) * G / np;
+    const int nc = hv_c1 - hv_c0, bl = b - hv_c0;
+    t0 = (long long)hv_p * tpp + (long long)tpp * bl / nc;
+    t1 = (long long)hv_p * tpp + (long long)tpp * (bl + 1) / nc;
+  } else {
+    const long long T = (long long)np * tpp;
+    t0 = T * blockIdx.x / gridDim.x;
+    t1 = T * (blockIdx.x + 1) / gridDim.x;
+  }
   const int ntiles = (int)(t1 - t0);
 
   if (warp == 8) {  // ---------------- producer ----------------
@@ -138,10 +159,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         const int tile = (int)(t - (long long)p * tpp);
         if (p != cur_p) {
           const __nv_bfloat16* w;
-          if (EPI == kMatHead) {
+          if (kHead) {
             w = a.head_w;
           } else {
-            const LayerW& L = a.layers[work->first[s_prob[p]] + a.layer_i];
+            const LayerW& L = a.layers[work->first[s_pg[p]] + a.layer_i];
             w = EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;
           }
           wb = reinterpret_cast<const unsigned char*>(w);
@@ -163,12 +184,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   float bestv[M];
   int besti[M];
   bool mact[M];
+  int vslot[M], vpos[M];  // per vector of the current problem
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     bestv[m] = -FLT_MAX;
     besti[m] = INT_MAX;
-    mact[m] = EPI == kMatHead ? work->head_slot[m] >= 0 : true;
+    mact[m] = false;
+    vslot[m] = vpos[m] = 0;
   }
+  int cur_v0 = 0;
+  int chunk_n0 = 0;  // first tile of the current (not yet flushed) epilogue chunk
 
   if (ntiles > 0) {
     const int nvec = K >> 3;
@@ -177,26 +202,38 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     for (int n = 0; n < ntiles; ++n) {
       const long long t = t0 + n;
       const int p = (int)(t / tpp);
-      if (p != cur_p) {  // load + normalise this problem's input slice
+      if (p != cur_p) {  // load + normalise this problem's input vectors
         cur_p = p;
         const float* nw[M];
         const float* src[M];
+        const int g = s_pg[p];
+        cur_v0 = s_pv[p];
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           nw[m] = nullptr;
           src[m] = nullptr;
-          if (EPI == kMatHead) {
+          if (kHead2) {
             const int s = work->head_slot[m];
+            mact[m] = s >= 0;
+            vslot[m] = s;
             nw[m] = m == 0 ? a.head_norm0 : a.head_norm1;
             src[m] = s >= 0 ? a.x + (size_t)s * a.dm.d : nullptr;
           } else {
-            const int g = s_prob[p];
-            const int s = work->slot[g];
-            const LayerW& L = a.layers[work->first[g] + a.layer_i];
-            if (EPI == kMatQKV) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.attn_norm; }
-            if (EPI == kMatGU) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.mlp_norm; }
-            if (EPI == kMatO) src[m] = a.o + (size_t)s * a.dm.H * a.dm.hd;
-            if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn;
+            mact[m] = cur_v0 + m < work->nv[g];
+            vslot[m] = work->slot[g] + cur_v0 + m;
+            vpos[m] = work->pos[g] + cur_v0 + m;
+            if (!mact[m]) continue;
+            const int s = vslot[m];
+            if (kHeadV) {
+              src[m] = a.x + (size_t)s * a.dm.d;
+              nw[m] = a.head_norm1;
+            } else {
+              const LayerW& L = a.layers[work->first[g] + a.layer_i];
+              if (EPI == kMatQKV) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.attn_norm; }
+              if (EPI == kMatGU) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.mlp_norm; }
+              if (EPI == kMatO) src[m] = a.o + (size_t)s * a.dm.H * a.dm.hd;
+              if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn;
+            }
           }
         }
 #pragma unroll
@@ -275,14 +312,18 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           }
         }
       }
-      const int ct = n % CHT;
+      const int ct = n - chunk_n0;
       const float s = transpose_reduce<NV>(acc, lane);
       constexpr int kShift = 5 - ilog2(NV);
       if ((lane & ((1 << kShift) - 1)) == 0) red[(ct * 8 + warp) * NV + (lane >> kShift)] = s;
 
-      if (ct == CHT - 1 || n == ntiles - 1) {  // deferred epilogue over CHT tiles
+      // deferred epilogue over CHT tiles (or at a problem boundary: the
+      // per-vector state above belongs to the current problem)
+      const bool last_of_problem = (n == ntiles - 1) || ((t0 + n + 1) / tpp != p);
+      if (ct == CHT - 1 || last_of_problem) {
         named_bar_sync(1, kGemvConsumers);
-        const int n0 = n - ct;
+        const int n0 = chunk_n0;
+        chunk_n0 = n + 1;
         const int nrows = (ct + 1) * TR;
         auto rowsum = [&](int rl, int m) {
           const int tt = rl / TR, r = rl % TR;
@@ -294,49 +335,51 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         if (EPI == kMatQKV || EPI == kMatGU) {
           for (int pr = tid; pr < nrows / 2; pr += kGemvConsumers) {
             const int rl = pr * 2;
-            const float y0 = rowsum(rl, 0), y1 = rowsum(rl + 1, 0);
             const long long tg = t0 + n0 + rl / TR;
-            const int pp = (int)(tg / tpp);
-            const int rr = (int)(tg - (long long)pp * tpp) * TR + rl % TR;
-            const int g = s_prob[pp];
-            const int slot = work->slot[g], pos = work->pos[g];
-            if (EPI == kMatGU) {
-              a.h[(size_t)slot * a.dm.ffn + (rr >> 1)] = y0 / (1.0f + expf(-y0)) * y1;
-            } else {
-              const int H = a.dm.H, KVh = a.dm.KV, hd = a.dm.hd;
-              const LayerW& L = a.layers[work->first[g] + a.layer_i];
-              const int head = rr / hd, w = rr - head * hd;
-              float o0 = y0, o1 = y1;
-              void* cache = nullptr;
-              int kvh = 0;
-              if (head < H + KVh) {
-                const int half = hd >> 1;
-                const float c = a.rope_cos[(size_t)pos * half + (w >> 1)];
-                const float sn = a.rope_sin[(size_t)pos * half + (w >> 1)];
-                o0 = y0 * c - y1 * sn;
-                o1 = y1 * c + y0 * sn;
-                if (head < H) {
-                  float* q = a.q + (size_t)slot * H * hd + head * hd + w;
-                  q[0] = o0;
-                  q[1] = o1;
-                } else {
-                  cache = L.kc;
-                  kvh = head - H;
-                }
+            const int rr = (int)(tg - (long long)p * tpp) * TR + rl % TR;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (!mact[m]) continue;
+              const float y0 = rowsum(rl, m), y1 = rowsum(rl + 1, m);
+              const int slot = vslot[m], pos = vpos[m];
+              if (EPI == kMatGU) {
+                a.h[(size_t)slot * a.dm.ffn + (rr >> 1)] = y0 / (1.0f + expf(-y0)) * y1;
               } else {
-                cache = L.vc;
-                kvh = head - H - KVh;
-              }
-              if (cache) {
-                const int page = a.page_table[pos / kPage];
-                const size_t off = (((size_t)page * KVh + kvh) * kPage + (pos % kPage)) * hd + w;
-                if (a.dm.kv_bf16) {
-                  *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) =
-                      __floats2bfloat162_rn(o0, o1);
+                const int H = a.dm.H, KVh = a.dm.KV, hd = a.dm.hd;
+                const LayerW& L = a.layers[work->first[s_pg[p]] + a.layer_i];
+                const int head = rr / hd, w = rr - head * hd;
+                float o0 = y0, o1 = y1;
+                void* cache = nullptr;
+                int kvh = 0;
+                if (head < H + KVh) {
+                  const int half = hd >> 1;
+                  const float c = a.rope_cos[(size_t)pos * half + (w >> 1)];
+                  const float sn = a.rope_sin[(size_t)pos * half + (w >> 1)];
+                  o0 = y0 * c - y1 * sn;
+                  o1 = y1 * c + y0 * sn;
+                  if (head < H) {
+                    float* q = a.q + (size_t)slot * H * hd + head * hd + w;
+                    q[0] = o0;
+                    q[1] = o1;
+                  } else {
+                    cache = L.kc;
+                    kvh = head - H;
+                  }
                 } else {
-                  float* cp = reinterpret_cast<float*>(cache) + off;
-                  cp[0] = o0;
-                  cp[1] = o1;
+                  cache = L.vc;
+                  kvh = head - H - KVh;
+                }
+                if (cache) {
+                  const int page = a.page_table[pos / kPage];
+                  const size_t off = (((size_t)page * KVh + kvh) * kPage + (pos % kPage)) * hd + w;
+                  if (a.dm.kv_bf16) {
+                    *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) =
+                        __floats2bfloat162_rn(o0, o1);
+                  } else {
+                    float* cp = reinterpret_cast<float*>(cache) + off;
+                    cp[0] = o0;
+                    cp[1] = o1;
+                  }
                 }
               }
             }
@@ -344,23 +387,21 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         } else {
           for (int rl = tid; rl < nrows; rl += kGemvConsumers) {
             const long long tg = t0 + n0 + rl / TR;
-            const int pp = (int)(tg / tpp);
-            const int rr = (int)(tg - (long long)pp * tpp) * TR + rl % TR;
-            if (EPI == kMatHead) {
+            const int rr = (int)(tg - (long long)p * tpp) * TR + rl % TR;
 #pragma unroll
-              for (int m = 0; m < M; ++m) {
-                if (!mact[m]) continue;
-                const float y = rowsum(rl, m);
-                a.logits[(size_t)m * a.dm.V + rr] = y;
+            for (int m = 0; m < M; ++m) {
+              if (!mact[m]) continue;
+              const float y = rowsum(rl, m);
+              if (kHead) {
+                const int vi = kHead2 ? m : cur_v0 + m;
+                a.logits[(size_t)vi * a.dm.V + rr] = y;
                 if (y > bestv[m]) {  // rows ascend per thread: strict > keeps first index
                   bestv[m] = y;
                   besti[m] = rr;
                 }
+              } else {
+                a.x[(size_t)vslot[m] * a.dm.d + rr] += y;
               }
-            } else {
-              const float y = rowsum(rl, 0);
-              const int slot = work->slot[s_prob[pp]];
-              a.x[(size_t)slot * a.dm.d + rr] += y;
             }
           }
         }
@@ -369,7 +410,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
   }
 
-  if (EPI == kMatHead) {  // deterministic first-index argmax across the grid
+  if (kHead) {  // deterministic first-index argmax across the CTAs of each problem
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       float v = bestv[m];
@@ -384,29 +425,35 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     }
     named_bar_sync(1, kGemvConsumers);
     if (tid == 0) {
+      // kHead2: one problem over the whole grid; kHeadV: this CTA's problem span
+      const int v0 = kHeadV ? s_pv[hv_p] : 0;
+      const int c0 = kHeadV ? hv_c0 : 0, c1 = kHeadV ? hv_c1 : (int)gridDim.x;
+      int* ticket = a.head_cnt + (kHeadV ? hv_p : 0);
       for (int m = 0; m < M; ++m) {
         float v = s_bv[0][m];
         int i = s_bi[0][m];
         for (int w = 1; w < 8; ++w)
           if (better(s_bv[w][m], s_bi[w][m], v, i)) { v = s_bv[w][m]; i = s_bi[w][m]; }
-        a.head_part[((size_t)blockIdx.x * 2 + m) * 2 + 0] = v;
-        a.head_part[((size_t)blockIdx.x * 2 + m) * 2 + 1] = __int_as_float(i);
+        a.head_part[((size_t)blockIdx.x * kMaxVec + v0 + m) * 2 + 0] = v;
+        a.head_part[((size_t)blockIdx.x * kMaxVec + v0 + m) * 2 + 1] = __int_as_float(i);
       }
       __threadfence();
-      if (atomicAdd(a.head_cnt, 1) == (int)gridDim.x - 1) {
+      if (atomicAdd(ticket, 1) == c1 - c0 - 1) {
         __threadfence();
         Work* wk = const_cast<Work*>(work);
+        const int nv0 = kHeadV ? work->nv[0] : 0;
         for (int m = 0; m < M; ++m) {
           float v = -FLT_MAX;
           int i = INT_MAX;
-          for (int b = 0; b < (int)gridDim.x; ++b) {
-            const float bv = __ldcg(&a.head_part[((size_t)b * 2 + m) * 2 + 0]);
-            const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * 2 + m) * 2 + 1]));
+          for (int b = c0; b < c1; ++b) {
+            const float bv = __ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 0]);
+            const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 1]));
             if (better(bv, bi, v, i)) { v = bv; i = bi; }
           }
-          wk->head_out[m] = mact[m] ? i : -1;
+          if (kHead2) wk->head_out[m] = work->head_slot[m] >= 0 ? i : -1;
+          else if (v0 + m < nv0) wk->vec_out[v0 + m] = i;
         }
-        *a.head_cnt = 0;
+        *ticket = 0;
       }
     }
   }
@@ -419,86 +466,104 @@ namespace {
 constexpr int kVpts[] = {1, 2, 3, 4, 6, 7, 8, 14};
 constexpr size_t kRingBudget = 212 * 1024;
 
-// rows per stage: ~64-96 KB bulk copies (tools/stream_bench.cu)
-constexpr int tr_for(int vpt) {
-  return vpt == 1 ? 16 : vpt <= 3 ? 8 : vpt <= 6 ? 4 : vpt <= 8 ? 2 : 1;
+// rows per stage: ~64-96 KB bulk copies at M=1 (tools/stream_bench.cu);
+// fewer rows when M vectors' input slices must also live in registers
+constexpr int tr_for(int vpt, int m) {
+  if (m == 1) return vpt == 1 ? 16 : vpt <= 3 ? 8 : vpt <= 6 ? 4 : vpt <= 8 ? 2 : 1;
+  if (m == 2) return vpt <= 2 ? 8 : vpt <= 4 ? 4 : 1;
+  return vpt == 1 ? 8 : vpt == 2 ? 4 : 2;  // m == 4
 }
+// vectors per weight pass of the batched (prefill / EESD) plans
+constexpr int m_batched(int vpt) { return vpt <= 4 ? 4 : vpt <= 8 ? 2 : 1; }
 
-template <int VPT, int EPI>
+template <int VPT, int M, int EPI>
 cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only) {
-  constexpr int TR = tr_for(VPT);
-  constexpr int M = EPI == kMatHead ? 2 : 1;
+  constexpr int TR = tr_for(VPT, M);
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return launch_pdl(fn, dim3(grid), dim3(kGemvThreads), smem, st, a);
 }
 
-template <int VPT>
-cudaError_t launch_vpt(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only,
-                       int mat) {
-  // only the instantiations gemv_pick can select: the fused pair epilogues
-  // need TR >= 2; the head runs on K = d_model <= 8192 (VPT <= 4)
-  if (mat == kMatO) return launch_one<VPT, kMatO>(a, smem, grid, st, attrs_only);
-  if (mat == kMatDown) return launch_one<VPT, kMatDown>(a, smem, grid, st, attrs_only);
-  if constexpr (tr_for(VPT) >= 2) {
-    if (mat == kMatQKV) return launch_one<VPT, kMatQKV>(a, smem, grid, st, attrs_only);
-    if (mat == kMatGU) return launch_one<VPT, kMatGU>(a, smem, grid, st, attrs_only);
+template <int VPT, int M>
+cudaError_t launch_vm(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only, int mat) {
+  if constexpr (M == 2 && VPT <= 4) {  // the PPSD tick head (exit + final)
+    if (mat == kMatHead) return launch_one<VPT, 2, kMatHead>(a, smem, grid, st, attrs_only);
   }
-  if constexpr (VPT <= 4) {
-    if (mat == kMatHead) return launch_one<VPT, kMatHead>(a, smem, grid, st, attrs_only);
+  if constexpr ((M == 1) || (M == m_batched(VPT))) {
+    if (mat == kMatO) return launch_one<VPT, M, kMatO>(a, smem, grid, st, attrs_only);
+    if (mat == kMatDown) return launch_one<VPT, M, kMatDown>(a, smem, grid, st, attrs_only);
+    if constexpr (tr_for(VPT, M) >= 2) {  // row-pair epilogues
+      if (mat == kMatQKV) return launch_one<VPT, M, kMatQKV>(a, smem, grid, st, attrs_only);
+      if (mat == kMatGU) return launch_one<VPT, M, kMatGU>(a, smem, grid, st, attrs_only);
+    }
+    if constexpr (M == 4) {
+      if (mat == kMatHeadV) return launch_one<VPT, 4, kMatHeadV>(a, smem, grid, st, attrs_only);
+    }
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t dispatch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st, bool attrs_only,
+template <int VPT>
+cudaError_t launch_vpt(const GemvArgs& a, int m, size_t smem, int grid, cudaStream_t st, bool attrs_only,
+                       int mat) {
+  switch (m) {
+    case 1: return launch_vm<VPT, 1>(a, smem, grid, st, attrs_only, mat);
+    case 2: return launch_vm<VPT, 2>(a, smem, grid, st, attrs_only, mat);
+    case 4: return launch_vm<VPT, 4>(a, smem, grid, st, attrs_only, mat);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t dispatch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st, bool attrs_only,
                      int mat) {
   switch (vpt) {
-    case 1: return launch_vpt<1>(a, smem, grid, st, attrs_only, mat);
-    case 2: return launch_vpt<2>(a, smem, grid, st, attrs_only, mat);
-    case 3: return launch_vpt<3>(a, smem, grid, st, attrs_only, mat);
-    case 4: return launch_vpt<4>(a, smem, grid, st, attrs_only, mat);
-    case 6: return launch_vpt<6>(a, smem, grid, st, attrs_only, mat);
-    case 7: return launch_vpt<7>(a, smem, grid, st, attrs_only, mat);
-    case 8: return launch_vpt<8>(a, smem, grid, st, attrs_only, mat);
-    case 14: return launch_vpt<14>(a, smem, grid, st, attrs_only, mat);
+    case 1: return launch_vpt<1>(a, m, smem, grid, st, attrs_only, mat);
+    case 2: return launch_vpt<2>(a, m, smem, grid, st, attrs_only, mat);
+    case 3: return launch_vpt<3>(a, m, smem, grid, st, attrs_only, mat);
+    case 4: return launch_vpt<4>(a, m, smem, grid, st, attrs_only, mat);
+    case 6: return launch_vpt<6>(a, m, smem, grid, st, attrs_only, mat);
+    case 7: return launch_vpt<7>(a, m, smem, grid, st, attrs_only, mat);
+    case 8: return launch_vpt<8>(a, m, smem, grid, st, attrs_only, mat);
+    case 14: return launch_vpt<14>(a, m, smem, grid, st, attrs_only, mat);
   }
   return cudaErrorInvalidValue;
 }
 }  // namespace
 
-// Choose the (VPT, TR, NS) instantiation for a [R][K] matrix; 0 on success.
-int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* smem) {
+// Choose the (VPT, TR, M, NS) instantiation for a [R][K] matrix; 0 on success.
+int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, size_t* smem) {
   if (K % 8 != 0 || K <= 0 || R <= 0) return -1;
   const int need = (K + 8 * kGemvConsumers - 1) / (8 * kGemvConsumers);
   int v = -1;
   for (int c : kVpts)
     if (c >= need) { v = c; break; }
   if (v < 0) return -1;
-  const int t = tr_for(v);
+  const int mm = mat == kMatHead ? 2 : mat == kMatHeadV ? 4 : batched ? m_batched(v) : 1;
+  if ((mat == kMatHead || mat == kMatHeadV) && v > 4) return -1;
+  const int t = tr_for(v, mm);
   if (R % t != 0) return -1;
   if ((mat == kMatQKV || mat == kMatGU) && t < 2) return -1;
-  if (mat == kMatHead && v > 4) return -1;
-  const int M = mat == kMatHead ? 2 : 1;
   const int cht = 128 / t < 1 ? 1 : 128 / t;
   const size_t stage = (size_t)t * K * 2;
-  const size_t red = (size_t)cht * 8 * M * t * 4;
+  const size_t red = (size_t)cht * 8 * mm * t * 4;
   int ns = (int)((kRingBudget - red) / stage);
   if (ns > 6) ns = 6;
   if (ns < 2) return -1;
   *vpt = v;
   *tr = t;
+  *m = mm;
   *nstage = ns;
   *smem = stage * ns + red + 2 * ns * sizeof(uint64_t);
   return 0;
 }
 
-cudaError_t gemv_set_attrs(int vpt, int mat, size_t smem) {
+cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem) {
   GemvArgs dummy{};
-  return dispatch(dummy, vpt, smem, 0, 0, true, mat);
+  return dispatch(dummy, vpt, m, smem, 0, 0, true, mat);
 }
 
-cudaError_t gemv_launch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st) {
-  return dispatch(a, vpt, smem, grid, st, false, a.mat);
+cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st) {
+  return dispatch(a, vpt, m, smem, grid, st, false, a.mat);
 }
 
 }  // namespace ppsd

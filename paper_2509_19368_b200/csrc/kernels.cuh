@@ -11,7 +11,7 @@ namespace ppsd {
 constexpr int kPage = 64;          // KV page = attention chunk (tokens)
 constexpr int kGemvConsumers = 256;  // 8 consumer warps
 constexpr int kGemvThreads = 288;    // + 1 bulk-copy producer warp
-constexpr int kGemvChunkTiles = 16;  // tiles per deferred epilogue batch
+constexpr int kMaxVec = 16;         // vectors per group (batched prefill / EESD verify)
 
 // Per-tick local work: one group per local pipeline stage. Written by the
 // scheduler kernel at the start of every tick, read by every layer kernel.
@@ -21,8 +21,11 @@ struct Work {
   int32_t pos[kMaxStages];      // token index the chain processes (RoPE / KV index)
   int32_t first[kMaxStages];    // global index of the stage's first layer
   int32_t nl[kMaxStages];       // layers in the stage
+  int32_t nv[kMaxStages];       // vectors (consecutive slots / positions) in the group: 1 per
+                                // pipeline chain; >1 for batched prefill and EESD verify
   int32_t head_slot[2];         // [0] exit head input slot, [1] final head input slot
   int32_t head_out[2];          // argmax written by the head kernel
+  int32_t vec_out[kMaxVec];     // kMatHeadV: argmax of each vector of group 0 (final head)
 };
 
 struct LayerW {
@@ -42,7 +45,8 @@ struct Dims {
   int32_t kv_bf16;
 };
 
-enum : int { kMatQKV = 0, kMatO = 1, kMatGU = 2, kMatDown = 3, kMatHead = 4 };
+enum : int { kMatQKV = 0, kMatO = 1, kMatGU = 2, kMatDown = 3, kMatHead = 4, kMatHeadV = 5 };
+constexpr int kNumMats = 6;
 
 struct GemvArgs {
   Work* work;
@@ -63,8 +67,8 @@ struct GemvArgs {
   const float* rope_cos;
   const float* rope_sin;
   const int32_t* page_table;
-  float* head_part;  // [grid][2][2] (value, index-as-float bits)
-  int32_t* head_cnt;
+  float* head_part;  // [grid][kMaxVec][2] (value, index-as-float bits)
+  int32_t* head_cnt; // [kMaxVec] arrival tickets
 };
 
 struct AttnArgs {
@@ -102,9 +106,12 @@ cudaError_t launch_pdl(Kern fn, dim3 grid, dim3 block, size_t smem, cudaStream_t
 }
 
 // launchers (gemv.cu / attn.cu)
-int gemv_pick(int K, int R, int mat, int* vpt, int* tr, int* nstage, size_t* smem);
-cudaError_t gemv_launch(const GemvArgs& a, int vpt, size_t smem, int grid, cudaStream_t st);
-cudaError_t gemv_set_attrs(int vpt, int mat, size_t smem);
+// A GEMV plan: `m` = vectors per weight pass (1 for the decode tick; up to 4
+// for batched prefill / EESD verify, where a group of nv vectors takes
+// ceil(nv/m) passes).
+int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, size_t* smem);
+cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st);
+cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 

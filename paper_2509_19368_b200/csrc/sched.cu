@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       w->pos[g] = slot >= 0 ? s.c.n_prompt + s.ch_pos[slot] - 2 : 0;
       w->first[g] = s.c.stage_first[st];
       w->nl[g] = s.c.stage_layers[st];
+      w->nv[g] = 1;
     }
     w->head_slot[0] = (s.c.k >= c.lo && s.c.k <= c.hi) ? s.exit_slot : -1;
     w->head_slot[1] = (s.c.S >= c.lo && s.c.S <= c.hi) ? s.final_slot : -1;
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
     Work* w = c.work_ar;
     w->G = 1;
     w->slot[0] = active ? 0 : -1;
+    w->nv[0] = 1;
     w->pos[0] = active ? j : 0;
     w->first[0] = ctl->first_layer;
     w->nl[0] = ctl->n_layers;
@@ -160,6 +162,33 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
   }
 }
 
+// Batched prefill: the next chunk of up to kMaxVec prompt tokens goes through
+// the layers as ONE group of nv vectors (ceil(nv/m) weight passes per matrix
+// instead of nv), positions j0..j0+nv-1.
+__global__ void __launch_bounds__(256) prefill_chunk_kernel(const TickCtx* ctxp, ArCtl* ctl) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  __shared__ int s_j0, s_n;
+  if (threadIdx.x == 0) {
+    const int j0 = ctl->j;
+    const int n = min(c.prefill_chunk, ctl->end - j0);
+    Work* w = c.work_ar;
+    w->G = 1;
+    w->slot[0] = n > 0 ? 0 : -1;
+    w->nv[0] = n > 0 ? n : 1;
+    w->pos[0] = j0;
+    w->first[0] = ctl->first_layer;
+    w->nl[0] = ctl->n_layers;
+    w->head_slot[0] = w->head_slot[1] = -1;
+    ctl->j = j0 + (n > 0 ? n : 0);
+    s_j0 = j0;
+    s_n = n;
+  }
+  __syncthreads();
+  for (int v = 0; v < s_n; ++v) embed_row(c, v, c.tokens[s_j0 + v]);
+}
+
 // ---- autoregressive / prefill control (decode_autoregressive, pipesim.py:390-409)
 __global__ void __launch_bounds__(256) ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head) {
   pdl_wait();
@@ -170,6 +199,7 @@ __global__ void __launch_bounds__(256) ar_begin_kernel(const TickCtx* ctxp, ArCt
     Work* w = c.work_ar;
     w->G = 1;
     w->slot[0] = 0;
+    w->nv[0] = 1;
     w->pos[0] = j;
     w->first[0] = ctl->first_layer;
     w->nl[0] = ctl->n_layers;

@@ -122,6 +122,45 @@ class Engine:
                                    rows.shape[0] if trace else 0, C.byref(n_rows)), "simulate")
         return self._finish(m, rows, n_rows.value)
 
+    def _eesd_result(self, m: _lib.Metrics, rows, n_rows: int):
+        self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
+                         ticks=m.ticks, committed=m.committed_tokens)
+        thr = m.committed_tokens / m.ticks if m.ticks > 0 else 0.0
+        metrics = RunMetrics(m.committed_tokens, m.ticks, m.accepts, m.rejects,
+                             m.alpha_all_measured if m.alpha_valid else None, thr,
+                             thr * self.cfg.ar_ticks_per_token)
+        trace = EventTrace.from_array(rows[:n_rows]) if rows is not None else EventTrace()
+        return metrics, trace
+
+    def _eesd_rows(self, horizon: int, gamma: int):
+        return np.zeros((horizon * (2 * gamma + self.cfg.n_stages + 1) + 8, 6), dtype=np.int32)
+
+    def decode_eesd(self, prompt, horizon: int, gamma: int, trace: bool = True):
+        L = _lib.lib()
+        p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
+        cap_tok = horizon + gamma + 1
+        out = np.zeros(cap_tok, dtype=np.int32)
+        m = _lib.Metrics()
+        rows = self._eesd_rows(horizon, gamma) if trace else None
+        n_rows = C.c_int64(0)
+        _lib.check(L.ppsd_decode_eesd(self.h, gamma, p, len(prompt), horizon,
+                                      out.ctypes.data_as(C.POINTER(C.c_int32)), cap_tok, C.byref(m),
+                                      rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
+                                      rows.shape[0] if trace else 0, C.byref(n_rows)), "decode_eesd")
+        metrics, tr = self._eesd_result(m, rows, n_rows.value)
+        return out[:metrics.committed_tokens].tolist(), metrics, tr
+
+    def simulate_eesd(self, gamma: int, alpha: float, verify_seed: int, horizon: int, trace: bool = True):
+        L = _lib.lib()
+        m = _lib.Metrics()
+        rows = self._eesd_rows(horizon, gamma) if trace else None
+        n_rows = C.c_int64(0)
+        _lib.check(L.ppsd_simulate_eesd(self.h, gamma, float(alpha), verify_seed & ((1 << 64) - 1), horizon,
+                                        C.byref(m),
+                                        rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
+                                        rows.shape[0] if trace else 0, C.byref(n_rows)), "simulate_eesd")
+        return self._eesd_result(m, rows, n_rows.value)
+
     def read_logits(self, which: int) -> np.ndarray:
         V = self._vocab
         out = np.zeros(V, dtype=np.float32)
@@ -211,15 +250,8 @@ def simulate_ppsd(cfg: PipelineConfig, oracle: AcceptanceOracle, horizon: int, r
         raise ValueError("horizon must be >= 1")
     _require_draft_head(cfg)
     if oracle.mode is OracleMode.BERNOULLI:
-        import torch  # noqa: F401
-
-        dev = _lib.require_cuda().index
-        key = ("bernoulli", _cfg_key(cfg), dev)
-        if key not in _ENGINES:
-            _ENGINES[key] = Engine(_lib.ModelDesc(kind=_lib.MODEL_BERNOULLI, n_layers=cfg.n_layers),
-                                   None, cfg, device=dev)
-        m, tr = _ENGINES[key].simulate(oracle.alpha, rng.split("verify").seed, horizon,
-                                       trace=trace is not None)
+        m, tr = _bernoulli_engine(cfg).simulate(oracle.alpha, rng.split("verify").seed, horizon,
+                                                trace=trace is not None)
     else:
         _greedy_only("greedy" if oracle.greedy else "sampling")
         lm = oracle.lm
@@ -246,3 +278,45 @@ def simulate_autoregressive(cfg: PipelineConfig, horizon: int, *, trace: EventTr
             trace.add(start + (s - 1) * per, s, StageMessage(FINAL_TOKEN, i))
     ticks = 1 + (horizon - 1) * s * per + (s - 1) * per
     return make_metrics(horizon, ticks, 0, horizon, 0, cfg.ar_ticks_per_token)
+
+
+def _bernoulli_engine(cfg: PipelineConfig) -> Engine:
+    dev = _lib.require_cuda().index
+    key = ("bernoulli", _cfg_key(cfg), dev)
+    if key not in _ENGINES:
+        _ENGINES[key] = Engine(_lib.ModelDesc(kind=_lib.MODEL_BERNOULLI, n_layers=cfg.n_layers), None, cfg,
+                               device=dev)
+    return _ENGINES[key]
+
+
+def simulate_eesd(cfg: PipelineConfig, gamma: int, oracle: AcceptanceOracle, horizon: int, rng: RngStream, *,
+                  trace: EventTrace | None = None) -> RunMetrics:
+    """Draft-then-verify rounds (pipesim.py:435-551) on the GPU: gamma drafts
+    through the exit layers, one batched verify, acceptance scan."""
+    if horizon < 1:
+        raise ValueError("horizon must be >= 1")
+    if gamma < 1:
+        raise ValueError("gamma must be >= 1")
+    _require_draft_head(cfg)
+    if oracle.mode is OracleMode.BERNOULLI:
+        m, tr = _bernoulli_engine(cfg).simulate_eesd(gamma, oracle.alpha, rng.split("verify").seed, horizon,
+                                                      trace=trace is not None)
+    else:
+        _greedy_only("greedy" if oracle.greedy else "sampling")
+        lm = oracle.lm
+        prompt = default_prompt(lm.vocab, rng)
+        _, m, tr = engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma, trace=trace is not None)
+    if trace is not None:
+        trace._rows.extend(tr.rows())
+    return m
+
+
+def decode_eesd(lm, cfg: PipelineConfig, prompt: list[int], horizon: int, gamma: int
+                ) -> tuple[list[int], RunMetrics, EventTrace]:
+    """EESD with an explicit prompt, returning the committed tokens as well
+    (the baseline next to decode_ppsd / decode_autoregressive in bench tools)."""
+    _check_prompt(lm, prompt)
+    if cfg.n_layers != lm.n_layers:
+        raise ValueError(f"pipeline is {cfg.n_layers} layers deep but the model has {lm.n_layers}")
+    _require_draft_head(cfg)
+    return engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma)

@@ -180,3 +180,47 @@ def test_ppsd_equals_ar_bit_exact(name):
         assert m.committed_tokens == 96 and m.accepts + m.rejects == 96
         rows = [r for r in tr if r.kind in ("FINAL_TOKEN", "CHECK_TOKEN")]
         assert [r.token for r in rows] == toks
+
+
+# ---------------------------------------------------------------- EESD -----
+
+@pytest.mark.parametrize("case", load_golden("eesd_toy.json"), ids=lambda c: f"{c['kind']}-g{c['gamma']}")
+def test_eesd_matches_reference(case):
+    cfg = ppsd.PipelineConfig(32, 8)
+    tr = ppsd.EventTrace()
+    if case["kind"] == "toy":
+        lm = ppsd.ToyLM(32, 16, case["lm_seed"], case["beta"])
+        oracle = ppsd.AcceptanceOracle.toylm_greedy(lm)
+    else:
+        oracle = ppsd.AcceptanceOracle.bernoulli(case["alpha"])
+    m = ppsd.simulate_eesd(cfg, case["gamma"], oracle, case["horizon"], ppsd.RngStream(case["rng_seed"]), trace=tr)
+    assert _metrics_list(m) == case["metrics"]
+    assert tr.to_csv() == case["trace_csv"]
+
+
+@pytest.mark.parametrize("gamma,seed,ds", [(5, 0, 0.1), (3, 1, 0.25), (10, 2, 0.15)])
+def test_tiny_transformer_eesd_matches_oracle(gamma, seed, ds, tiny_models):
+    """GPU EESD (batched verify through kMatHeadV) vs the oracle port's
+    simulate_eesd (pinned to reference EESD goldens) on the CPU decoder."""
+    from oracle import specpipe_port as sp
+    from oracle.transformer import TransformerOracle, tiny_config
+
+    lm = tiny_models(seed, ds)
+    prompt = ppsd.default_prompt(256, ppsd.RngStream(seed))
+    toks, m, tr = ppsd.decode_eesd(lm, ppsd.PipelineConfig(32, 8), prompt, 96, gamma)
+    orc = TransformerOracle(tiny_config(), seed=seed, deep_scale=ds, deep_from=8)
+    want_toks, want_m, rows = sp.simulate_eesd(orc, 32, 8, gamma, 96, 0, prompt=prompt)
+    assert toks == want_toks[:len(toks)]
+    assert _metrics_list(m) == list(want_m)
+    assert tr.to_csv() == sp.trace_csv(rows)
+
+
+@pytest.mark.parametrize("gamma", [1, 4, 7, 15])
+def test_eesd_lossless_vs_ar(gamma):
+    config = ppsd.TransformerConfig(6, 512, 8, 2, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
+    lm = ppsd.TransformerLM(config, seed=21, deep_scale=0.3, deep_from=2)
+    prompt = [int(t) for t in np.random.default_rng(3).integers(0, config.vocab, size=40)]
+    ar = ppsd.decode_autoregressive(lm, prompt, 100, "greedy", ppsd.RngStream(0))
+    toks, m, _ = ppsd.decode_eesd(lm, ppsd.PipelineConfig(6, 2), prompt, 100, gamma)
+    assert toks[:100] == ar
+    assert m.committed_tokens >= 100
