@@ -130,6 +130,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PPSD_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         return run_pipelined(args, world, rank, local)
@@ -248,13 +250,27 @@ def run_pipelined(args, world, rank, local):
     import paper_2509_19368_b200 as ppsd
     from paper_2509_19368_b200.distributed import StageShard, decode_ppsd_pipelined, nccl_exchange
 
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # PPSD_BENCH_EXCHANGE=host + PPSD_BENCH_SAME_GPU=1: exercise this path with
+    # every rank on cuda:0 (gloo over host memory) — a test mode, not a bench.
+    host_mode = os.environ.get("PPSD_BENCH_EXCHANGE") == "host"
+    if os.environ.get("PPSD_BENCH_SAME_GPU") == "1":
+        local = 0
+        torch.cuda.set_device(0)
+    if host_mode:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     config = ppsd.TransformerConfig.llama2_7b(max_ctx=1024)
     exit_depth = EXIT_DEPTH if world <= 4 else config.n_layers // world
     cfg = ppsd.PipelineConfig(config.n_layers, exit_depth)
     shard = StageShard(config, cfg, rank, world, seed=SEED, deep_scale=args.deep_scale,
                        deep_from=exit_depth, device=local)
-    exchange = nccl_exchange(shard)
+    if host_mode:
+        from paper_2509_19368_b200.distributed import host_exchange
+
+        exchange = host_exchange(shard)
+    else:
+        exchange = nccl_exchange(shard)
     rng = ppsd.RngStream(ppsd.derive_seed(SEED, "run"))
     pstream = rng.split("prompt")
     prompt = [pstream.randbelow(config.vocab) for _ in range(PROMPT_LEN)]
@@ -270,11 +286,14 @@ def run_pipelined(args, world, rank, local):
             launches += shard.last["gpu_launches"]
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([sum(dec)], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([sum(dec)], dtype=torch.float64, device="cpu" if host_mode else f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     toks, m, tr = res
     value = NEW_TOKENS * args.steps / (total_ms / 1e3)
+    if host_mode:
+        print(json.dumps({"rank": rank, "tokens_head": toks[:8], "ticks": m.ticks, "accepts": m.accepts}),
+              file=sys.stderr)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3),

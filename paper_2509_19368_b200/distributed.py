@@ -146,3 +146,23 @@ def decode_ppsd_pipelined(shard: StageShard, prompt, max_tokens: int, exchange=N
         if done:
             break
     return shard.end()
+
+
+def host_exchange(shard: StageShard, group=None):
+    """The same box all-gather through host memory over a gloo group. Slow;
+    only for exercising the multi-rank path when the ranks share one GPU
+    (NCCL refuses two ranks on one device)."""
+    import torch
+    import torch.distributed as dist
+
+    world = shard.world
+
+    def exchange():
+        torch.cuda.synchronize(shard.lm.device)
+        out = shard.outbox.cpu()
+        boxes = [torch.empty_like(out) for _ in range(world)]
+        dist.all_gather(boxes, out, group=group)
+        shard.inbox.copy_(torch.stack(boxes))
+        torch.cuda.synchronize(shard.lm.device)
+
+    return exchange
