@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
   __shared__ float s_m[QPK], s_l[QPK];
   __shared__ int s_last;
   __shared__ __align__(8) uint64_t bar;
+  constexpr int kMergePages = 32;  // contexts up to 2048 positions merge from smem
+  __shared__ float s_pm[QPK][kMergePages], s_pl[QPK][kMergePages];
 
   const Work* w = a.work;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -150,20 +152,52 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
       s_last = atomicAdd(&a.cnt[slot * KVh + kvh], 1) == nch - 1;
     }
     __syncthreads();
-    if (s_last) {  // ordered merge of the page partials
+    if (s_last) {  // ordered merge of the page partials (page statistics staged in smem)
       __threadfence();
-      for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-        const int i = idx / HD, d = idx - i * HD;
-        const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2);
-        float M = -FLT_MAX;
-        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(pb + (size_t)cc * (HD + 2) + HD));
-        float Ls = 0.f, O = 0.f;
-        for (int cc = 0; cc < nch; ++cc) {
-          const float e = expf(__ldcg(pb + (size_t)cc * (HD + 2) + HD) - M);
-          Ls = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + HD + 1), e, Ls);
-          O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + d), e, O);
+      if (nch <= kMergePages) {
+        for (int idx = tid; idx < QPK * nch; idx += kAttnThreads) {
+          const int i = idx / nch, cc = idx - i * nch;
+          const float* pb = pbase + ((size_t)i * a.max_pages + cc) * (HD + 2);
+          s_pm[i][cc] = __ldcg(pb + HD);
+          s_pl[i][cc] = __ldcg(pb + HD + 1);
         }
-        a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / Ls;
+        __syncthreads();
+        for (int i = warp; i < QPK; i += 4) {
+          float M = -FLT_MAX;
+          for (int cc = lane; cc < nch; cc += 32) M = fmaxf(M, s_pm[i][cc]);
+          M = warp_max(M);
+          float Ls = 0.f;
+          for (int cc = lane; cc < nch; cc += 32) {
+            const float e = expf(s_pm[i][cc] - M);
+            s_pm[i][cc] = e;  // page weight
+            Ls = fmaf(s_pl[i][cc], e, Ls);
+          }
+          Ls = warp_sum(Ls);
+          if (lane == 0) s_l[i] = Ls;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
+          const int i = idx / HD, d = idx - i * HD;
+          const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2) + d;
+          float O = 0.f;
+#pragma unroll 4
+          for (int cc = 0; cc < nch; ++cc) O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2)), s_pm[i][cc], O);
+          a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / s_l[i];
+        }
+      } else {
+        for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
+          const int i = idx / HD, d = idx - i * HD;
+          const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2);
+          float M = -FLT_MAX;
+          for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(pb + (size_t)cc * (HD + 2) + HD));
+          float Ls = 0.f, O = 0.f;
+          for (int cc = 0; cc < nch; ++cc) {
+            const float e = expf(__ldcg(pb + (size_t)cc * (HD + 2) + HD) - M);
+            Ls = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + HD + 1), e, Ls);
+            O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + d), e, O);
+          }
+          a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / Ls;
+        }
       }
       if (tid == 0) a.cnt[slot * KVh + kvh] = 0;
     }

@@ -424,11 +424,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       if (lane == 0) { s_bv[warp][m] = v; s_bi[warp][m] = i; }
     }
     named_bar_sync(1, kGemvConsumers);
+    // kHead2: one problem over the whole grid; kHeadV: this CTA's problem span
+    const int v0 = kHeadV ? s_pv[hv_p] : 0;
+    const int c0 = kHeadV ? hv_c0 : 0, c1 = kHeadV ? hv_c1 : (int)gridDim.x;
+    int* ticket = a.head_cnt + (kHeadV ? hv_p : 0);
+    __shared__ int s_last;
     if (tid == 0) {
-      // kHead2: one problem over the whole grid; kHeadV: this CTA's problem span
-      const int v0 = kHeadV ? s_pv[hv_p] : 0;
-      const int c0 = kHeadV ? hv_c0 : 0, c1 = kHeadV ? hv_c1 : (int)gridDim.x;
-      int* ticket = a.head_cnt + (kHeadV ? hv_p : 0);
       for (int m = 0; m < M; ++m) {
         float v = s_bv[0][m];
         int i = s_bi[0][m];
@@ -438,18 +439,37 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         a.head_part[((size_t)blockIdx.x * kMaxVec + v0 + m) * 2 + 1] = __int_as_float(i);
       }
       __threadfence();
-      if (atomicAdd(ticket, 1) == c1 - c0 - 1) {
-        __threadfence();
+      s_last = atomicAdd(ticket, 1) == c1 - c0 - 1;
+    }
+    named_bar_sync(1, kGemvConsumers);
+    if (s_last) {  // the last CTA merges the per-CTA partials, all loads in parallel
+      __threadfence();
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        float v = -FLT_MAX;
+        int i = INT_MAX;
+        for (int b = c0 + tid; b < c1; b += kGemvConsumers) {
+          const float bv = __ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 0]);
+          const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 1]));
+          if (better(bv, bi, v, i)) { v = bv; i = bi; }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, v, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, i, off);
+          if (better(ov, oi, v, i)) { v = ov; i = oi; }
+        }
+        if (lane == 0) { s_bv[warp][m] = v; s_bi[warp][m] = i; }
+      }
+      named_bar_sync(1, kGemvConsumers);
+      if (tid == 0) {
         Work* wk = const_cast<Work*>(work);
         const int nv0 = kHeadV ? work->nv[0] : 0;
         for (int m = 0; m < M; ++m) {
-          float v = -FLT_MAX;
-          int i = INT_MAX;
-          for (int b = c0; b < c1; ++b) {
-            const float bv = __ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 0]);
-            const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 1]));
-            if (better(bv, bi, v, i)) { v = bv; i = bi; }
-          }
+          float v = s_bv[0][m];
+          int i = s_bi[0][m];
+          for (int w = 1; w < 8; ++w)
+            if (better(s_bv[w][m], s_bi[w][m], v, i)) { v = s_bv[w][m]; i = s_bi[w][m]; }
           if (kHead2) wk->head_out[m] = work->head_slot[m] >= 0 ? i : -1;
           else if (v0 + m < nv0) wk->vec_out[v0 + m] = i;
         }
