@@ -120,15 +120,20 @@ int ppsd_engine_create(const ppsd_model_desc* model, const ppsd_weights* weights
                        ppsd_engine** out);
 int ppsd_engine_destroy(ppsd_engine* e);
 
-/* greedy verify-while-draft decode; tokens/trace are HOST buffers */
-int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
-                int32_t max_tokens, int32_t force_reject, int32_t* out_tokens,
+/* verify-while-draft decode; tokens/trace are HOST buffers. greedy = 1:
+ * greedy_match verdicts (the parity contract); greedy = 0: sampling mode —
+ * draft / verify / commit draws from the streams derive_seed(rng_seed,
+ * "draft" | "verify" | "commit") exactly as _ToyVerifier (pipesim.py:339-365);
+ * rng_seed = the caller's RngStream.seed. */
+int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t* prompt,
+                int32_t n_prompt, int32_t max_tokens, int32_t force_reject, int32_t* out_tokens,
                 ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
                 int64_t* trace_len);
 
-/* greedy full-model autoregressive decode (the oracle / AR baseline) */
-int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
-                   int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out);
+/* full-model autoregressive decode (the oracle / AR baseline); sampling mode
+ * draws one commit-stream uniform per token (pipesim.py:397-406) */
+int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t* prompt,
+                   int32_t n_prompt, int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out);
 
 /* greedy draft-then-verify rounds of gamma drafts (EESD baseline,
  * simulate_eesd with a greedy model oracle, pipesim.py:435-551): gamma

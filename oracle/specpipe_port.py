@@ -116,6 +116,33 @@ def first_argmax(v) -> int:
     return int(np.argmax(np.asarray(v)))
 
 
+# speccore.py:76-113 — the sampling primitives
+
+
+def sample_token(p: np.ndarray, stream: Stream) -> int:
+    """Inverse CDF: first index whose running sum exceeds u (speccore.py:76-87)."""
+    u = stream.uniform()
+    idx = int(np.searchsorted(np.cumsum(p), u, side="right"))
+    return min(idx, len(p) - 1)
+
+
+def accept_draft(p_tok: float, q_tok: float, stream: Stream) -> bool:
+    """r <= min(1, q/p), one draw; a token without target mass never passes (speccore.py:90-101)."""
+    r = stream.uniform()
+    if q_tok == 0.0:
+        return False
+    return r <= min(1.0, q_tok / p_tok)
+
+
+def residual(p: np.ndarray, q: np.ndarray) -> np.ndarray:
+    """Normalised positive part of q - p (speccore.py:104-113)."""
+    diff = np.maximum(q - p, 0.0)
+    z = float(diff.sum())
+    if z <= 1e-12:
+        raise ValueError("q <= p pointwise; residual has no mass")
+    return diff / z
+
+
 # --------------------------------------------------------------------------
 # toylm.py:55-130, as a protocol object
 
@@ -223,8 +250,8 @@ def ppsd_machine(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=None,
     rng = Stream(rng_seed)
     toy = lm is not None
     if toy:
-        if not greedy:
-            raise NotImplementedError("oracle port restates the greedy path only")
+        # _ToyVerifier streams (pipesim.py:339-344); greedy draws none
+        s_draft, s_verify, s_commit = rng.split("draft"), rng.split("verify"), rng.split("commit")
         seq_tok = list(prompt)
         seq_dig = [lm.empty_digest()]
         for t in prompt:
@@ -252,7 +279,7 @@ def ppsd_machine(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=None,
         if toy:
             fin = lm.advance_digest(ch.digest, ch.layer, n_layers)
             ch.p = _probs(lm.exit_dist_from_states(_State(fin), _State(ch.digest)))
-            ch.token = first_argmax(ch.p)
+            ch.token = first_argmax(ch.p) if greedy else sample_token(ch.p, s_draft)
             push(ch.token)
         if trace:
             rows.append((tick, st, DRAFT_TOKEN, ch.pos, ch.token, ""))
@@ -276,12 +303,20 @@ def ppsd_machine(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=None,
                 if ch.pos != committed + 1:
                     raise AssertionError("verdicts must land in position order")
                 if toy:
-                    top_q = first_argmax(_probs(lm.dist_from_final_state(_State(ch.digest))))
-                    if force_reject:
-                        ok, tok = False, top_q
+                    q = _probs(lm.dist_from_final_state(_State(ch.digest)))
+                    if greedy:
+                        top_q = first_argmax(q)
+                        if force_reject:
+                            ok, tok = False, top_q
+                        else:
+                            ok = first_argmax(ch.p) == top_q
+                            tok = ch.token if ok else top_q
+                    elif force_reject:  # full_model_token (pipesim.py:360-365)
+                        ok, tok = False, sample_token(q, s_commit)
+                    elif accept_draft(ch.p[ch.token], q[ch.token], s_verify):  # pipesim.py:356-358
+                        ok, tok = True, ch.token
                     else:
-                        ok = first_argmax(ch.p) == top_q
-                        tok = ch.token if ok else top_q
+                        ok, tok = False, sample_token(residual(ch.p, q), s_commit)
                 else:
                     ok = (not force_reject) and verify.uniform() < bernoulli_alpha
                     tok = None
@@ -335,8 +370,9 @@ def decode_ppsd(lm, n_layers, exit_depth, prompt, max_tokens, **kw):
     return ppsd_machine(lm, n_layers, exit_depth, prompt, max_tokens, **kw)
 
 
-def decode_autoregressive(lm, prompt, max_tokens):
-    """pipesim.py:390-409, greedy."""
+def decode_autoregressive(lm, prompt, max_tokens, greedy=True, rng_seed=0):
+    """pipesim.py:390-409."""
+    commit = Stream(rng_seed).split("commit")
     seq = list(prompt)
     d = lm.empty_digest()
     digs = [d]
@@ -345,7 +381,8 @@ def decode_autoregressive(lm, prompt, max_tokens):
     out = []
     for _ in range(max_tokens):
         fin = lm.advance_digest(digs[-1], 0, lm.n_layers)
-        tok = first_argmax(_probs(lm.dist_from_final_state(_State(fin))))
+        q = _probs(lm.dist_from_final_state(_State(fin)))
+        tok = first_argmax(q) if greedy else sample_token(q, commit)
         seq.append(tok)
         digs.append(lm.extend_digest(digs[-1], tok))
         out.append(tok)

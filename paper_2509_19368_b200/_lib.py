@@ -69,11 +69,11 @@ EXPORTS = {
     "ppsd_engine_create": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(Weights),
                                      C.POINTER(PipelineDesc), C.c_void_p, C.POINTER(C.c_void_p)]),
     "ppsd_engine_destroy": (C.c_int, [C.c_void_p]),
-    "ppsd_decode": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
-                              C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics),
+    "ppsd_decode": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
+                              C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics),
                               C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
-    "ppsd_decode_ar": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
-                                 C.POINTER(C.c_int32), C.POINTER(Metrics)]),
+    "ppsd_decode_ar": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
+                                 C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics)]),
     "ppsd_decode_eesd": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
                                    C.POINTER(C.c_int32), C.c_int32, C.POINTER(Metrics),
                                    C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),

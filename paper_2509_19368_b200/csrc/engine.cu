@@ -77,6 +77,8 @@ struct ppsd_engine {
   GemvPlan gp[kNumMats];   // decode tick: one vector per weight pass (head: exit + final)
   GemvPlan gpb[kNumMats];  // batched prefill / EESD verify: up to 4 vectors per pass
   int nbuf = 0;            // activation slots (>= nslot, >= kMaxVec)
+  uint64_t verify_seed = 0;  // sampling mode: derive_seed(rng.seed, "verify")
+  double *d_pdist = nullptr, *d_qbuf = nullptr, *d_wbuf = nullptr, *d_logits64 = nullptr;
   const __nv_bfloat16* lm_head = nullptr;
   const float* final_norm = nullptr;
   const float* exit_norm = nullptr;
@@ -217,7 +219,7 @@ static int build_graphs(ppsd_engine* e) {
         int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
-        if (launch_pdl(ar_end_kernel, dim3(1), dim3(32), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
+        if (launch_pdl(ar_end_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
             cudaSuccess)
           return -1;
         return m + 3;
@@ -255,7 +257,8 @@ static void free_engine(ppsd_engine* e) {
   if (e->d_eesd) cudaFree(e->d_eesd);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
-                  e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv};
+                  e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
+                  e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_sched) cudaFreeHost(e->h_sched);
@@ -337,6 +340,8 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     c.chain_dig = e->d_chain_dig;
     c.beta = md->toy_misalignment;
     c.toy_seed = md->toy_seed;
+    CU(dalloc(&e->d_logits64, sizeof(double) * 2 * (size_t)md->vocab));
+    c.logits64 = e->d_logits64;
   } else if (md->kind == PPSD_MODEL_TRANSFORMER) {
     Dims& d = e->dm;
     d.d = md->d_model;
@@ -422,10 +427,20 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * nb * d.KV));
     CU(dalloc(&e->d_head_part, sizeof(float) * 2 * kMaxVec * (size_t)e->num_sms));
     CU(dalloc(&e->d_head_cnt, sizeof(int32_t) * kMaxVec));
+    c.logits32 = e->d_logits;
     c.x = e->d_x;
   } else if (md->kind != PPSD_MODEL_BERNOULLI) {
     return fail(PPSD_EINVAL, "unknown model kind");
   }
+  if (md->kind != PPSD_MODEL_BERNOULLI) {  // sampling-mode float64 scratch
+    CU(dalloc(&e->d_pdist, sizeof(double) * (size_t)std::max(nslot, (int)kMaxVec) * md->vocab));
+    CU(dalloc(&e->d_qbuf, sizeof(double) * (size_t)md->vocab));
+    CU(dalloc(&e->d_wbuf, sizeof(double) * (size_t)md->vocab));
+    c.pdist = e->d_pdist;
+    c.qbuf = e->d_qbuf;
+    c.wbuf = e->d_wbuf;
+  }
+  c.greedy = 1;
   CU(cudaMemcpy(e->d_ctx, &c, sizeof(TickCtx), cudaMemcpyHostToDevice));
   return build_graphs(e);
 }
@@ -586,13 +601,23 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   return PPSD_OK;
 }
 
-extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
-                           int32_t max_tokens, int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out,
-                           ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+// Sampling mode: the three _ToyVerifier streams (pipesim.py:339-344) derived
+// from the caller's RngStream seed; greedy runs draw nothing.
+static int set_mode(ppsd_engine* e, int greedy, uint64_t rng_seed) {
+  e->h_ctx.greedy = greedy ? 1 : 0;
+  e->h_ctx.draft_seed = derive_seed_str(rng_seed, "draft");
+  e->h_ctx.commit_seed = derive_seed_str(rng_seed, "commit");
+  e->verify_seed = derive_seed_str(rng_seed, "verify");
+  CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t* prompt,
+                           int32_t n_prompt, int32_t max_tokens, int32_t force_reject, int32_t* out_tokens,
+                           ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
   if (!e || !out) return fail(PPSD_EINVAL, "null argument");
   if (e->lo != 1 || e->hi != e->S) return fail(PPSD_EINVAL, "engine holds a stage subset: use ppsd_step_*");
   if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines run ppsd_simulate");
-  if (!greedy) return fail(PPSD_EUNSUPPORTED, "sampling mode is not implemented on the B200 engine yet");
   int rc = check_prompt(e, prompt, n_prompt);
   if (rc) return rc;
   if (max_tokens < 0) return fail(PPSD_EINVAL, "max_tokens must be >= 0");
@@ -603,13 +628,16 @@ extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, const int32_t* prompt
   if (need > e->md.max_ctx)
     return fail(PPSD_EINVAL, "prompt + max_tokens exceeds the engine's max_ctx (" + std::to_string(e->md.max_ctx) + ")");
   CU(cudaSetDevice(e->device));
+  rc = set_mode(e, greedy, rng_seed);
+  if (rc) return rc;
   rc = upload_prompt(e, prompt, n_prompt);
   if (rc) return rc;
   int64_t launches = 0;
   double pre_ms = 0;
   rc = prefill(e, n_prompt, &pre_ms, &launches);
   if (rc) return rc;
-  rc = run_machine(e, 1, n_prompt, max_tokens, force_reject, 0.0, 0, out, trace, trace_cap, trace_len, launches);
+  rc = run_machine(e, 1, n_prompt, max_tokens, force_reject, 0.0, greedy ? 0 : e->verify_seed, out, trace,
+                   trace_cap, trace_len, launches);
   if (rc) return rc;
   out->prefill_ms = pre_ms;
   if (out_tokens)
@@ -629,12 +657,11 @@ extern "C" int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed,
   return run_machine(e, 0, 0, horizon, force_reject, alpha, verify_seed, out, trace, trace_cap, trace_len, 0);
 }
 
-extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* prompt, int32_t n_prompt,
-                              int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out) {
+extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t* prompt,
+                              int32_t n_prompt, int32_t max_tokens, int32_t* out_tokens, ppsd_metrics* out) {
   if (!e || !out) return fail(PPSD_EINVAL, "null argument");
   if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines have no model");
   if (e->lo != 1 || e->hi != e->S) return fail(PPSD_EINVAL, "engine holds a stage subset");
-  if (!greedy) return fail(PPSD_EUNSUPPORTED, "sampling mode is not implemented on the B200 engine yet");
   int rc = check_prompt(e, prompt, n_prompt);
   if (rc) return rc;
   if (max_tokens < 0) return fail(PPSD_EINVAL, "max_tokens must be >= 0");
@@ -642,6 +669,8 @@ extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* pro
   if (max_tokens == 0) return PPSD_OK;
   if ((int64_t)n_prompt + max_tokens + 2 > e->md.max_ctx) return fail(PPSD_EINVAL, "exceeds max_ctx");
   CU(cudaSetDevice(e->device));
+  rc = set_mode(e, greedy, rng_seed);
+  if (rc) return rc;
   rc = upload_prompt(e, prompt, n_prompt);
   if (rc) return rc;
   int64_t launches = 0;
@@ -656,7 +685,8 @@ extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, const int32_t* pro
     rc = prefill(e, n_prompt, &pre_ms, &launches);
     if (rc) return rc;
     out->prefill_ms = pre_ms;
-    ArCtl ctl{n_prompt - 1, e->first_local_layer, e->n_local_layers, 0};
+    // end = first decoded index: commit-stream draw of step j is j - end
+    ArCtl ctl{n_prompt - 1, e->first_local_layer, e->n_local_layers, n_prompt - 1};
     CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
     CU(cudaEventRecord(e->ev0, e->st));
     for (int i = 0; i < max_tokens; ++i) CU(cudaGraphLaunch(e->g_ar, e->st));

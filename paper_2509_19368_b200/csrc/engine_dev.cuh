@@ -35,6 +35,14 @@ struct TickCtx {
   int32_t owner_k, owner_S, owner_prev;  // ranks owning the exit stage, stage S, stage lo-1
   int32_t n_prompt;
   int32_t model_stages;  // S
+  // sampling mode (mode == "sampling"): stream seeds and float64 scratch
+  int32_t greedy;
+  uint64_t draft_seed, commit_seed;  // derive_seed(rng.seed, "draft" | "commit")
+  const float* logits32;  // transformer heads [2][V]
+  double* logits64;       // ToyLM heads [2][V]
+  double* pdist;          // per-chain draft distribution [nbuf][V]
+  double* qbuf;           // target / sampling scratch [V]
+  double* wbuf;           // residual scratch [V]
   int32_t prefill_chunk; // prompt tokens per batched prefill launch (<= kMaxVec)
 };
 

@@ -28,6 +28,13 @@ PPSD_HD double counter_uniform(uint64_t seed, uint64_t c) {
   return (double)(hmix64(seed + (c + 1) * kGoldenGamma) >> 11) * 0x1p-53;
 }
 
+// derive_seed(seed, label) for a string label — rng.py:51-63
+PPSD_HD uint64_t derive_seed_str(uint64_t seed, const char* label) {
+  uint64_t h = hmix64(seed ^ 0xA24BAED4963EE407ull);
+  for (const char* c = label; *c; ++c) h = hmix64(h ^ ((uint64_t)(unsigned char)*c + 1));
+  return h;
+}
+
 // ToyLM salts — toylm.py:25-29
 constexpr uint64_t kSeqSalt = 0x243F6A8885A308D3ull;
 constexpr uint64_t kTokenSalt = 0x13198A2E03707344ull;

@@ -5,8 +5,64 @@
 // the chain launched at stage 1 gets its input (embedding row / ToyLM prefix
 // digest). No host round trip per tick: the host only enqueues tick graphs.
 #include "engine_dev.cuh"
+#include "sample.cuh"
 
 namespace ppsd {
+
+// Sampling mode, run by the whole block before sched_finish (pipesim.py:346-365):
+// the draft for this tick's exit chain is drawn from p = softmax(exit logits)
+// (p kept per chain for its verdict), and the verdict for the chain at stage S
+// runs accept_draft / the residual resample against q = softmax(final logits).
+__device__ void sampling_tick(const TickCtx& c, Sched& s, int* exit_tok, int* final_ok, int* final_tok) {
+  const int V = c.vocab;
+  const bool exact = V <= kExactVocab;
+  const double* l64 = c.logits64;
+  const float* l32 = c.logits32;
+  if (s.final_slot >= 0) {  // verdict first: its draws do not interleave with the draft stream
+    block_softmax(l64 ? l64 + V : nullptr, l32 ? l32 + V : nullptr, V, c.qbuf, exact);
+    const double* p = c.pdist + (size_t)s.final_slot * V;
+    const int d = s.ch_tok[s.final_slot];
+    __shared__ int s_ok;
+    __shared__ double s_u;
+    if (threadIdx.x == 0) {
+      if (s.c.force_reject) {
+        s_ok = 0;  // full_model_token: sample q with the commit stream
+        s_u = counter_uniform(c.commit_seed, s.commit_counter++);
+      } else {
+        const double r = counter_uniform(s.c.verify_seed, s.verify_counter++);
+        const double pt = p[d], qt = c.qbuf[d];
+        s_ok = (qt != 0.0) && r <= fmin(1.0, __ddiv_rn(qt, pt));  // speccore.py:90-101
+        if (!s_ok) s_u = counter_uniform(c.commit_seed, s.commit_counter++);
+      }
+    }
+    __syncthreads();
+    const int ok = s_ok;
+    int tok = d;
+    if (!ok) {
+      const double* dist = c.qbuf;
+      if (!s.c.force_reject) {  // residual max(q - p, 0) / Z (speccore.py:104-113)
+        for (int i = threadIdx.x; i < V; i += blockDim.x) c.wbuf[i] = fmax(__dsub_rn(c.qbuf[i], p[i]), 0.0);
+        __syncthreads();
+        const double z = block_sum(c.wbuf, V, exact);
+        if (z <= 1e-12 && threadIdx.x == 0) s.error |= kErrResidual;
+        for (int i = threadIdx.x; i < V; i += blockDim.x) c.wbuf[i] = __ddiv_rn(c.wbuf[i], z);
+        __syncthreads();
+        dist = c.wbuf;
+      }
+      tok = block_sample(dist, V, s_u, exact);
+    }
+    *final_ok = ok;
+    *final_tok = tok;
+  }
+  if (s.exit_slot >= 0) {  // the draft: sample_token(p, draft_stream)
+    double* p = c.pdist + (size_t)s.exit_slot * V;
+    block_softmax(l64, l32, V, p, exact);
+    __shared__ double s_ud;
+    if (threadIdx.x == 0) s_ud = counter_uniform(c.draft_seed, s.draft_counter++);
+    __syncthreads();
+    *exit_tok = block_sample(p, V, s_ud, exact);
+  }
+}
 
 // block copy with all loads of a thread issued before its stores (one
 // memory round trip instead of a dependent chain per element)
@@ -73,13 +129,31 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       for (int i = threadIdx.x; i < c.d; i += blockDim.x) x[i] = box[kBoxHeader + i];
     }
   }
+  __shared__ int s_exit_tok, s_final_ok, s_final_tok;
   if (threadIdx.x == 0) {
-    int exit_tok = c.work->head_out[0], final_tok = c.work->head_out[1];
+    s_exit_tok = c.work->head_out[0];
+    s_final_tok = c.work->head_out[1];
+    s_final_ok = -1;  // greedy verdict inside sched_finish
+  }
+  __syncthreads();
+  if (!begin && !c.greedy && s.c.model != 0) {
+    int e = -1, ok = -1, f = -1;
+    sampling_tick(c, s, &e, &ok, &f);
+    if (threadIdx.x == 0) {
+      s_exit_tok = e;
+      s_final_ok = ok;
+      s_final_tok = f;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int exit_tok = s_exit_tok, final_tok = s_final_tok;
     if (c.inbox) {  // replicated scheduler: head results come from their owners' boxes
       exit_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_k * c.box_words)[0];
       final_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_S * c.box_words)[1];
     }
-    if (!begin) sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap);
+    if (!begin)
+      sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap, s_final_ok);
     sched_plan(&s);
     Work* w = c.work;
     w->G = c.hi - c.lo + 1;
@@ -213,9 +287,17 @@ __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head) {
   pdl_wait();
   pdl_trigger();
   const TickCtx c = *ctxp;
+  const int j = ctl->j;
+  int tok = c.work_ar->head_out[1];
+  if (with_head && !c.greedy) {  // sample_token(q, commit_stream), one draw per token
+    const int V = c.vocab;
+    const bool exact = V <= kExactVocab;
+    block_softmax(nullptr, c.logits32 + V, V, c.qbuf, exact);
+    tok = block_sample(c.qbuf, V, counter_uniform(c.commit_seed, (uint64_t)(j - ctl->end)), exact);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int j = ctl->j;
-    if (with_head) c.tokens[j + 1] = c.work_ar->head_out[1];
+    if (with_head) c.tokens[j + 1] = tok;
     ctl->j = j + 1;
   }
 }

@@ -31,7 +31,7 @@ constexpr int kTransitCap = 512;
 
 enum : int { kKindAct = 0, kKindDraft = 1, kKindFinal = 2, kKindCheck = 3 };
 enum : int { kVerdictNone = 0, kVerdictAccept = 1, kVerdictReject = 2 };
-enum : int { kErrOrder = 1, kErrTrace = 2, kErrTransit = 4 };
+enum : int { kErrOrder = 1, kErrTrace = 2, kErrTransit = 4, kErrResidual = 8 };
 
 struct TraceRow {
   int32_t tick, stage, kind, position, token, verdict;
@@ -55,6 +55,7 @@ struct Sched {
   SchedCfg c;
   int32_t t, committed, accepts, rejects, draft_head, next_launch, done, error;
   uint64_t verify_counter;
+  uint64_t draft_counter, commit_counter;  // sampling-mode streams (pipesim.py:339-344)
   int64_t trace_n;
   int32_t launched;     // the stage-1 chain this tick is a fresh launch
   int32_t exit_slot;    // chain whose exit head runs this tick, -1 none
@@ -74,6 +75,7 @@ PPSD_HD void sched_reset(Sched* s) {
   s->done = (s->c.stop <= 0);
   s->error = 0;
   s->verify_counter = 0;
+  s->draft_counter = s->commit_counter = 0;
   s->trace_n = 0;
   s->launched = 0;
   s->exit_slot = s->final_slot = kNone;
@@ -164,10 +166,13 @@ PPSD_HD void sched_emit(Sched* s, int slot, int st, TraceRow* tr, int64_t cap) {
   s->tq_n += 1;
 }
 
-// End of tick t. exit_tok / final_tok are the argmax outputs of the exit and
-// final heads for s->exit_slot / s->final_slot (ignored for Bernoulli).
+// End of tick t. exit_tok / final_tok are the exit and final heads' outputs for
+// s->exit_slot / s->final_slot (ignored for Bernoulli). Greedy: final_ok < 0
+// and the verdict is greedy_match. Sampling: the model side already ran
+// accept_draft / the residual resample (pipesim.py:351-365) and passes the
+// verdict in final_ok with the committed token in final_tok.
 PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens, uint64_t* pdig,
-                          TraceRow* tr, int64_t cap) {
+                          TraceRow* tr, int64_t cap, int final_ok = -1) {
   // a tick that sched_plan declined (run already done) leaves work[] idle
   // and launched == 0, so nothing below fires.
   const int S = s->c.S, k = s->c.k;
@@ -181,7 +186,10 @@ PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens
       if (pos != s->committed + 1) s->error |= kErrOrder;  // pipesim.py:740-741
       bool ok;
       int tok;
-      if (s->c.model != 0) {  // greedy_match (speccore.py:116-126), pipesim.py:351-358
+      if (s->c.model != 0 && final_ok >= 0) {  // sampling verdict computed by the model side
+        ok = final_ok != 0;
+        tok = final_tok;
+      } else if (s->c.model != 0) {  // greedy_match (speccore.py:116-126), pipesim.py:351-358
         ok = !s->c.force_reject && s->ch_tok[slot] == final_tok;
         tok = final_tok;  // == the draft when accepted
       } else {            // pipesim.py:749

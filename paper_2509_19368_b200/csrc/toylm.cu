@@ -10,6 +10,7 @@
 #include <limits.h>
 
 #include "engine_dev.cuh"
+#include "sample.cuh"
 
 namespace ppsd {
 
@@ -85,12 +86,21 @@ __global__ void __launch_bounds__(256) toy_tick_kernel(const TickCtx* ctxp) {
     while (w->slot[g] != slot) ++g;
     const uint64_t d = s_dig[g];
     int tok;
+    double* out64 = c.greedy ? nullptr : c.logits64 + (size_t)m * c.vocab;  // sampling: full logits
     if (m == 0) {  // exit head: final digest + noise keyed by the exit state (pipesim.py:711-715)
       const uint64_t fin = toy_advance(d, s_after[g], c.n_layers);
       const double beta = c.beta;
-      tok = block_argmax(c.vocab, [&](int v) { return toy_exit_logit(fin, d, beta, v); });
+      tok = block_argmax(c.vocab, [&](int v) {
+        const double z = toy_exit_logit(fin, d, beta, v);
+        if (out64) out64[v] = z;
+        return z;
+      });
     } else {
-      tok = block_argmax(c.vocab, [&](int v) { return toy_logit(d, v); });
+      tok = block_argmax(c.vocab, [&](int v) {
+        const double z = toy_logit(d, v);
+        if (out64) out64[v] = z;
+        return z;
+      });
     }
     if (threadIdx.x == 0) w->head_out[m] = tok;
   }
@@ -103,7 +113,16 @@ __global__ void __launch_bounds__(256) toy_ar_kernel(const TickCtx* ctxp, int n_
     const int len = n_prompt + i;
     const uint64_t d0 = c.pdig[len];
     const uint64_t fin = toy_advance(d0, 0, c.n_layers);
-    const int tok = block_argmax(c.vocab, [&](int v) { return toy_logit(fin, v); });
+    int tok;
+    if (c.greedy) {
+      tok = block_argmax(c.vocab, [&](int v) { return toy_logit(fin, v); });
+    } else {  // sample_token(q, commit_stream) (pipesim.py:403-406)
+      for (int v = threadIdx.x; v < c.vocab; v += blockDim.x) c.logits64[v] = toy_logit(fin, v);
+      __syncthreads();
+      const bool exact = c.vocab <= kExactVocab;
+      block_softmax(c.logits64, nullptr, c.vocab, c.qbuf, exact);
+      tok = block_sample(c.qbuf, c.vocab, counter_uniform(c.commit_seed, (uint64_t)i), exact);
+    }
     if (threadIdx.x == 0) {
       c.tokens[len] = tok;
       c.pdig[len + 1] = toy_extend(d0, tok);

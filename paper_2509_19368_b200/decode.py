@@ -86,26 +86,30 @@ class Engine:
         return metrics, trace
 
     # -- entry points ----------------------------------------------------
-    def decode(self, prompt, max_tokens: int, force_reject: bool = False, trace: bool = True):
+    def decode(self, prompt, max_tokens: int, force_reject: bool = False, trace: bool = True,
+               mode: str = "greedy", rng_seed: int = 0):
         L = _lib.lib()
         p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
         out = np.zeros(max(1, max_tokens), dtype=np.int32)
         m = _lib.Metrics()
         rows = np.zeros((self._trace_cap(max_tokens), 6), dtype=np.int32) if trace else None
         n_rows = C.c_int64(0)
-        _lib.check(L.ppsd_decode(self.h, 1, p, len(prompt), max_tokens, int(bool(force_reject)),
+        greedy = int(mode == "greedy")
+        _lib.check(L.ppsd_decode(self.h, greedy, rng_seed & ((1 << 64) - 1), p, len(prompt), max_tokens,
+                                 int(bool(force_reject)),
                                  out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(m),
                                  rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
                                  rows.shape[0] if trace else 0, C.byref(n_rows)), "decode")
         metrics, tr = self._finish(m, rows, n_rows.value)
         return out[:max_tokens].tolist(), metrics, tr
 
-    def decode_ar(self, prompt, max_tokens: int):
+    def decode_ar(self, prompt, max_tokens: int, mode: str = "greedy", rng_seed: int = 0):
         L = _lib.lib()
         p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
         out = np.zeros(max(1, max_tokens), dtype=np.int32)
         m = _lib.Metrics()
-        _lib.check(L.ppsd_decode_ar(self.h, 1, p, len(prompt), max_tokens,
+        _lib.check(L.ppsd_decode_ar(self.h, int(mode == "greedy"), rng_seed & ((1 << 64) - 1), p, len(prompt),
+                                    max_tokens,
                                     out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(m)), "decode_ar")
         self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
                          ticks=m.ticks, committed=m.committed_tokens)
@@ -218,29 +222,28 @@ def decode_ppsd(lm, cfg: PipelineConfig, prompt: list[int], max_tokens: int, mod
     _require_draft_head(cfg)
     if max_tokens == 0:
         return [], make_metrics(0, 0, 0, 0, 0, cfg.ar_ticks_per_token), EventTrace()
-    _greedy_only(mode)
     if isinstance(lm, ToyLM):
         _toy_ctx_for(lm, len(prompt), max_tokens, cfg)
-    return engine_for(lm, cfg).decode(prompt, max_tokens, force_reject)
+    return engine_for(lm, cfg).decode(prompt, max_tokens, force_reject, mode=mode, rng_seed=rng.seed)
 
 
 def decode_autoregressive(lm, prompt: list[int], max_tokens: int, mode: str, rng: RngStream) -> list[int]:
-    """Full-model greedy decode on the GPU (pipesim.py:390-409)."""
+    """Full-model decode on the GPU (pipesim.py:390-409); sampling draws one
+    commit-stream uniform per token."""
     _check_mode(mode)
     _check_prompt(lm, prompt)
     if max_tokens == 0:
         return []
-    _greedy_only(mode)
     n = lm.n_layers
     if n < 2:
         raise NotImplementedError("single-layer models are not supported by the engine")
     cfg = PipelineConfig(n, max(1, n // 2))
     if isinstance(lm, ToyLM):
         _toy_ctx_for(lm, len(prompt), max_tokens, cfg)
-        return engine_for(lm, cfg).decode_ar(prompt, max_tokens)
+        return engine_for(lm, cfg).decode_ar(prompt, max_tokens, mode=mode, rng_seed=rng.seed)
     cached = getattr(lm, "_engines", None)
     eng = next(iter(cached.values())) if cached else engine_for(lm, cfg)  # reuse the KV pool
-    return eng.decode_ar(prompt, max_tokens)
+    return eng.decode_ar(prompt, max_tokens, mode=mode, rng_seed=rng.seed)
 
 
 def simulate_ppsd(cfg: PipelineConfig, oracle: AcceptanceOracle, horizon: int, rng: RngStream, *,
@@ -253,10 +256,10 @@ def simulate_ppsd(cfg: PipelineConfig, oracle: AcceptanceOracle, horizon: int, r
         m, tr = _bernoulli_engine(cfg).simulate(oracle.alpha, rng.split("verify").seed, horizon,
                                                 trace=trace is not None)
     else:
-        _greedy_only("greedy" if oracle.greedy else "sampling")
         lm = oracle.lm
         prompt = default_prompt(lm.vocab, rng)
-        _, m, tr = engine_for(lm, cfg).decode(prompt, horizon, trace=trace is not None)
+        _, m, tr = engine_for(lm, cfg).decode(prompt, horizon, trace=trace is not None,
+                                              mode="greedy" if oracle.greedy else "sampling", rng_seed=rng.seed)
     if trace is not None:
         trace._rows.extend(tr.rows())
     return m

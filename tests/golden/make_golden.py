@@ -180,11 +180,49 @@ def make_transformer():
     return out
 
 
+SAMPLING_CASES = [
+    ("s_b1", 32, 16, 0, 1.0, dict(n_layers=32, exit_depth=8), None, 128),
+    ("s_b0", 32, 16, 4, 0.0, dict(n_layers=32, exit_depth=8), [1], 64),
+    ("s_b2", 32, 16, 12, 2.0, dict(n_layers=32, exit_depth=8), [11, 4, 4, 0], 96),
+    ("s_deep_exit", 32, 16, 5, 1.0, dict(n_layers=32, exit_depth=8, exit_stage=2), [6, 6], 64),
+    ("s_comm_lat", 32, 16, 6, 1.5, dict(n_layers=32, exit_depth=8, comm_latency=1), [2, 7], 64),
+    ("s_remainder", 33, 16, 7, 0.7, dict(n_layers=33, exit_depth=8), [9, 0, 2], 80),
+    ("s_v1000", 32, 1000, 10, 0.5, dict(n_layers=32, exit_depth=8), [17, 999, 0], 64),
+]
+
+
+def make_sampling():
+    out = []
+    for name, n, vocab, seed, beta, cfgkw, prompt, max_tokens in SAMPLING_CASES:
+        lm = sp.ToyLM(n_layers=n, vocab=vocab, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        cfg = sp.PipelineConfig(**cfgkw)
+        if prompt is None:
+            prompt = sp.default_prompt(vocab, run_rng(seed))
+        toks, m, tr = sp.decode_ppsd(lm, cfg, prompt, max_tokens, "sampling", run_rng(seed))
+        ar = sp.decode_autoregressive(lm, prompt, max_tokens, "sampling", run_rng(seed))
+        fr, fm, _ = sp.decode_ppsd(lm, cfg, prompt, max_tokens, "sampling", run_rng(seed), force_reject=True)
+        assert fr == ar
+        out.append(dict(name=name, n_layers=n, vocab=vocab, lm_seed=lm.seed, beta=beta, cfg=cfgkw,
+                        prompt=list(map(int, prompt)), max_tokens=max_tokens, rng_seed=run_rng(seed).seed,
+                        tokens=toks, metrics=metrics_list(m), trace_csv=trace_text(tr), ar_tokens=ar,
+                        force_reject_metrics=metrics_list(fm)))
+    # simulate_ppsd with a toy sampling oracle (default prompt from the run stream)
+    for seed, beta in ((1, 1.0), (2, 0.5)):
+        lm = sp.ToyLM(n_layers=32, vocab=16, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        tr = EventTrace()
+        m = sp.simulate_ppsd(sp.PipelineConfig(32, 8), sp.AcceptanceOracle.toylm_sampling(lm), 100,
+                             run_rng(seed), trace=tr)
+        out.append(dict(name=f"sim_sampling_{seed}", kind="simulate", n_layers=32, vocab=16, lm_seed=lm.seed,
+                        beta=beta, cfg=dict(n_layers=32, exit_depth=8), rng_seed=run_rng(seed).seed,
+                        max_tokens=100, metrics=metrics_list(m), trace_csv=trace_text(tr)))
+    return out
+
+
 def main(argv):
-    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf"}
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp"}
     jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
             ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
-            ("tf", "transformer.json", make_transformer)]
+            ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling)]
     for key, fname, fn in jobs:
         if key in which:
             data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",
