@@ -178,6 +178,21 @@ int ppsd_step_poll(ppsd_engine* e, int32_t* done, int64_t* committed, int64_t* t
 int ppsd_step_end(ppsd_engine* e, int32_t* out_tokens, ppsd_metrics* out,
                   ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len);
 
+/* NVLink peer-store transport (the fused alternative to the all-gather):
+ * every rank's pack kernel stores its box straight into every rank's
+ * exchange buffer (CUDA IPC-mapped, NVLink/NVSwitch) and releases a flag; the
+ * scheduler kernel acquire-waits on the flags, so a whole tick is one graph
+ * and ticks run back to back with no host work. prepare() allocates this
+ * rank's buffer and returns its cudaIpcMemHandle_t (64 bytes) and device
+ * pointer; connect() maps the peers from their handles (separate processes)
+ * or takes their device pointers directly (engines in one process). */
+int ppsd_p2p_prepare(ppsd_engine* e, int32_t world, void* ipc_handle, void** xbuf);
+int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_handles, void* const* local_xbufs,
+                     const int32_t* stage_owner);
+int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
+                    int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out,
+                    ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len);
+
 /* Device weight initialiser: the counter-hash init of oracle/transformer.py,
  * written straight into the engine's physical layout.
  * layout: 0 plain [rows][cols]; 1 = fused qkv (q,k pair-interleaved);

@@ -94,6 +94,12 @@ EXPORTS = {
                                  C.POINTER(C.c_int64)]),
     "ppsd_step_end": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(Metrics),
                                 C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
+    "ppsd_p2p_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ppsd_p2p_connect": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p),
+                                   C.POINTER(C.c_int32)]),
+    "ppsd_p2p_decode": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32,
+                                  C.POINTER(C.c_int32), C.POINTER(Metrics), C.POINTER(TraceRowC), C.c_int64,
+                                  C.POINTER(C.c_int64)]),
     "ppsd_init_weight": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,
                                    C.POINTER(C.c_uint64), C.POINTER(C.c_float), C.c_int32, C.c_int32,
                                    C.c_int32, C.c_void_p]),

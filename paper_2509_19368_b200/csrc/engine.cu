@@ -92,10 +92,26 @@ struct ppsd_engine {
   int64_t compute_launches = 0, finish_launches = 0, mr_prefill_launches = 0;
   int mr_world = 0, mr_rank = 0, mr_stop = 0, mr_n_prompt = 0;
   int64_t mr_launches = 0, mr_ticks_launched = 0;
+  // NVLink peer-store transport
+  float* d_xbuf = nullptr;          // [2][world][box] + world flags, shared via IPC
+  float* d_p2p_outbox = nullptr;    // local box scratch
+  uint64_t* d_xcount = nullptr;
+  int32_t* d_xerr = nullptr;
+  std::vector<void*> retired;  // buffers replaced while peers may still run (freed at destroy)
+  float** d_peer_xbuf = nullptr;
+  std::vector<void*> ipc_opened;    // peer mappings to close
+  int p2p_world = 0;
+  cudaGraphExec_t g_p2p_tick = nullptr;
+  int64_t p2p_tick_launches = 0;
   int64_t tick_launches = 0, ar_launches = 0, prefill_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   // host staging
   Sched* h_sched = nullptr;  // pinned
+  // p2p: pinned staging for the per-decode uploads (ctx, ArCtl, prompt) so a
+  // decode never issues a pageable copy or an allocation while peer engines
+  // of this process spin on flags it has yet to set
+  char* h_p2p_pin = nullptr;
+  int32_t* h_p2p_out = nullptr;
   TickCtx h_ctx{};
 };
 
@@ -254,7 +270,13 @@ static void free_engine(ppsd_engine* e) {
   if (e->g_finish) cudaGraphExecDestroy(e->g_finish);
   if (e->g_mr_prefill) cudaGraphExecDestroy(e->g_mr_prefill);
   for (auto& kv : e->eesd_graphs) cudaGraphExecDestroy(kv.second.first);
+  if (e->g_p2p_tick) cudaGraphExecDestroy(e->g_p2p_tick);
+  for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void* b : {(void*)e->d_xbuf, (void*)e->d_p2p_outbox, (void*)e->d_xcount, (void*)e->d_peer_xbuf,
+                  (void*)e->d_xerr})
+    if (b) cudaFree(b);
   if (e->d_eesd) cudaFree(e->d_eesd);
+  for (void* b : e->retired) cudaFree(b);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
@@ -262,6 +284,7 @@ static void free_engine(ppsd_engine* e) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (e->h_sched) cudaFreeHost(e->h_sched);
+  if (e->h_p2p_pin) cudaFreeHost(e->h_p2p_pin);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->ev2) cudaEventDestroy(e->ev2);
@@ -280,7 +303,10 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
                        ppsd_engine* e) {
   e->md = *md;
   e->pd = *pd;
-  if (const char* v = getenv("PPSD_PDL")) ppsd::g_pdl = atoi(v) != 0;
+  {
+    const char* v = getenv("PPSD_PDL");  // read at engine creation; graphs capture it
+    ppsd::g_pdl = v ? atoi(v) != 0 : true;
+  }
   e->device = pd->device;
   CU(cudaSetDevice(e->device));
   CU(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, e->device));
@@ -510,7 +536,9 @@ static int prefill(ppsd_engine* e, int n_prompt, double* ms, int64_t* launches) 
 
 static int ensure_trace(ppsd_engine* e, int64_t cap) {
   if (cap <= e->trace_cap) return PPSD_OK;
-  if (e->d_trace) CU(cudaFree(e->d_trace));
+  // no cudaFree here: it synchronizes the device, which would wait on other
+  // engines of this process spinning on p2p flags this engine has yet to set
+  if (e->d_trace) e->retired.push_back(e->d_trace);
   e->d_trace = nullptr;
   e->trace_cap = 0;
   CU(cudaMalloc(&e->d_trace, sizeof(TraceRow) * cap));
@@ -1125,5 +1153,212 @@ extern "C" int ppsd_step_end(ppsd_engine* e, int32_t* out_tokens, ppsd_metrics* 
   e->h_ctx.inbox = nullptr;
   e->h_ctx.outbox = nullptr;
   CU(cudaMemcpy(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice));
+  return PPSD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NVLink peer-store transport (p2p.cuh): no host work per tick — a whole tick
+// (local stages, local heads, box peer-stores + release flags, acquire-wait,
+// replicated scheduler) is one graph, launched back to back like single-GPU.
+
+// pinned staging: [TickCtx][ArCtl][prompt int32 x max_ctx][xerr int32]
+static size_t p2p_pin_bytes(const ppsd_engine* e) {
+  return sizeof(TickCtx) + sizeof(ArCtl) + sizeof(int32_t) * ((size_t)e->md.max_ctx + 1);
+}
+
+extern "C" int ppsd_p2p_prepare(ppsd_engine* e, int32_t world, void* ipc_handle, void** xbuf) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "p2p needs a transformer engine");
+  if (world < 1 || world > e->S) return fail(PPSD_EINVAL, "bad world size");
+  CU(cudaSetDevice(e->device));
+  const int box = kBoxHeader + e->dm.d;
+  if (!e->d_xbuf || e->p2p_world != world) {
+    if (e->d_xbuf) CU(cudaFree(e->d_xbuf));
+    size_t bytes = sizeof(float) * 2 * (size_t)world * box + sizeof(uint64_t) * world;
+#ifdef PPSD_P2P_DEBUG
+    bytes += sizeof(uint64_t) * (1 + 500 * 8);
+#endif
+    CU(dalloc(&e->d_xbuf, bytes));  // flags start at 0; exchange numbers start at 1
+    e->p2p_world = world;
+  }
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, e->d_xbuf));
+    memcpy(ipc_handle, &h, sizeof(h));
+  }
+  if (xbuf) *xbuf = e->d_xbuf;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_handles, void* const* local_xbufs,
+                                const int32_t* stage_owner) {
+  if (!e || !e->d_xbuf) return fail(PPSD_ESTATE, "call ppsd_p2p_prepare first");
+  const int world = e->p2p_world;
+  if (rank < 0 || rank >= world || !stage_owner || (!ipc_handles && !local_xbufs))
+    return fail(PPSD_EINVAL, "bad p2p_connect arguments");
+  for (int st = e->lo; st <= e->hi; ++st)
+    if (stage_owner[st] != rank) return fail(PPSD_EINVAL, "stage_owner disagrees with the engine's stage range");
+  CU(cudaSetDevice(e->device));
+  std::vector<float*> peers(world);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      peers[r] = e->d_xbuf;
+    } else if (local_xbufs) {
+      peers[r] = reinterpret_cast<float*>(local_xbufs[r]);
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, static_cast<const char*>(ipc_handles) + r * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      e->ipc_opened.push_back(p);
+      peers[r] = reinterpret_cast<float*>(p);
+    }
+  }
+  if (!e->d_peer_xbuf) CU(dalloc(&e->d_peer_xbuf, sizeof(float*) * kMaxStages));
+  CU(cudaMemcpy(e->d_peer_xbuf, peers.data(), sizeof(float*) * world, cudaMemcpyHostToDevice));
+  if (!e->d_p2p_outbox) CU(dalloc(&e->d_p2p_outbox, sizeof(float) * (kBoxHeader + e->dm.d)));
+  if (!e->d_xcount) CU(dalloc(&e->d_xcount, sizeof(uint64_t)));
+  if (!e->d_xerr) CU(dalloc(&e->d_xerr, sizeof(int32_t)));
+  {  // everything a decode up to max_ctx can need, allocated now
+    const int64_t max_ticks = (int64_t)e->md.max_ctx * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
+    int rc0 = ensure_trace(e, max_ticks * (e->S + 2));
+    if (rc0) return rc0;
+    if (!e->h_p2p_pin) {
+      const size_t pin = p2p_pin_bytes(e);
+      CU(cudaMallocHost(reinterpret_cast<void**>(&e->h_p2p_pin), pin));
+      e->h_p2p_out = reinterpret_cast<int32_t*>(e->h_p2p_pin + pin) - 1;  // xerr word
+    }
+  }
+  TickCtx& c = e->h_ctx;
+  c.p2p = 1;
+  c.peer_xbuf = e->d_peer_xbuf;
+  c.my_xbuf = e->d_xbuf;
+  c.xcount = e->d_xcount;
+  c.xerr = e->d_xerr;
+  c.outbox = e->d_p2p_outbox;
+  c.inbox = nullptr;
+  c.box_words = kBoxHeader + e->dm.d;
+  c.rank = rank;
+  c.world = world;
+  c.owner_k = stage_owner[e->cfg.k];
+  c.owner_S = stage_owner[e->S];
+  c.owner_prev = e->lo > 1 ? stage_owner[e->lo - 1] : -1;
+  CU(cudaMemcpy(e->d_ctx, &c, sizeof(TickCtx), cudaMemcpyHostToDevice));
+  // Load every kernel a decode launches outside a graph now: with lazy module
+  // loading the first launch of a kernel waits for the device to drain, which
+  // never happens while a peer engine on the same device spins on our flags.
+  cudaFuncAttributes fa;
+  CU(cudaFuncGetAttributes(&fa, sched_tick_kernel));
+  CU(cudaFuncGetAttributes(&fa, p2p_wait_kernel));
+  int rc = build_mr_graphs(e);
+  if (rc) return rc;
+  if (!e->g_p2p_tick) {
+    rc = capture(
+        e,
+        [&]() -> int {
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+          if (m < 0) return -1;
+          if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
+          if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
+              cudaSuccess)
+            return -1;
+          if (launch_pdl(sched_tick_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
+              cudaSuccess)
+            return -1;
+          return m + 3;
+        },
+        &e->g_p2p_tick, &e->p2p_tick_launches);
+    if (rc) return rc;
+  }
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
+                               int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out, ppsd_trace_row* trace,
+                               int64_t trace_cap, int64_t* trace_len) {
+  if (!e || !e->g_p2p_tick) return fail(PPSD_ESTATE, "call ppsd_p2p_connect first");
+  int rc = check_prompt(e, prompt, n_prompt);
+  if (rc) return rc;
+  if (max_tokens < 1) return fail(PPSD_EINVAL, "max_tokens must be >= 1");
+  if ((int64_t)n_prompt + max_tokens + (int64_t)e->S * e->cfg.per + 2 > e->md.max_ctx)
+    return fail(PPSD_EINVAL, "prompt + max_tokens exceeds the engine's max_ctx");
+  CU(cudaSetDevice(e->device));
+  // No allocation and no pageable copy from here on (see h_p2p_pin): with
+  // several engines on one device either can wait for a peer's spinning wait.
+  const int64_t max_ticks = (int64_t)max_tokens * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
+  if (max_ticks * (e->S + 2) > e->trace_cap) return fail(PPSD_ESTATE, "p2p trace reservation too small");
+  TickCtx& c = e->h_ctx;
+  c.trace = e->d_trace;
+  c.trace_cap = e->trace_cap;
+  c.n_prompt = n_prompt;
+  c.greedy = 1;
+  Sched& s = *e->h_sched;
+  memset(&s, 0, sizeof(Sched));
+  s.c = e->cfg;
+  s.c.model = 1;
+  s.c.force_reject = force_reject;
+  s.c.stop = max_tokens;
+  s.c.n_prompt = n_prompt;
+  sched_reset(&s);
+  char* pin = e->h_p2p_pin;
+  TickCtx* pin_ctx = reinterpret_cast<TickCtx*>(pin);
+  ArCtl* pin_ctl = reinterpret_cast<ArCtl*>(pin + sizeof(TickCtx));
+  int32_t* pin_prompt = reinterpret_cast<int32_t*>(pin + sizeof(TickCtx) + sizeof(ArCtl));
+  *pin_ctx = c;
+  *pin_ctl = ArCtl{0, e->first_local_layer, e->n_local_layers, 0};
+  memcpy(pin_prompt, prompt, sizeof(int32_t) * n_prompt);
+  CU(cudaMemcpyAsync(e->d_tokens, pin_prompt, sizeof(int32_t) * n_prompt, cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_arctl, pin_ctl, sizeof(ArCtl), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_ctx, pin_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemcpyAsync(e->d_sched, &s, sizeof(Sched), cudaMemcpyHostToDevice, e->st));
+  sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 1);  // plan tick 1 (+ embed on rank 0)
+  CU(cudaGetLastError());
+  int64_t launches = 1;
+  CU(cudaEventRecord(e->ev0, e->st));
+  const int steps = n_prompt >= 2 ? (n_prompt - 1) + (e->p2p_world - 1) : 0;  // pipelined prefill
+  for (int i = 0; i < steps; ++i) CU(cudaGraphLaunch(e->g_mr_prefill, e->st));
+  launches += (int64_t)steps * e->mr_prefill_launches;
+  if (steps > 0) {
+    p2p_wait_kernel<<<1, 32, 0, e->st>>>(e->d_ctx);
+    CU(cudaGetLastError());
+    launches += 1;
+  }
+  CU(cudaEventRecord(e->ev2, e->st));
+  int64_t ticks_launched = 0;
+  const size_t off = offsetof(Sched, t);
+  const size_t len = offsetof(Sched, verify_counter) - off;
+  for (;;) {  // replicated state: every rank launches the same number of ticks
+    const int64_t n = std::max<int64_t>(1, (int64_t)max_tokens - s.committed);
+    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(e->g_p2p_tick, e->st));
+    ticks_launched += n;
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
+                       cudaMemcpyDeviceToHost, e->st));
+    CU(cudaStreamSynchronize(e->st));
+    if (s.error || s.done) break;
+    if (ticks_launched > max_ticks + 4) return fail(PPSD_ESTATE, "tick machine did not converge");
+  }
+  CU(cudaEventRecord(e->ev1, e->st));
+  CU(cudaMemcpyAsync(&s, e->d_sched, sizeof(Sched), cudaMemcpyDeviceToHost, e->st));
+  CU(cudaMemcpyAsync(e->h_p2p_out, e->d_xerr, sizeof(int32_t), cudaMemcpyDeviceToHost, e->st));
+  CU(cudaStreamSynchronize(e->st));
+  const int32_t xerr = *e->h_p2p_out;
+  if (s.error && !xerr) return fail(PPSD_ESTATE, "scheduler error flags " + std::to_string(s.error));
+  float ms = 0, pre = 0;
+  CU(cudaEventElapsedTime(&ms, e->ev2, e->ev1));
+  CU(cudaEventElapsedTime(&pre, e->ev0, e->ev2));
+  memset(out, 0, sizeof(*out));
+  fill_metrics(e, s, out);
+  out->decode_ms = ms;
+  out->prefill_ms = pre;
+  out->gpu_launches = launches + ticks_launched * e->p2p_tick_launches;
+  if (out_tokens) CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * max_tokens, cudaMemcpyDeviceToHost));
+  if (trace) {
+    const int64_t nr = std::min<int64_t>(s.trace_n, trace_cap);
+    if (nr > 0) CU(cudaMemcpy(trace, e->d_trace, sizeof(TraceRow) * nr, cudaMemcpyDeviceToHost));
+    if (trace_len) *trace_len = nr;
+  } else if (trace_len) {
+    *trace_len = 0;
+  }
+  // outputs are filled either way so a failed exchange can be inspected
+  if (xerr) return fail(PPSD_ECUDA, "p2p exchange timed out waiting for a peer rank");
   return PPSD_OK;
 }

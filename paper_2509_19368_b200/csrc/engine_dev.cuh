@@ -43,6 +43,12 @@ struct TickCtx {
   double* pdist;          // per-chain draft distribution [nbuf][V]
   double* qbuf;           // target / sampling scratch [V]
   double* wbuf;           // residual scratch [V]
+  // NVLink peer-store transport (p2p.cuh); p2p == 0: caller-driven all-gather
+  int32_t p2p;
+  float* const* peer_xbuf;  // [world] device pointers (IPC-mapped) of every rank's exchange buffer
+  float* my_xbuf;           // this rank's exchange buffer
+  uint64_t* xcount;         // exchange counter (device)
+  int32_t* xerr;            // sticky p2p wait timeout flag (device)
   int32_t prefill_chunk; // prompt tokens per batched prefill launch (<= kMaxVec)
 };
 
@@ -71,6 +77,7 @@ __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void toy_tick_kernel(const TickCtx* ctxp);
 __global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
 __global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
+__global__ void p2p_wait_kernel(const TickCtx* ctxp);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);
 __global__ void prefill_chunk_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void eesd_draft_begin_kernel(const TickCtx* ctxp, EesdState* es);

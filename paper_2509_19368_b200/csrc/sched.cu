@@ -5,6 +5,7 @@
 // the chain launched at stage 1 gets its input (embedding row / ToyLM prefix
 // digest). No host round trip per tick: the host only enqueues tick graphs.
 #include "engine_dev.cuh"
+#include "p2p.cuh"
 #include "sample.cuh"
 
 namespace ppsd {
@@ -120,11 +121,14 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
   const TickCtx c = *ctxp;
   copy_words(&s, c.sched, sizeof(Sched));
   __syncthreads();
-  if (!begin && c.inbox && c.owner_prev >= 0) {
+  // multi-rank: this tick's boxes — all-gathered by the caller, or peer-stored (p2p)
+  const float* inbox = c.inbox;
+  if (!begin && c.p2p) inbox = p2p_wait_latest(c);
+  if (!begin && inbox && c.owner_prev >= 0) {
     // the chain stage lo-1 (another rank) ran this tick arrives with its activation
     const int prev = s.work[c.lo - 1];
     if (prev >= 0) {
-      const float* box = c.inbox + (size_t)c.owner_prev * c.box_words;
+      const float* box = inbox + (size_t)c.owner_prev * c.box_words;
       float* x = c.x + (size_t)prev * c.d;
       for (int i = threadIdx.x; i < c.d; i += blockDim.x) x[i] = box[kBoxHeader + i];
     }
@@ -148,9 +152,9 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
   }
   if (threadIdx.x == 0) {
     int exit_tok = s_exit_tok, final_tok = s_final_tok;
-    if (c.inbox) {  // replicated scheduler: head results come from their owners' boxes
-      exit_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_k * c.box_words)[0];
-      final_tok = reinterpret_cast<const int32_t*>(c.inbox + (size_t)c.owner_S * c.box_words)[1];
+    if (inbox) {  // replicated scheduler: head results come from their owners' boxes
+      exit_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_k * c.box_words)[0];
+      final_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_S * c.box_words)[1];
     }
     if (!begin)
       sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap, s_final_ok);
@@ -204,6 +208,19 @@ __global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, i
     const float* x = c.x + (size_t)slot * c.d;
     for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.outbox[kBoxHeader + i] = x[i];
   }
+  if (c.p2p) {  // NVLink peer stores into every rank's exchange buffer + release flags
+    __syncthreads();
+    p2p_publish(c);
+  }
+}
+
+// p2p: wait until every rank published the latest exchange (orders the first
+// decode tick after every rank finished reading the last prefill box)
+__global__ void __launch_bounds__(32) p2p_wait_kernel(const TickCtx* ctxp) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  if (c.p2p) p2p_wait_latest(c);
 }
 
 // Multi-rank pipelined prefill: at step p rank r runs its layers on prompt
@@ -215,6 +232,8 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
   const int p = ctl->j;
   const int j = p - c.rank;
   const bool active = j >= 0 && j < c.n_prompt - 1;
+  const float* inbox = c.inbox;
+  if (c.p2p && p > 0) inbox = p2p_wait_latest(c);  // every rank, every step: lockstep
   __syncthreads();
   if (threadIdx.x == 0) {
     Work* w = c.work_ar;
@@ -231,7 +250,7 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
   if (c.rank == 0) {
     embed_row(c, 0, c.tokens[j]);
   } else {
-    const float* box = c.inbox + (size_t)(c.rank - 1) * c.box_words;
+    const float* box = inbox + (size_t)(c.rank - 1) * c.box_words;
     for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.x[i] = box[kBoxHeader + i];
   }
 }

@@ -166,3 +166,62 @@ def host_exchange(shard: StageShard, group=None):
         torch.cuda.synchronize(shard.lm.device)
 
     return exchange
+
+
+# ---------------------------------------------------------------------------
+# NVLink peer-store transport: boxes are stored by the pack kernel directly
+# into every rank's exchange buffer (CUDA IPC), flags released at system
+# scope; a whole tick is one graph and the host only launches ticks.
+
+
+def p2p_prepare(shard: StageShard) -> tuple[bytes, int]:
+    """Allocate this rank's exchange buffer; returns (IPC handle bytes, device pointer)."""
+    handle = (C.c_char * 64)()
+    xbuf = C.c_void_p()
+    _lib.check(_lib.lib().ppsd_p2p_prepare(shard.engine.h, shard.world, handle, C.byref(xbuf)), "p2p_prepare")
+    return bytes(handle), xbuf.value
+
+
+def p2p_connect(shard: StageShard, handles: list[bytes] | None = None, local_xbufs: list[int] | None = None):
+    """Map the peers' exchange buffers: IPC handles (one process per GPU) or raw
+    device pointers (engines sharing one process)."""
+    own = (C.c_int32 * len(shard.owner))(*shard.owner)
+    if local_xbufs is not None:
+        arr = (C.c_void_p * shard.world)(*local_xbufs)
+        rc = _lib.lib().ppsd_p2p_connect(shard.engine.h, shard.rank, None, arr, own)
+    else:
+        blob = C.create_string_buffer(b"".join(handles), 64 * shard.world)
+        rc = _lib.lib().ppsd_p2p_connect(shard.engine.h, shard.rank, blob, None, own)
+    _lib.check(rc, "p2p_connect")
+    shard.transport = "p2p"
+
+
+def p2p_setup_group(shard: StageShard, group=None):
+    """Exchange IPC handles over torch.distributed (any backend) and connect."""
+    import torch.distributed as dist
+
+    handle, _ = p2p_prepare(shard)
+    handles = [None] * shard.world
+    dist.all_gather_object(handles, handle, group=group)
+    p2p_connect(shard, handles=handles)
+
+
+def decode_ppsd_p2p(shard: StageShard, prompt, max_tokens: int, *, force_reject: bool = False):
+    """The pipelined decode over the peer-store transport (after p2p_connect);
+    every rank calls it with the same arguments."""
+    L = _lib.lib()
+    p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
+    out = np.zeros(max_tokens, dtype=np.int32)
+    m = _lib.Metrics()
+    cap = shard.engine._trace_cap(max_tokens)
+    rows = np.zeros((cap, 6), dtype=np.int32)
+    n = C.c_int64()
+    rc = L.ppsd_p2p_decode(shard.engine.h, p, len(prompt), max_tokens, int(bool(force_reject)),
+                           out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(m),
+                           rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)), cap, C.byref(n))
+    shard.last_raw = (rc, out.tolist(), EventTrace.from_array(rows[: n.value]))
+    _lib.check(rc, "p2p_decode")
+    metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects, m.accepts + m.rejects,
+                           shard.cfg.ar_ticks_per_token)
+    shard.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches, ticks=m.ticks)
+    return out.tolist(), metrics, EventTrace.from_array(rows[: n.value])
