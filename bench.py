@@ -240,58 +240,84 @@ def run_ours(args):
 
 
 def run_pipelined(args, world, rank, local):
-    """N > 1: one pipeline rank per GPU (stages split contiguously), boxes
-    all-gathered over NCCL each tick; E=8 (4 stages) up to 4 GPUs, E=32/N
-    beyond. Timed on each rank's stream with CUDA events; max over ranks."""
+    """N > 1: one pipeline rank per GPU (stages split contiguously); E=8
+    (4 stages) up to 4 GPUs, E=32/N beyond. Transport (PPSD_BENCH_EXCHANGE):
+    `p2p` (default) — NVLink peer stores + system-scope flags, a whole tick
+    is one CUDA graph per rank; `nccl` — box all-gather between the compute
+    and finish graphs; `host` — gloo through host memory (test mode only).
+    Timed on each rank's stream with CUDA events; max over ranks."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2509_19368_b200 as ppsd
-    from paper_2509_19368_b200.distributed import StageShard, decode_ppsd_pipelined, nccl_exchange
+    from paper_2509_19368_b200 import distributed as D
 
-    # PPSD_BENCH_EXCHANGE=host + PPSD_BENCH_SAME_GPU=1: exercise this path with
-    # every rank on cuda:0 (gloo over host memory) — a test mode, not a bench.
-    host_mode = os.environ.get("PPSD_BENCH_EXCHANGE") == "host"
-    if os.environ.get("PPSD_BENCH_SAME_GPU") == "1":
+    transport = os.environ.get("PPSD_BENCH_EXCHANGE", "p2p")
+    # PPSD_BENCH_SAME_GPU=1: every rank on cuda:0 — exercises this path on one
+    # device (a test mode, not a bench). Ranks sharing a device must not use
+    # programmatic dependent launch with the p2p spin-waits (DESIGN.md §5).
+    same_gpu = os.environ.get("PPSD_BENCH_SAME_GPU") == "1"
+    if same_gpu:
         local = 0
-        torch.cuda.set_device(0)
-    if host_mode:
+        os.environ["PPSD_PDL"] = "0"
+    torch.cuda.set_device(local)
+    if transport == "host" or same_gpu:
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    reduce_dev = "cpu" if (transport == "host" or same_gpu) else f"cuda:{local}"
     config = ppsd.TransformerConfig.llama2_7b(max_ctx=1024)
     exit_depth = EXIT_DEPTH if world <= 4 else config.n_layers // world
     cfg = ppsd.PipelineConfig(config.n_layers, exit_depth)
-    shard = StageShard(config, cfg, rank, world, seed=SEED, deep_scale=args.deep_scale,
-                       deep_from=exit_depth, device=local)
-    if host_mode:
-        from paper_2509_19368_b200.distributed import host_exchange
+    shard = D.StageShard(config, cfg, rank, world, seed=SEED, deep_scale=args.deep_scale,
+                         deep_from=exit_depth, device=local)
+    if transport == "p2p":
+        D.p2p_setup_group(shard)
 
-        exchange = host_exchange(shard)
+        def decode(prompt):
+            return D.decode_ppsd_p2p(shard, prompt, NEW_TOKENS)
     else:
-        exchange = nccl_exchange(shard)
+        exchange = D.host_exchange(shard) if transport == "host" else D.nccl_exchange(shard)
+
+        def decode(prompt):
+            return D.decode_ppsd_pipelined(shard, prompt, NEW_TOKENS, exchange)
     rng = ppsd.RngStream(ppsd.derive_seed(SEED, "run"))
     pstream = rng.split("prompt")
     prompt = [pstream.randbelow(config.vocab) for _ in range(PROMPT_LEN)]
     for _ in range(args.warmup):
-        decode_ppsd_pipelined(shard, prompt, NEW_TOKENS, exchange)
+        decode(prompt)
     dist.barrier()
     torch.cuda.synchronize()
     dec, launches, res = [], 0, None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            res = decode_ppsd_pipelined(shard, prompt, NEW_TOKENS, exchange)
+            res = decode(prompt)
             dec.append(shard.last["decode_ms"])
             launches += shard.last["gpu_launches"]
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([sum(dec)], dtype=torch.float64, device="cpu" if host_mode else f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
     toks, m, tr = res
+
+    # end to end through the per-rank public call (host prompt in, host tokens,
+    # metrics and trace out), wall clock, max over ranks
+    e2e = []
+    for _ in range(max(1, min(3, args.steps))):
+        dist.barrier()
+        t0 = time.perf_counter()
+        out = decode(prompt)
+        e2e.append(time.perf_counter() - t0)
+        assert out[0] == toks
+
+    # every rank must hold the same tokens (replicated scheduler)
+    digest = int(np.bitwise_xor.reduce(np.asarray(toks, dtype=np.int64) * 1000003 + np.arange(len(toks)))) & (2**40 - 1)
+    agg = torch.tensor([sum(dec), sum(e2e), digest, -digest], dtype=torch.float64, device=reduce_dev)
+    dist.all_reduce(agg, op=dist.ReduceOp.MAX)
+    total_ms, e2e_s = float(agg[0].item()), float(agg[1].item())
+    if int(agg[2].item()) != digest or int(-agg[3].item()) != digest:
+        raise RuntimeError("ranks disagree on the decoded tokens")
     value = NEW_TOKENS * args.steps / (total_ms / 1e3)
-    if host_mode:
+    if same_gpu or transport == "host":
         print(json.dumps({"rank": rank, "tokens_head": toks[:8], "ticks": m.ticks, "accepts": m.accepts}),
               file=sys.stderr)
     line = {
@@ -302,8 +328,12 @@ def run_pipelined(args, world, rank, local):
         "config": {"workload": f"Llama-2-7B-shaped greedy PPSD decode, E={exit_depth} "
                                f"({cfg.n_stages} stages over {world} GPUs), bs=1, prompt 128, 512 new tokens",
                    "model": "llama2-7b-shape", "exit_depth": exit_depth, "n_stages": cfg.n_stages,
-                   "deep_scale": args.deep_scale, "parallelism": f"pp{world} (stage pipeline, NCCL box all-gather)",
+                   "deep_scale": args.deep_scale, "transport": transport,
+                   "parallelism": f"pp{world} (stage pipeline, {transport} box exchange per tick)",
                    "l2": "inputs larger than L2 (weights streamed per step)"},
+        "e2e": {"value": round(NEW_TOKENS * len(e2e) / e2e_s, 3), "unit": "tokens/s",
+                "h2d_bytes_per_step": 4 * PROMPT_LEN, "d2h_bytes_per_step": 4 * NEW_TOKENS + 24 * len(tr) + 88,
+                "note": "per-rank public decode call incl. prefill, wall clock, max over ranks"},
         "clocks": clk.summary(), "gpu_launches": launches,
         "alpha_measured": m.alpha_all_measured, "ticks": m.ticks, "tick_speedup": m.speedup_vs_ar,
         "ppsd_speedup_eq7": ppsd.ppsd_speedup(m.alpha_all_measured, config.n_layers, exit_depth)
