@@ -77,6 +77,14 @@ struct ppsd_engine {
   GemvPlan gp[kNumMats];   // decode tick: one vector per weight pass (head: exit + final)
   GemvPlan gpb[kNumMats];  // batched prefill / EESD verify: up to 4 vectors per pass
   int nbuf = 0;            // activation slots (>= nslot, >= kMaxVec)
+  // tcgen05 prefill (umma.cu): weight tensor maps [n_layers][4], activation
+  // operand per input width (d, H*hd, ffn) with its map, split-tile scratch
+  bool umma = false;
+  void* d_wmaps = nullptr;
+  void* d_xmaps = nullptr;
+  __nv_bfloat16* d_xs[3] = {nullptr, nullptr, nullptr};
+  float* d_umws = nullptr;
+  int32_t* d_umcnt = nullptr;
   uint64_t verify_seed = 0;  // sampling mode: derive_seed(rng.seed, "verify")
   double *d_pdist = nullptr, *d_qbuf = nullptr, *d_wbuf = nullptr, *d_logits64 = nullptr;
   const __nv_bfloat16* lm_head = nullptr;
@@ -169,8 +177,54 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   return attn_launch(a, attn_grid(e), e->st);
 }
 
+static cudaError_t enqueue_umma(ppsd_engine* e, Work* w, int layer_i, int mat) {
+  const int Rq = (e->dm.H + 2 * e->dm.KV) * e->dm.hd;
+  const int R[4] = {Rq, e->dm.d, 2 * e->dm.ffn, e->dm.d};
+  const int K[4] = {e->dm.d, e->dm.H * e->dm.hd, e->dm.d, e->dm.ffn};
+  const int xi = mat == kMatO ? 1 : mat == kMatDown ? 2 : 0;
+  UmmaArgs a{};
+  a.work = w;
+  a.layer_i = layer_i;
+  a.mat = mat;
+  a.R = R[mat];
+  a.K = K[mat];
+  a.layers = e->d_layers;
+  a.wmaps = e->d_wmaps;
+  a.xmap = static_cast<const unsigned char*>(e->d_xmaps) + xi * umma_map_bytes();
+  a.xs = e->d_xs[xi];
+  a.dm = e->dm;
+  a.x = e->d_x;
+  a.q = e->d_q;
+  a.o = e->d_o;
+  a.h = e->d_h;
+  a.rope_cos = e->rope_cos;
+  a.rope_sin = e->rope_sin;
+  a.page_table = e->d_page_table;
+  a.ws = e->d_umws;
+  a.cnt = e->d_umcnt;
+  return umma_launch(a, e->num_sms, e->st);
+}
+
+// Prompt layers for a chunk of <= kMaxVec vectors in group 0 of `w`: the
+// tcgen05 GEMM when planned (2 launches per matrix: operand staging + GEMM),
+// else the batched GEMV. Returns launches enqueued, or -1.
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched);
+static int enqueue_prefill_layers(ppsd_engine* e, Work* w, int n_slots) {
+  if (!e->umma) return enqueue_layers(e, w, n_slots, true);
+  int n = 0;
+  for (int i = 0; i < n_slots; ++i) {
+    if (enqueue_umma(e, w, i, kMatQKV) != cudaSuccess) return -1;
+    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
+    if (enqueue_umma(e, w, i, kMatO) != cudaSuccess) return -1;
+    if (enqueue_umma(e, w, i, kMatGU) != cudaSuccess) return -1;
+    if (enqueue_umma(e, w, i, kMatDown) != cudaSuccess) return -1;
+    n += 9;
+  }
+  return n;
+}
+
 // returns launches enqueued, or -1 on error
-static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched = false) {
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
     if (enqueue_gemv(e, w, i, kMatQKV, batched) != cudaSuccess) return -1;
@@ -208,7 +262,7 @@ static int build_graphs(ppsd_engine* e) {
       [&]() -> int {
         int n = 0;
         if (kind == PPSD_MODEL_TRANSFORMER) {
-          int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
           n += m;
           if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
@@ -232,7 +286,7 @@ static int build_graphs(ppsd_engine* e) {
         if (launch_pdl(ar_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
             cudaSuccess)
           return -1;
-        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
+        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, false);
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
         if (launch_pdl(ar_end_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
@@ -248,7 +302,7 @@ static int build_graphs(ppsd_engine* e) {
         if (launch_pdl(prefill_chunk_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
                        e->d_arctl) != cudaSuccess)
           return -1;
-        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);
+        int m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
         if (m < 0) return -1;
         return m + 1;
       },
@@ -276,6 +330,9 @@ static void free_engine(ppsd_engine* e) {
                   (void*)e->d_xerr})
     if (b) cudaFree(b);
   if (e->d_eesd) cudaFree(e->d_eesd);
+  for (void* b : {e->d_wmaps, e->d_xmaps, (void*)e->d_xs[0], (void*)e->d_xs[1], (void*)e->d_xs[2],
+                  (void*)e->d_umws, (void*)e->d_umcnt})
+    if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
@@ -297,6 +354,44 @@ static cudaError_t dalloc(T** p, size_t bytes) {
   cudaError_t r = cudaMalloc(reinterpret_cast<void**>(p), bytes);
   if (r == cudaSuccess) r = cudaMemset(*p, 0, bytes);
   return r;
+}
+
+// tcgen05 prefill plan: tensor maps over every local layer's matrices. Off
+// (batched GEMV prefill) when a matrix does not tile by 128 x 128 or with
+// PPSD_UMMA=0.
+static int setup_umma(ppsd_engine* e, const int (*shapes)[2]) {
+  const char* env = getenv("PPSD_UMMA");
+  if (env && atoi(env) == 0) return PPSD_OK;
+  for (int m = kMatQKV; m <= kMatDown; ++m)
+    if (!umma_shape_ok(shapes[m][0], shapes[m][1])) return PPSD_OK;
+  const int L = e->md.n_layers;
+  const size_t mb = umma_map_bytes();
+  std::vector<unsigned char> maps((size_t)L * 4 * mb, 0);
+  for (int l = 0; l < L; ++l) {
+    const LayerW& W = e->h_layers[l];
+    if (!W.qkv) continue;
+    const void* ptr[4] = {W.qkv, W.o, W.gu, W.down};
+    for (int m = 0; m < 4; ++m)
+      if (umma_encode_map(&maps[((size_t)l * 4 + m) * mb], ptr[m], shapes[m][0], shapes[m][1], umma_tile_rows()))
+        return PPSD_OK;  // no driver tensor-map entry point: stay on the GEMV prefill
+  }
+  const int widths[3] = {e->dm.d, e->dm.H * e->dm.hd, e->dm.ffn};
+  std::vector<unsigned char> xm(3 * mb, 0);
+  for (int i = 0; i < 3; ++i) {
+    CU(dalloc(&e->d_xs[i], sizeof(__nv_bfloat16) * 2 * umma_n() * (size_t)widths[i]));
+    if (umma_encode_map(&xm[i * mb], e->d_xs[i], 2 * umma_n(), widths[i], umma_n())) return PPSD_OK;
+  }
+  CU(cudaMalloc(&e->d_wmaps, maps.size()));
+  CU(cudaMemcpy(e->d_wmaps, maps.data(), maps.size(), cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&e->d_xmaps, xm.size()));
+  CU(cudaMemcpy(e->d_xmaps, xm.data(), xm.size(), cudaMemcpyHostToDevice));
+  int tiles = 0;
+  for (int m = kMatQKV; m <= kMatDown; ++m) tiles = std::max(tiles, shapes[m][0] / umma_tile_rows());
+  CU(dalloc(&e->d_umws, sizeof(float) * (size_t)e->num_sms * 2 * umma_tile_rows() * umma_n()));
+  CU(dalloc(&e->d_umcnt, sizeof(int32_t) * tiles));
+  CU(umma_set_attrs());
+  e->umma = true;
+  return PPSD_OK;
 }
 
 static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const ppsd_pipeline_desc* pd,
@@ -455,6 +550,8 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_head_cnt, sizeof(int32_t) * kMaxVec));
     c.logits32 = e->d_logits;
     c.x = e->d_x;
+    int rc = setup_umma(e, shapes);
+    if (rc) return rc;
   } else if (md->kind != PPSD_MODEL_BERNOULLI) {
     return fail(PPSD_EINVAL, "unknown model kind");
   }
@@ -761,7 +858,7 @@ static int eesd_graph(ppsd_engine* e, int gamma, cudaGraphExec_t* out, int64_t* 
         }
         for (int h = 0; h < gamma; ++h) {  // gamma one-token drafts through the exit layers
           if (launch_pdl(eesd_draft_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
-          const int m = enqueue_layers(e, e->d_work_ar, exit_layer);
+          const int m = enqueue_layers(e, e->d_work_ar, exit_layer, false);
           if (m < 0) return -1;
           if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
           if (launch_pdl(eesd_draft_end_kernel, dim3(1), dim3(32), 0, e->st, ctx, es) != cudaSuccess) return -1;
@@ -980,7 +1077,7 @@ static int build_mr_graphs(ppsd_engine* e) {
   int rc = capture(
       e,
       [&]() -> int {
-        int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+        int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
         if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
@@ -1006,7 +1103,7 @@ static int build_mr_graphs(ppsd_engine* e) {
         if (launch_pdl(mr_prefill_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
                        e->d_arctl) != cudaSuccess)
           return -1;
-        int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers);
+        int m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
         if (m < 0) return -1;
         if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 1) !=
             cudaSuccess)
@@ -1255,7 +1352,7 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
     rc = capture(
         e,
         [&]() -> int {
-          int m = enqueue_layers(e, e->d_work, e->max_local_layers);
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
           if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
           if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=

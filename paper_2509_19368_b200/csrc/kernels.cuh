@@ -84,6 +84,29 @@ struct AttnArgs {
   int32_t max_pages;
 };
 
+// tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
+// up to 16 vectors in group 0 of `work`.
+struct UmmaArgs {
+  const Work* work;
+  int32_t layer_i;
+  int32_t mat;           // kMatQKV / kMatO / kMatGU / kMatDown
+  int32_t R, K;
+  const LayerW* layers;
+  const void* wmaps;     // CUtensorMap [n_layers][4] over the weight matrices
+  const void* xmap;      // CUtensorMap over xs
+  __nv_bfloat16* xs;     // [32][K] activation operand: rows 0-15 hi, 16-31 lo
+  Dims dm;
+  float* x;
+  float* q;
+  float* o;
+  float* h;
+  const float* rope_cos;
+  const float* rope_sin;
+  const int32_t* page_table;
+  float* ws;             // [grid][2][128][16] split-tile partials
+  int32_t* cnt;          // [R / 128] arrival tickets
+};
+
 // Programmatic dependent launch (PDL): every kernel of a decode step is
 // launched with programmatic stream serialization so it can be scheduled
 // while its predecessor drains; kernels order their own accesses with
@@ -114,5 +137,12 @@ cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid
 cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
+bool umma_shape_ok(int R, int K);
+int umma_encode_map(void* map, const void* base, int rows, int K, int box_rows);
+size_t umma_map_bytes();
+int umma_tile_rows();
+int umma_n();
+cudaError_t umma_set_attrs();
+cudaError_t umma_launch(const UmmaArgs& a, int grid, cudaStream_t st);
 
 }  // namespace ppsd
