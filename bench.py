@@ -93,16 +93,32 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def algorithmic_bytes(trace, config, cfg, n_prompt):
-    """HBM bytes a decode must move: stage weights per
-    stage-forward, one tied LM-head pass per tick that runs any head, and the
-    KV rows each forward's attention reads."""
-    import numpy as np  # noqa: F401
+def algorithmic_bytes(trace, config, cfg, n_prompt, last=None):
+    """HBM bytes a decode must move.
 
+    Pipelined schedule: stage weights per stage-forward, one tied LM-head pass
+    per tick that runs any head, and the KV rows each forward's attention
+    reads. Folded schedule: per launched chain its shallow
+    stages + the exit-head pass; per deep batch the deep stages + one
+    final-head pass (weights counted ONCE per batch: that is the point of
+    the batch); KV rows per chain and layer either way."""
     from paper_2509_19368_b200.pipeline import ACTIVATION, CHECK_TOKEN, DRAFT_TOKEN, FINAL_TOKEN
 
     layer_b = config.layer_bytes()
     kv_b = config.kv_bytes_per_token_layer()
+    if last and last.get("schedule") == "folded":
+        k = cfg.exit_stage or 1
+        shallow = sum(cfg.stage_layers[:k])
+        deep = config.n_layers - shallow
+        launches = [r.position for r in trace if r.kind == ACTIVATION and r.stage == 1]
+        nb, nvec, psum = last["deep_batches"], last["deep_vectors"], last["deep_pos_sum"]
+        weights = len(launches) * shallow * layer_b + nb * deep * layer_b
+        heads = (len(launches) + nb) * config.head_bytes()
+        kv = (shallow * kv_b * sum(n_prompt + p - 1 for p in launches)
+              + deep * kv_b * (psum + nvec * (n_prompt - 1)))
+        return weights + heads + kv, dict(schedule="folded", shallow_passes=len(launches),
+                                          deep_batches=nb, deep_vectors=nvec, weight_bytes=weights,
+                                          head_bytes=heads, kv_bytes=kv)
     head_ticks = set()
     weights = kv = 0
     fwd = 0
@@ -116,7 +132,7 @@ def algorithmic_bytes(trace, config, cfg, n_prompt):
         if r.kind in (DRAFT_TOKEN, FINAL_TOKEN, CHECK_TOKEN):
             head_ticks.add(r.tick)
     heads = len(head_ticks) * config.head_bytes()
-    return weights + heads + kv, dict(stage_forwards=fwd, head_passes=len(head_ticks),
+    return weights + heads + kv, dict(schedule="pipelined", stage_forwards=fwd, head_passes=len(head_ticks),
                                       weight_bytes=weights, head_bytes=heads, kv_bytes=kv)
 
 
@@ -158,10 +174,31 @@ def run_ours(args):
             steps.append(one_step())
         torch.cuda.synchronize()
     dec_ms = [s[3]["decode_ms"] for s in steps]
-    toks0, m0, tr0, _ = steps[0]
+    toks0, m0, tr0, last0 = steps[0]
     assert all(s[0] == toks0 for s in steps), "decode is not deterministic across steps"
     value = NEW_TOKENS * len(steps) / (sum(dec_ms) / 1e3)
     launches = sum(s[3]["gpu_launches"] for s in steps)
+
+    # the other single-device schedule on the same engine: identical tokens,
+    # metrics and trace, its own time
+    other = "pipelined" if last0["schedule"] == "folded" else "folded"
+    alt = None
+    try:
+        eng.set_schedule(other)
+        alt_ms = []
+        for _ in range(max(1, min(3, args.steps))):
+            t_, m_, tr_ = eng.decode(prompt, NEW_TOKENS)
+            assert t_ == toks0 and m_ == m0 and tr_.to_csv() == tr0.to_csv(), \
+                f"{other} schedule differs from {last0['schedule']}"
+            alt_ms.append(eng.last["decode_ms"])
+        alt_bytes, alt_bd = algorithmic_bytes(tr_, config, cfg, PROMPT_LEN, eng.last)
+        alt = {"schedule": other, "tokens_per_s": round(NEW_TOKENS / (np.median(alt_ms) / 1e3), 3),
+               "ms_per_step": round(float(np.median(alt_ms)), 3), "gpu_launches": eng.last["gpu_launches"],
+               "step_gbs": round(alt_bytes / (np.median(alt_ms) / 1e3) / 1e9, 1), **alt_bd}
+    except (ValueError, NotImplementedError):
+        alt = None
+    finally:
+        eng.set_schedule("auto")
 
     # end to end through the public API: host prompt -> tokens/trace on host
     e2e_times = []
@@ -192,7 +229,7 @@ def run_ours(args):
     reps = 50
     gu_ms, gu_bytes = eng.probe_gemv(2, cfg.n_stages, reps)
     achieved = gu_bytes / (gu_ms / 1e3) / 1e9
-    step_bytes, breakdown = algorithmic_bytes(tr0, config, cfg, PROMPT_LEN)
+    step_bytes, breakdown = algorithmic_bytes(tr0, config, cfg, PROMPT_LEN, last0)
     step_gbs = step_bytes / (np.median(dec_ms) / 1e3) / 1e9
     alpha = m0.alpha_all_measured
     traffic = None
@@ -214,7 +251,8 @@ def run_ours(args):
                                "prompt 128, 512 new tokens",
                    "model": "llama2-7b-shape", "exit_depth": EXIT_DEPTH, "n_stages": cfg.n_stages,
                    "deep_scale": args.deep_scale, "prompt_len": PROMPT_LEN, "new_tokens": NEW_TOKENS,
-                   "kv_dtype": config.kv_dtype, "parallelism": "pp-stages grouped on 1 GPU",
+                   "kv_dtype": config.kv_dtype, "schedule": last0["schedule"],
+                   "parallelism": "pp-stages on 1 GPU (" + last0["schedule"] + " schedule)",
                    "l2": "inputs larger than L2 (13.5 GB weights streamed per step)"},
         "e2e": {"value": round(e2e_val, 3), "unit": "tokens/s", "h2d_bytes_per_step": 4 * PROMPT_LEN,
                 "d2h_bytes_per_step": 4 * NEW_TOKENS + 24 * len(tr0) + 88,
@@ -232,6 +270,7 @@ def run_ours(args):
         "ppsd_speedup_eq7": ppsd.ppsd_speedup(alpha, config.n_layers, EXIT_DEPTH) if alpha is not None else None,
         "ar_tokens_per_s": round(ar_tps, 3), "speedup_vs_our_ar": round(value / ar_tps, 4),
         "prefill_ms": round(steps[0][3]["prefill_ms"], 3),
+        "other_schedule": alt,
     }
     if cpu:
         line["cpu_baseline"] = cpu

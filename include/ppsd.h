@@ -97,7 +97,21 @@ typedef struct {
   int32_t comm_latency; /* pipesim.py:72, 107-110 */
   int32_t stage_lo, stage_hi; /* local stages (1-based, inclusive); 0,0 = all */
   int32_t device;
+  int32_t schedule;     /* PPSD_SCHEDULE_*: how one device executes the machine */
 } ppsd_pipeline_desc;
+
+/* Execution schedule of a single-device engine (all stages local). Both give
+ * the machine's exact tokens, metrics and trace; they differ in when the
+ * stage forwards run:
+ *   PIPELINED: every planned (stage, chain) forward in its tick, the stages'
+ *              work grouped into one launch per layer slot;
+ *   FOLDED:    shallow stages + exit head at launch, deep stages of all
+ *              in-flight chains in one batched weight pass when a verdict
+ *              needs them (greedy, or sampling with exit_stage 1);
+ *   AUTO:      FOLDED where it applies, else PIPELINED. */
+#define PPSD_SCHEDULE_AUTO 0
+#define PPSD_SCHEDULE_PIPELINED 1
+#define PPSD_SCHEDULE_FOLDED 2
 
 typedef struct {
   int64_t committed_tokens, ticks, accepts, rejects; /* RunMetrics order */
@@ -106,6 +120,11 @@ typedef struct {
   double decode_ms;     /* CUDA-event time of the decode loop (prefill excluded) */
   double prefill_ms;    /* CUDA-event time of the prompt prefill */
   int64_t gpu_launches; /* kernels this engine launched for the call */
+  /* execution accounting (not RunMetrics): the schedule that ran
+   * (PPSD_SCHEDULE_PIPELINED / FOLDED) and, folded, the deep batches, the
+   * chains they carried and the sum of those chains' positions */
+  int32_t schedule;
+  int64_t deep_batches, deep_vectors, deep_pos_sum;
 } ppsd_metrics;
 
 typedef struct {
@@ -129,6 +148,12 @@ int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t
                 int32_t n_prompt, int32_t max_tokens, int32_t force_reject, int32_t* out_tokens,
                 ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
                 int64_t* trace_len);
+
+/* Change the engine's schedule (PPSD_SCHEDULE_*) for later decodes;
+ * PPSD_EUNSUPPORTED when FOLDED cannot apply. get_schedule reports the
+ * schedule a ppsd_decode in the given mode would run. */
+int ppsd_set_schedule(ppsd_engine* e, int32_t schedule);
+int ppsd_get_schedule(ppsd_engine* e, int32_t greedy, int32_t* schedule);
 
 /* full-model autoregressive decode (the oracle / AR baseline); sampling mode
  * draws one commit-stream uniform per token (pipesim.py:397-406) */

@@ -16,6 +16,8 @@ LIB_PATH = os.path.join(HERE, "libppsd.so")
 
 PPSD_OK, PPSD_EINVAL, PPSD_ECUDA, PPSD_ESTATE, PPSD_EUNSUPPORTED = 0, -1, -2, -3, -4
 MODEL_BERNOULLI, MODEL_TOYLM, MODEL_TRANSFORMER = 0, 1, 2
+# execution schedules of a single-device engine (include/ppsd.h PPSD_SCHEDULE_*)
+SCHEDULES = {"auto": 0, "pipelined": 1, "folded": 2}
 
 
 class ModelDesc(C.Structure):
@@ -44,7 +46,7 @@ class PipelineDesc(C.Structure):
     _fields_ = [
         ("n_layers", C.c_int32), ("exit_depth", C.c_int32), ("exit_stage", C.c_int32),
         ("comm_latency", C.c_int32), ("stage_lo", C.c_int32), ("stage_hi", C.c_int32),
-        ("device", C.c_int32),
+        ("device", C.c_int32), ("schedule", C.c_int32),
     ]
 
 
@@ -54,7 +56,8 @@ class Metrics(C.Structure):
         ("rejects", C.c_int64), ("alpha_valid", C.c_int32),
         ("alpha_all_measured", C.c_double), ("throughput", C.c_double),
         ("speedup_vs_ar", C.c_double), ("decode_ms", C.c_double), ("prefill_ms", C.c_double),
-        ("gpu_launches", C.c_int64),
+        ("gpu_launches", C.c_int64), ("schedule", C.c_int32), ("deep_batches", C.c_int64),
+        ("deep_vectors", C.c_int64), ("deep_pos_sum", C.c_int64),
     ]
 
 
@@ -72,6 +75,8 @@ EXPORTS = {
     "ppsd_decode": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
                               C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics),
                               C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
+    "ppsd_set_schedule": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ppsd_get_schedule": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "ppsd_decode_ar": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
                                  C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics)]),
     "ppsd_decode_eesd": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,

@@ -59,6 +59,7 @@ struct ppsd_engine {
   Sched* d_sched = nullptr;
   Work* d_work = nullptr;
   Work* d_work_ar = nullptr;
+  Work* d_work_deep = nullptr;  // folded schedule: the deep batch
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
   int32_t* d_tokens = nullptr;
@@ -94,6 +95,12 @@ struct ppsd_engine {
   const float* rope_sin = nullptr;
   // graphs
   cudaGraphExec_t g_tick = nullptr, g_ar = nullptr, g_prefill = nullptr;
+  // folded schedule (sched.h: sched_fold_plan): one graph per tick =
+  // [sched, shallow layers, exit head, IF(deep batch){deep layers, final heads}]
+  cudaGraphExec_t g_fold = nullptr;
+  bool fold_ok = false;      // engine can run the folded schedule
+  int schedule = PPSD_SCHEDULE_AUTO;
+  int64_t fold_tick_launches = 0, fold_deep_launches = 0;
   cudaGraphExec_t g_compute = nullptr, g_finish = nullptr, g_mr_prefill = nullptr;  // multi-rank
   std::map<int, std::pair<cudaGraphExec_t, int64_t>> eesd_graphs;  // per gamma: round graph, launches
   EesdState* d_eesd = nullptr;
@@ -134,7 +141,8 @@ static int attn_grid(const ppsd_engine* e) { return 4 * e->num_sms; }
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
 
-static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, bool batched = false) {
+static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, bool batched = false,
+                                float* logits = nullptr) {
   const GemvPlan& p = batched ? e->gpb[mat] : e->gp[mat];
   GemvArgs a{};
   a.work = w;
@@ -153,7 +161,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   a.q = e->d_q;
   a.o = e->d_o;
   a.h = e->d_h;
-  a.logits = e->d_logits;
+  a.logits = logits ? logits : e->d_logits;
   a.rope_cos = e->rope_cos;
   a.rope_sin = e->rope_sin;
   a.page_table = e->d_page_table;
@@ -255,6 +263,95 @@ static int capture(ppsd_engine* e, F body, cudaGraphExec_t* out, int64_t* nlaunc
   return PPSD_OK;
 }
 
+// Folded tick graph. The deep batch runs only in ticks that need a verdict
+// the batch has not produced yet, so it sits behind a graph IF node whose
+// condition the scheduler kernel (first node) sets for this launch; the
+// handle resets to 0 at every launch (cudaGraphCondAssignDefault).
+static int build_fold_graph(ppsd_engine* e) {
+  const int shallow = e->cfg.shallow_layers, deep = e->md.n_layers - shallow;
+  cudaStream_t main_st = e->st, body_st = nullptr;
+  CU(cudaStreamCreateWithFlags(&body_st, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  int n_outer = 0, n_body = 0;
+  bool ok = true;
+  std::string err;
+  auto need = [&](bool cond, const char* what) {
+    if (!cond && ok) {
+      ok = false;
+      err = std::string(what) + ": " + cudaGetErrorString(cudaGetLastError());
+    }
+  };
+  cudaError_t ce = cudaStreamBeginCapture(main_st, cudaStreamCaptureModeThreadLocal);
+  if (ce != cudaSuccess) {
+    cudaStreamDestroy(body_st);
+    CU(ce);
+  }
+  need(launch_pdl(sched_tick_kernel, dim3(1), dim3(256), 0, main_st, (const TickCtx*)e->d_ctx, 0) ==
+           cudaSuccess, "sched");
+  n_outer = 1;
+  if (ok) {
+    const int m = enqueue_layers(e, e->d_work, shallow, false);
+    need(m >= 0, "shallow layers");
+    n_outer += m;
+  }
+  need(ok && enqueue_gemv(e, e->d_work, 0, kMatHead) == cudaSuccess, "exit head");
+  n_outer += 1;
+  cudaGraphNode_t cnode = nullptr;
+  cudaGraph_t body = nullptr;
+  if (ok) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg = nullptr;
+    need(cudaStreamGetCaptureInfo(main_st, &cs, nullptr, &cg, &deps, &nd) == cudaSuccess, "capture info");
+    cudaGraphConditionalHandle h = 0;
+    if (ok) need(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault) == cudaSuccess,
+                 "conditional handle");
+    if (ok) {
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeIf;
+      cp.conditional.size = 1;
+      need(cudaGraphAddNode(&cnode, cg, deps, nd, &cp) == cudaSuccess, "conditional node");
+      if (ok) body = cp.conditional.phGraph_out[0];
+      if (ok) need(cudaStreamUpdateCaptureDependencies(main_st, &cnode, 1, cudaStreamSetCaptureDependencies) ==
+                       cudaSuccess, "capture deps");
+      e->h_ctx.cond = h;
+    }
+  }
+  if (ok) {  // body: deep layers of the batch (batched plans), final heads
+    need(cudaStreamBeginCaptureToGraph(body_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+             cudaSuccess, "body capture");
+    if (ok) {
+      e->st = body_st;
+      const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+      need(m >= 0, "deep layers");
+      n_body = m;
+      need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
+           "final heads");
+      n_body += 1;
+      e->st = main_st;
+      cudaGraph_t bg = body;
+      need(cudaStreamEndCapture(body_st, &bg) == cudaSuccess, "body end capture");
+    }
+  }
+  e->st = main_st;
+  ce = cudaStreamEndCapture(main_st, &g);
+  cudaStreamDestroy(body_st);
+  if (!ok) {
+    if (g) cudaGraphDestroy(g);
+    return fail(PPSD_ECUDA, "folded tick graph: " + err);
+  }
+  CU(ce);
+  ce = cudaGraphInstantiate(&e->g_fold, g, 0);
+  cudaGraphDestroy(g);
+  CU(ce);
+  e->fold_tick_launches = n_outer;
+  e->fold_deep_launches = n_body;
+  return PPSD_OK;
+}
+
 static int build_graphs(ppsd_engine* e) {
   const int kind = e->md.kind;
   int rc = capture(
@@ -308,6 +405,7 @@ static int build_graphs(ppsd_engine* e) {
       },
       &e->g_prefill, &e->prefill_launches);
   if (rc) return rc;
+  if (e->fold_ok) return build_fold_graph(e);
   return PPSD_OK;
 }
 
@@ -318,6 +416,7 @@ static void free_engine(ppsd_engine* e) {
   cudaSetDevice(e->device);
   if (e->st) cudaStreamSynchronize(e->st);
   if (e->g_tick) cudaGraphExecDestroy(e->g_tick);
+  if (e->g_fold) cudaGraphExecDestroy(e->g_fold);
   if (e->g_ar) cudaGraphExecDestroy(e->g_ar);
   if (e->g_prefill) cudaGraphExecDestroy(e->g_prefill);
   if (e->g_compute) cudaGraphExecDestroy(e->g_compute);
@@ -334,7 +433,7 @@ static void free_engine(ppsd_engine* e) {
                   (void*)e->d_umws, (void*)e->d_umcnt})
     if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
-  void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+  void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
                   e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
@@ -432,6 +531,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   CU(dalloc(&e->d_sched, sizeof(Sched)));
   CU(dalloc(&e->d_work, sizeof(Work)));
   CU(dalloc(&e->d_work_ar, sizeof(Work)));
+  CU(dalloc(&e->d_work_deep, sizeof(Work)));
   CU(dalloc(&e->d_ctx, sizeof(TickCtx)));
   CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
   CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
@@ -442,6 +542,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.sched = e->d_sched;
   c.work = e->d_work;
   c.work_ar = e->d_work_ar;
+  c.work_deep = e->d_work_deep;
   c.tokens = e->d_tokens;
   c.model = md->kind;
   c.lo = e->lo;
@@ -543,7 +644,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_h, sizeof(float) * nb * d.ffn));
-    CU(dalloc(&e->d_logits, sizeof(float) * kMaxVec * (size_t)d.V));
+    CU(dalloc(&e->d_logits, sizeof(float) * (kMaxVec + 1) * (size_t)d.V));  // folded: exit + batch rows
     CU(dalloc(&e->d_attn_part, sizeof(float) * nb * d.H * e->max_pages * (d.hd + 2)));
     CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * nb * d.KV));
     CU(dalloc(&e->d_head_part, sizeof(float) * 2 * kMaxVec * (size_t)e->num_sms));
@@ -552,6 +653,13 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     c.x = e->d_x;
     int rc = setup_umma(e, shapes);
     if (rc) return rc;
+    // folded schedule: single-device engine, every in-flight chain fits one batch
+    e->schedule = pd->schedule;
+    e->fold_ok = e->lo == 1 && e->hi == e->S && sched_fold_width(&e->cfg) <= kMaxVec &&
+                 pd->schedule != PPSD_SCHEDULE_PIPELINED;
+    if (pd->schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
+      return fail(PPSD_EUNSUPPORTED, "folded schedule needs all stages on this device and at most " +
+                                         std::to_string(kMaxVec) + " chains in flight");
   } else if (md->kind != PPSD_MODEL_BERNOULLI) {
     return fail(PPSD_EINVAL, "unknown model kind");
   }
@@ -666,9 +774,14 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
     int rc = ensure_trace(e, cap);
     if (rc) return rc;
   }
+  // folded schedule: greedy model decodes, and sampling when the draft is
+  // drawn in the launch tick (exit_stage 1: the eager exit logits are current)
+  const bool fold = e->fold_ok && e->schedule != PPSD_SCHEDULE_PIPELINED && model != 0 &&
+                    (e->h_ctx.greedy || e->cfg.k == 1);
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
+  s.c.fold = fold ? 1 : 0;
   s.c.model = model;
   s.c.force_reject = force_reject;
   s.c.stop = stop;
@@ -680,19 +793,27 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   e->h_ctx.inbox = nullptr;  // single-rank run
   e->h_ctx.outbox = nullptr;
   e->h_ctx.trace_cap = cap;
+  e->h_ctx.fold = fold ? 1 : 0;
   CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
   CU(cudaMemcpyAsync(e->d_sched, &s, sizeof(Sched), cudaMemcpyHostToDevice, e->st));
   CU(cudaEventRecord(e->ev0, e->st));
-  sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 1);
-  CU(cudaGetLastError());
-  launches += 1;
+  cudaGraphExec_t tick = e->g_tick;
+  int64_t per_tick = e->tick_launches;
+  if (fold) {  // the graph's scheduler node plans tick 1 (finishing "tick 0" is a no-op)
+    tick = e->g_fold;
+    per_tick = e->fold_tick_launches;
+  } else {
+    sched_tick_kernel<<<1, 256, 0, e->st>>>(e->d_ctx, 1);
+    CU(cudaGetLastError());
+    launches += 1;
+  }
   int64_t committed = 0, ticks_launched = 0;
   // small readback: committed .. error (8 int32 after SchedCfg)
   const size_t off = offsetof(Sched, t);
   const size_t len = offsetof(Sched, verify_counter) - off;
   for (;;) {
     const int64_t n = std::max<int64_t>(1, (int64_t)stop - committed);
-    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(e->g_tick, e->st));
+    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(tick, e->st));
     ticks_launched += n;
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
                        cudaMemcpyDeviceToHost, e->st));
@@ -714,7 +835,11 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   if (s.error & kErrTrace) return fail(PPSD_ESTATE, "trace buffer too small");
   fill_metrics(e, s, out);
   out->decode_ms = ms;
-  out->gpu_launches = launches + ticks_launched * e->tick_launches;
+  out->gpu_launches = launches + ticks_launched * per_tick + (int64_t)s.fold_batches * e->fold_deep_launches;
+  out->schedule = fold ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
+  out->deep_batches = s.fold_batches;
+  out->deep_vectors = s.fold_vectors;
+  out->deep_pos_sum = s.fold_pos_sum;
   if (trace) {
     const int64_t nrows = std::min<int64_t>(s.trace_n, trace_cap);
     if (nrows > 0)
@@ -767,6 +892,23 @@ extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, co
   out->prefill_ms = pre_ms;
   if (out_tokens)
     CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * max_tokens, cudaMemcpyDeviceToHost));
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_set_schedule(ppsd_engine* e, int32_t schedule) {
+  if (!e) return fail(PPSD_EINVAL, "null argument");
+  if (schedule < PPSD_SCHEDULE_AUTO || schedule > PPSD_SCHEDULE_FOLDED) return fail(PPSD_EINVAL, "unknown schedule");
+  if (schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
+    return fail(PPSD_EUNSUPPORTED, "this engine cannot run the folded schedule");
+  e->schedule = schedule;
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_get_schedule(ppsd_engine* e, int32_t greedy, int32_t* schedule) {
+  if (!e || !schedule) return fail(PPSD_EINVAL, "null argument");
+  const bool fold = e->fold_ok && e->schedule != PPSD_SCHEDULE_PIPELINED && e->md.kind == PPSD_MODEL_TRANSFORMER &&
+                    (greedy || e->cfg.k == 1);
+  *schedule = fold ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
   return PPSD_OK;
 }
 

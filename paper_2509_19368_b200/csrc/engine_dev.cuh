@@ -50,6 +50,12 @@ struct TickCtx {
   uint64_t* xcount;         // exchange counter (device)
   int32_t* xerr;            // sticky p2p wait timeout flag (device)
   int32_t prefill_chunk; // prompt tokens per batched prefill launch (<= kMaxVec)
+  // folded single-GPU execution (sched.h: sched_fold_plan): `work` carries
+  // the launched chain's shallow stages + exit head, `work_deep` the deep
+  // batch + final heads, gated by the graph conditional `cond`
+  int32_t fold;
+  Work* work_deep;
+  unsigned long long cond;  // cudaGraphConditionalHandle of the folded tick graph
 };
 
 constexpr int kBoxHeader = 4;

@@ -82,6 +82,22 @@ void ppsdh_finish(void* p, int exit_tok, int final_tok) {
   sched_finish(&h->s, exit_tok, final_tok, h->tokens, h->pdig, h->trace, h->cap);
 }
 
+// folded schedule (sched.h: sched_fold_plan)
+void ppsdh_set_fold(void* p, int on) { ((HostSched*)p)->s.c.fold = on; }
+int ppsdh_fold_width(void* p) { return sched_fold_width(&((HostSched*)p)->s.c); }
+
+// out: [fold_row, fold_nb, fold_base, deep_done, shallow_layers, deep_done before]
+void ppsdh_fold_plan(void* p, int32_t* out) {
+  HostSched* h = (HostSched*)p;
+  out[5] = h->s.deep_done;
+  sched_fold_plan(&h->s);
+  out[0] = h->s.fold_row;
+  out[1] = h->s.fold_nb;
+  out[2] = h->s.fold_base;
+  out[3] = h->s.deep_done;
+  out[4] = h->s.c.shallow_layers;
+}
+
 int ppsdh_chain_pos(void* p, int slot) { return ((HostSched*)p)->s.ch_pos[slot]; }
 int ppsdh_chain_tok(void* p, int slot) { return ((HostSched*)p)->s.ch_tok[slot]; }
 uint64_t ppsdh_prefix_digest(void* p, int n) { return ((HostSched*)p)->pdig[n]; }

@@ -20,7 +20,11 @@ __device__ void sampling_tick(const TickCtx& c, Sched& s, int* exit_tok, int* fi
   const double* l64 = c.logits64;
   const float* l32 = c.logits32;
   if (s.final_slot >= 0) {  // verdict first: its draws do not interleave with the draft stream
-    block_softmax(l64 ? l64 + V : nullptr, l32 ? l32 + V : nullptr, V, c.qbuf, exact);
+    // folded: the final logits of the deep batch sit in rows 1.. (position order)
+    const float* q32 = !l32 ? nullptr
+                       : c.fold ? l32 + (size_t)(1 + s.ch_pos[s.final_slot] - s.fold_base) * V
+                                : l32 + V;
+    block_softmax(l64 ? l64 + V : nullptr, q32, V, c.qbuf, exact);
     const double* p = c.pdist + (size_t)s.final_slot * V;
     const int d = s.ch_tok[s.final_slot];
     __shared__ int s_ok;
@@ -156,24 +160,55 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       exit_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_k * c.box_words)[0];
       final_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_S * c.box_words)[1];
     }
+    if (c.fold && !begin) {
+      // the chain launched last tick ran its shallow stages and exit head eagerly
+      if (s.launched) s.ch_draft[s.work[1]] = c.work->head_out[0];
+      if (c.greedy) exit_tok = s.exit_slot >= 0 ? s.ch_draft[s.exit_slot] : -1;
+      final_tok = (c.greedy && s.final_slot >= 0)
+                      ? c.work_deep->vec_out[s.ch_pos[s.final_slot] - s.fold_base] : final_tok;
+    }
     if (!begin)
       sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap, s_final_ok);
     sched_plan(&s);
     Work* w = c.work;
-    w->G = c.hi - c.lo + 1;
-    for (int g = 0; g < w->G; ++g) {
-      const int st = c.lo + g;
-      const int slot = s.work[st];
-      w->slot[g] = slot;
-      w->pos[g] = slot >= 0 ? s.c.n_prompt + s.ch_pos[slot] - 2 : 0;
-      w->first[g] = s.c.stage_first[st];
-      w->nl[g] = s.c.stage_layers[st];
-      w->nv[g] = 1;
+    if (c.fold) {  // sched.h: sched_fold_plan
+      sched_fold_plan(&s);
+      const int row = s.fold_row;
+      w->G = 1;
+      w->slot[0] = row;
+      w->pos[0] = row >= 0 ? s.c.n_prompt + s.ch_pos[s.work[1]] - 2 : 0;
+      w->first[0] = 0;
+      w->nl[0] = s.c.shallow_layers;
+      w->nv[0] = 1;
+      w->head_slot[0] = row;
+      w->head_slot[1] = -1;
+      Work* wd = c.work_deep;
+      wd->G = 1;
+      wd->slot[0] = s.fold_nb > 0 ? 0 : -1;
+      wd->pos[0] = s.c.n_prompt + s.fold_base - 2;
+      wd->first[0] = s.c.shallow_layers;
+      wd->nl[0] = s.c.n_layers - s.c.shallow_layers;
+      wd->nv[0] = s.fold_nb > 0 ? s.fold_nb : 1;
+      wd->head_slot[0] = wd->head_slot[1] = -1;
+      if (s.fold_nb > 0) cudaGraphSetConditional(c.cond, 1u);
+      s_launch_slot = row;
+      s_launch_pos = row >= 0 ? s.ch_pos[s.work[1]] : 0;
+    } else {
+      w->G = c.hi - c.lo + 1;
+      for (int g = 0; g < w->G; ++g) {
+        const int st = c.lo + g;
+        const int slot = s.work[st];
+        w->slot[g] = slot;
+        w->pos[g] = slot >= 0 ? s.c.n_prompt + s.ch_pos[slot] - 2 : 0;
+        w->first[g] = s.c.stage_first[st];
+        w->nl[g] = s.c.stage_layers[st];
+        w->nv[g] = 1;
+      }
+      w->head_slot[0] = (s.c.k >= c.lo && s.c.k <= c.hi) ? s.exit_slot : -1;
+      w->head_slot[1] = (s.c.S >= c.lo && s.c.S <= c.hi) ? s.final_slot : -1;
+      s_launch_slot = (s.launched && c.lo == 1) ? s.work[1] : -1;
+      s_launch_pos = s_launch_slot >= 0 ? s.ch_pos[s_launch_slot] : 0;
     }
-    w->head_slot[0] = (s.c.k >= c.lo && s.c.k <= c.hi) ? s.exit_slot : -1;
-    w->head_slot[1] = (s.c.S >= c.lo && s.c.S <= c.hi) ? s.final_slot : -1;
-    s_launch_slot = (s.launched && c.lo == 1) ? s.work[1] : -1;
-    s_launch_pos = s_launch_slot >= 0 ? s.ch_pos[s_launch_slot] : 0;
   }
   __syncthreads();
   const int slot = s_launch_slot;

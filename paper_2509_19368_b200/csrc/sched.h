@@ -44,11 +44,12 @@ struct SchedCfg {
   int32_t stop;         // stop_commits (max_tokens / horizon)
   int32_t n_prompt;
   int32_t nslot;
-  int32_t pad_;
+  int32_t fold;         // 1: folded single-GPU execution (sched_fold_plan)
   double alpha;         // Bernoulli acceptance rate
   uint64_t verify_seed; // derive_seed(rng.seed, "verify") (pipesim.py:693)
   int32_t stage_layers[kMaxStages + 1];  // 1-based
   int32_t stage_first[kMaxStages + 1];   // global index of the stage's first layer
+  int32_t shallow_layers;                // layers of stages 1..k (the exit layer k*E)
 };
 
 struct Sched {
@@ -65,6 +66,16 @@ struct Sched {
   int32_t work[kMaxStages + 2];  // chain slot each stage runs this tick, -1 idle
   int32_t tq_ready[kTransitCap], tq_dest[kTransitCap], tq_slot[kTransitCap];
   int32_t ch_pos[kMaxSlots], ch_layer[kMaxSlots], ch_tok[kMaxSlots];
+  // folded execution (sched_fold_plan): see the comment there
+  int32_t deep_done;     // highest position whose deep stages + final head ran on the current prefix
+  int32_t fold_base;     // first position of the latest deep batch
+  int32_t fold_nb;       // vectors in this tick's deep batch, 0 = none
+  int32_t fold_row;      // fold row of the chain launched this tick, -1 = none
+  int32_t fold_batches;  // deep batches run so far
+  int32_t fold_pad_;
+  int64_t fold_vectors;  // chains that went through a deep batch
+  int64_t fold_pos_sum;  // sum of their positions (attention context accounting)
+  int32_t ch_draft[kMaxSlots];  // eager exit-head argmax per chain
 };
 
 constexpr int32_t kNone = -1;
@@ -81,6 +92,11 @@ PPSD_HD void sched_reset(Sched* s) {
   s->exit_slot = s->final_slot = kNone;
   s->tq_head = s->tq_n = 0;
   for (int i = 0; i <= s->c.S + 1; ++i) s->cur[i] = s->work[i] = kNone;
+  s->deep_done = s->fold_base = 0;
+  s->fold_nb = 0;
+  s->fold_row = kNone;
+  s->fold_batches = 0;
+  s->fold_vectors = s->fold_pos_sum = 0;
 }
 
 PPSD_HD void sched_trace(Sched* s, TraceRow* tr, int64_t cap, int st, int kind, int pos, int tok,
@@ -219,6 +235,7 @@ PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens
     sched_emit(s, slot, 1, tr, cap);
   }
   if (rollback != kNone) {  // pipesim.py:779-786
+    if (s->c.fold) s->deep_done = rollback;  // deep results past the rollback belong to flushed chains
     s->tq_n = 0;
     for (int st = 1; st <= S; ++st) s->cur[st] = kNone;
     s->draft_head = rollback;
@@ -227,6 +244,43 @@ PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens
   }
   if (s->committed >= s->c.stop) s->done = 1;
 }
+
+// Folded execution of the machine on ONE device (SchedCfg.fold). Every stage
+// shares one HBM, so time is bytes: instead of running each planned
+// (stage, chain) forward in the tick it is planned (the pipelined schedule,
+// one weight pass per stage per tick), the engine
+//   * runs a chain's shallow stages 1..k (layers [0, k*E)) and its exit head
+//     in the tick it is launched (the draft is then known early; the machine
+//     still emits it at stage k, sched_finish, from ch_draft), and
+//   * defers the deep stages k+1..S until a verdict needs them: in the tick the
+//     chain at stage S has no deep result yet, ALL launched chains past
+//     deep_done (positions deep_done+1 .. draft_head, consecutive, at most the
+//     (S-1)*per+1 chains in flight) go through layers [k*E, N) and the final
+//     head as ONE batch of vectors, i.e. one weight pass for up to S chains.
+// Chains flushed by a rollback never run their deep stages unless they were
+// already batched. Ticks, verdicts, tokens and the trace are exactly those of
+// the machine: only WHEN a forward runs changes, and the batched GEMV rows are
+// bit-identical to single-vector ones (gemv.cu), so the hidden states are too.
+// Chain rows: the chain at position p lives in activation row
+// p - deep_done - 1 (deep_done at its launch; a batch or rollback only moves
+// deep_done past or back to chains no longer in flight), so a deep batch is
+// rows 0 .. fold_nb-1 in position order.
+PPSD_HD void sched_fold_plan(Sched* s) {
+  s->fold_row = kNone;
+  s->fold_nb = 0;
+  if (s->launched) s->fold_row = s->ch_pos[s->work[1]] - s->deep_done - 1;
+  if (s->final_slot != kNone && s->ch_pos[s->final_slot] > s->deep_done) {
+    s->fold_base = s->deep_done + 1;
+    s->fold_nb = s->draft_head - s->deep_done;
+    s->deep_done = s->draft_head;
+    s->fold_batches += 1;
+    s->fold_vectors += s->fold_nb;
+    s->fold_pos_sum += (int64_t)s->fold_nb * (s->fold_base + s->draft_head) / 2;
+  }
+}
+
+// Largest fold row / batch the folded schedule can need: chains in flight.
+PPSD_HD int sched_fold_width(const SchedCfg* c) { return (c->S - 1) * c->per + 1; }
 
 // Host-side configuration helper (also used by the CPU test build).
 PPSD_HD int sched_configure(SchedCfg* c, int n_layers, int exit_depth, int exit_stage,
@@ -247,6 +301,8 @@ PPSD_HD int sched_configure(SchedCfg* c, int n_layers, int exit_depth, int exit_
     c->stage_first[st] = first;
     first += nl;
   }
+  c->shallow_layers = c->stage_first[k] + c->stage_layers[k];
+  c->fold = 0;
   c->nslot = (S - 1) * c->per + 2;
   if (c->nslot > kMaxSlots || S * c->per + 2 > kTransitCap) return -1;
   return 0;

@@ -72,6 +72,18 @@ class Engine:
     def close(self):
         self._fin()
 
+    def set_schedule(self, schedule: str) -> None:
+        """'auto' | 'pipelined' | 'folded' (include/ppsd.h PPSD_SCHEDULE_*)."""
+        if schedule not in _lib.SCHEDULES:
+            raise ValueError(f"schedule must be one of {sorted(_lib.SCHEDULES)}, got {schedule!r}")
+        _lib.check(_lib.lib().ppsd_set_schedule(self.h, _lib.SCHEDULES[schedule]), "set_schedule")
+
+    def schedule(self, mode: str = "greedy") -> str:
+        """The schedule a decode in `mode` runs on this engine."""
+        out = C.c_int32()
+        _lib.check(_lib.lib().ppsd_get_schedule(self.h, int(mode == "greedy"), C.byref(out)), "get_schedule")
+        return {v: k for k, v in _lib.SCHEDULES.items()}[out.value]
+
     # -- helpers ---------------------------------------------------------
     def _trace_cap(self, stop: int) -> int:
         c = self.cfg
@@ -79,7 +91,10 @@ class Engine:
 
     def _finish(self, m: _lib.Metrics, rows: np.ndarray | None, n_rows: int):
         self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
-                         ticks=m.ticks, committed=m.committed_tokens)
+                         ticks=m.ticks, committed=m.committed_tokens,
+                         schedule={v: k for k, v in _lib.SCHEDULES.items()}.get(m.schedule, "pipelined"),
+                         deep_batches=m.deep_batches, deep_vectors=m.deep_vectors,
+                         deep_pos_sum=m.deep_pos_sum)
         metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects,
                                m.accepts + m.rejects, self.cfg.ar_ticks_per_token)
         trace = EventTrace.from_array(rows[:n_rows]) if rows is not None else EventTrace()
@@ -195,6 +210,7 @@ def engine_for(lm, cfg: PipelineConfig) -> Engine:
         key = _cfg_key(cfg)
         if key not in cache:
             cache[key] = Engine(lm.model_desc(), lm.weights_struct(), cfg, device=lm.device.index)
+        cache[key].set_schedule(getattr(lm, "schedule", "auto"))
         return cache[key]
     if isinstance(lm, ToyLM):
         dev = _lib.require_cuda().index

@@ -126,7 +126,12 @@ class TransformerLM:
     deep_from: the deterministic misalignment knob that sets how often the
     early-exit head agrees with the final head. `layers`
     restricts materialisation to a [lo, hi) layer range (one pipeline rank).
+    `schedule` picks how a single-device engine executes the machine
+    ('auto' | 'pipelined' | 'folded', include/ppsd.h PPSD_SCHEDULE_*); every
+    schedule returns the same tokens, metrics and trace.
     """
+
+    schedule = "auto"
 
     def __init__(self, config: TransformerConfig, seed: int = 0, deep_scale: float = 1.0,
                  deep_from: int | None = None, device=None, layers: tuple[int, int] | None = None,

@@ -39,6 +39,9 @@ def lib():
         L.ppsdh_destroy.argtypes = [C.c_void_p]
         L.ppsdh_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.ppsdh_finish.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ppsdh_set_fold.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_fold_width.argtypes = [C.c_void_p]
+        L.ppsdh_fold_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.ppsdh_chain_pos.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_chain_tok.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_prefix_digest.argtypes = [C.c_void_p, C.c_int]
@@ -77,6 +80,17 @@ class HostSched:
     def plan(self):
         r = lib().ppsdh_plan(self.h, self.work, self.info)
         return r, list(self.work), list(self.info)
+
+    def set_fold(self, on=True):
+        lib().ppsdh_set_fold(self.h, int(on))
+
+    def fold_width(self):
+        return lib().ppsdh_fold_width(self.h)
+
+    def fold_plan(self):
+        out = (C.c_int32 * 6)()
+        lib().ppsdh_fold_plan(self.h, out)
+        return list(out)
 
     def finish(self, exit_tok=-1, final_tok=-1):
         lib().ppsdh_finish(self.h, exit_tok, final_tok)
@@ -152,6 +166,67 @@ def run_toy(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=0, comm_latenc
         hs.finish(e, f)
     m = hs.metrics()
     return hs.tokens(m[0]), m, hs.trace_rows()
+
+
+def run_toy_folded(lm, n_layers, exit_depth, prompt, stop, *, exit_stage=0, comm_latency=0,
+                   force_reject=False, max_batch=16):
+    """Folded single-device emulation (sched.h: sched_fold_plan), mirroring
+    what sched_tick_kernel and the folded tick graph do: the launched chain's
+    shallow stages + exit head run in its launch tick (the draft is kept per
+    chain until the machine emits it at stage k); when the chain at stage S
+    has no deep result, every chain past deep_done goes through the deep
+    layers + final head as one batch in fold rows 0..nb-1. Checks the row and
+    batch invariants the device kernels rely on. Returns (tokens, metrics,
+    trace, batch sizes)."""
+    hs = HostSched(n_layers, exit_depth, exit_stage=exit_stage, comm_latency=comm_latency,
+                   model=1, force_reject=force_reject, stop=stop, prompt=prompt, toy_seed=lm.seed)
+    hs.set_fold(True)
+    if stop == 0:
+        return [], sp.make_metrics(0, 0, 0, 0, 0, hs.S * hs.per), [], []
+    width = hs.fold_width()
+    assert width <= max_batch
+    shallow = sum(hs.layers[:(exit_stage or 1)])
+    draft = {}       # slot -> eager exit-head argmax
+    row_pos = {}     # fold row -> position of the chain living there
+    final = []       # final-head argmax per vector of the latest batch
+    base = 0
+    batches = []
+    while True:
+        r, work, info = hs.plan()
+        if not r:
+            break
+        launched, exit_slot, final_slot = info[1], info[2], info[3]
+        row, nb, fbase, deep_done, shallow_c, deep_before = hs.fold_plan()
+        assert shallow_c == shallow
+        if launched:  # shallow stages + exit head of the new chain, now
+            slot = work[1]
+            pos = hs.chain_pos(slot)
+            assert row == pos - deep_before - 1 and 0 <= row < width, (row, pos, deep_before)
+            row_pos[row] = pos
+            d = hs.prefix_digest(hs.n_prompt + pos - 1)
+            ex = lm.advance_digest(d, 0, shallow)
+            draft[slot] = sp.first_argmax(lm.exit_logits(lm.advance_digest(ex, shallow, n_layers), ex))
+        else:
+            assert row == -1
+        if nb > 0:  # deep batch over rows 0..nb-1 = positions fbase..fbase+nb-1
+            assert 1 <= nb <= width and fbase == deep_before + 1 and deep_done == fbase + nb - 1
+            for i in range(nb):
+                assert row_pos.get(i) == fbase + i, (i, row_pos.get(i), fbase)
+            base = fbase
+            final = []
+            for i in range(nb):
+                d = hs.prefix_digest(hs.n_prompt + fbase + i - 1)
+                final.append(sp.first_argmax(lm.logits(lm.advance_digest(d, 0, n_layers))))
+            batches.append(nb)
+        e = draft[exit_slot] if exit_slot >= 0 else -1
+        f = -1
+        if final_slot >= 0:
+            p = hs.chain_pos(final_slot)
+            assert base <= p < base + len(final), (p, base, len(final))
+            f = final[p - base]
+        hs.finish(e, f)
+    m = hs.metrics()
+    return hs.tokens(m[0]), m, hs.trace_rows(), batches
 
 
 def run_bernoulli(n_layers, exit_depth, alpha, horizon, verify_seed, *, exit_stage=0,

@@ -98,14 +98,21 @@ def tiny_models():
     return get
 
 
+@pytest.mark.parametrize("schedule", ["pipelined", "folded"])
 @pytest.mark.parametrize("case", load_golden("transformer.json"), ids=lambda c: c["name"])
-def test_tiny_transformer_matches_reference_scheduler(case, tiny_models):
+def test_tiny_transformer_matches_reference_scheduler(case, schedule, tiny_models):
     """The reference's decode_ppsd driving the fp64 CPU decoder produced these
-    tokens, accept/reject counts and trace; the GPU engine must match exactly."""
+    tokens, accept/reject counts and trace; the GPU engine must match exactly,
+    under both single-device schedules."""
     lm = tiny_models(case["seed"], case["deep_scale"], case["deep_from"])
     cfg = _cfg(case["cfg"])
-    toks, m, tr = ppsd.decode_ppsd(lm, cfg, case["prompt"], case["max_tokens"], "greedy",
-                                   ppsd.RngStream(0))
+    lm.schedule = schedule
+    try:
+        toks, m, tr = ppsd.decode_ppsd(lm, cfg, case["prompt"], case["max_tokens"], "greedy",
+                                       ppsd.RngStream(0))
+        assert ppsd.engine_for(lm, cfg).schedule("greedy") == schedule
+    finally:
+        lm.schedule = "auto"
     assert toks == case["tokens"]
     assert _metrics_list(m) == case["metrics"]
     assert tr.to_csv() == case["trace_csv"]
@@ -180,6 +187,32 @@ def test_ppsd_equals_ar_bit_exact(name):
         assert m.committed_tokens == 96 and m.accepts + m.rejects == 96
         rows = [r for r in tr if r.kind in ("FINAL_TOKEN", "CHECK_TOKEN")]
         assert [r.token for r in rows] == toks
+
+
+@pytest.mark.parametrize("name", ["l7b_2layer", "mid_gqa"])
+def test_folded_equals_pipelined(name):
+    """The folded single-device schedule (eager shallow stages, batched deep
+    verdicts) returns exactly the pipelined schedule's tokens, metrics and
+    trace — remainder stages, exit_stage > 1 and comm_latency included — and
+    does strictly less launch work."""
+    sh = dict(SHAPES[name])
+    sh["n_layers"] = 10
+    config = ppsd.TransformerConfig(**sh, kv_dtype="bf16", max_ctx=512)
+    lm = ppsd.TransformerLM(config, seed=5, deep_scale=0.35, deep_from=2)
+    prompt = [int(t) for t in np.random.default_rng(2).integers(0, config.vocab, size=21)]
+    for e, k, cl in ((2, 1, 0), (3, 1, 0), (4, 1, 1), (2, 2, 0), (3, 3, 0), (2, 1, 2)):
+        cfg = ppsd.PipelineConfig(10, e, exit_stage=k, comm_latency=cl)
+        out = {}
+        for sched in ("pipelined", "folded"):
+            lm.schedule = sched
+            toks, m, tr = ppsd.decode_ppsd(lm, cfg, prompt, 80, "greedy", ppsd.RngStream(0))
+            eng = ppsd.engine_for(lm, cfg)
+            assert eng.schedule("greedy") == sched
+            out[sched] = (toks, _metrics_list(m), tr.to_csv(), eng.last["gpu_launches"])
+        lm.schedule = "auto"
+        p, f = out["pipelined"], out["folded"]
+        assert f[:3] == p[:3], (e, k, cl)
+        assert f[3] < p[3], (e, k, cl, f[3], p[3])
 
 
 # ---------------------------------------------------------------- EESD -----

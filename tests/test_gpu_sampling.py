@@ -77,3 +77,24 @@ def test_transformer_sampling_force_reject_equals_ar():
     toks, m, _ = ppsd.decode_ppsd(lm, ppsd.PipelineConfig(6, 2), prompt, 40, "sampling", rng, force_reject=True)
     assert toks == ppsd.decode_autoregressive(lm, prompt, 40, "sampling", rng)
     assert m.accepts == 0
+
+
+def test_transformer_sampling_folded_equals_pipelined():
+    """Sampling mode under the folded schedule (exit_stage 1: the eager exit
+    logits are those of the draft tick; the batch's final logits are kept per
+    vector) draws exactly what the pipelined schedule draws; exit_stage > 1
+    sampling runs pipelined."""
+    config = ppsd.TransformerConfig(8, 256, 4, 4, 64, 704, 512, kv_dtype="bf16", max_ctx=256)
+    lm = ppsd.TransformerLM(config, seed=6, deep_scale=0.6, deep_from=2)
+    prompt = [9, 8, 7, 6, 5, 4]
+    cfg = ppsd.PipelineConfig(8, 2)
+    out = {}
+    for sched in ("pipelined", "folded"):
+        lm.schedule = sched
+        toks, m, tr = ppsd.decode_ppsd(lm, cfg, prompt, 60, "sampling", ppsd.RngStream(123))
+        assert ppsd.engine_for(lm, cfg).schedule("sampling") == sched
+        out[sched] = (toks, _ml(m), tr.to_csv())
+    lm.schedule = "auto"
+    assert out["folded"] == out["pipelined"]
+    assert 0 < out["folded"][1][2] < 60  # both verdict kinds occur
+    assert ppsd.engine_for(lm, ppsd.PipelineConfig(8, 2, exit_stage=2)).schedule("sampling") == "pipelined"
