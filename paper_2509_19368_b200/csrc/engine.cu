@@ -43,7 +43,7 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 struct GemvPlan {
-  int vpt = 0, tr = 0, m = 1, ns = 0, R = 0, K = 0;
+  int vpt = 0, tr = 0, m = 1, ns = 0, sub = 1, R = 0, K = 0;
   size_t smem = 0;
 };
 
@@ -156,6 +156,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   a.R = p.R;
   a.K = p.K;
   a.nstage = p.ns;
+  a.sub = p.sub;
   a.dm = e->dm;
   a.x = e->d_x;
   a.q = e->d_q;
@@ -298,7 +299,19 @@ static int build_fold_graph(ppsd_engine* e) {
   n_outer += 1;
   cudaGraphNode_t cnode = nullptr;
   cudaGraph_t body = nullptr;
-  if (ok) {
+  // PPSD_FOLD_COND=0 (profiling only: ncu does not profile graphs with
+  // conditional nodes): the deep part is captured inline and launched every
+  // tick; without a batch its kernels find no work and exit
+  const char* cv = getenv("PPSD_FOLD_COND");
+  if (ok && cv && atoi(cv) == 0) {
+    const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+    need(m >= 0, "deep layers");
+    need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
+         "final heads");
+    n_outer += m + 1;
+    e->h_ctx.cond = 0;
+    e->h_ctx.has_cond = 0;
+  } else if (ok) {
     cudaStreamCaptureStatus cs;
     const cudaGraphNode_t* deps = nullptr;
     size_t nd = 0;
@@ -318,9 +331,10 @@ static int build_fold_graph(ppsd_engine* e) {
       if (ok) need(cudaStreamUpdateCaptureDependencies(main_st, &cnode, 1, cudaStreamSetCaptureDependencies) ==
                        cudaSuccess, "capture deps");
       e->h_ctx.cond = h;
+      e->h_ctx.has_cond = 1;
     }
   }
-  if (ok) {  // body: deep layers of the batch (batched plans), final heads
+  if (ok && body) {  // body: deep layers of the batch (batched plans), final heads
     need(cudaStreamBeginCaptureToGraph(body_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
              cudaSuccess, "body capture");
     if (ok) {
@@ -593,7 +607,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         GemvPlan& p = b ? e->gpb[m] : e->gp[m];
         p.R = shapes[m][0];
         p.K = shapes[m][1];
-        if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.smem) != 0)
+        if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.sub, &p.smem) != 0)
           return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
                                              std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
         CU(gemv_set_attrs(p.vpt, p.m, m, p.smem));
@@ -1165,33 +1179,46 @@ extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t
 
 extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps, double* avg_ms,
                                double* bytes_per_launch) {
+  // n_groups > 0: the decode-tick plan (one vector per group, groups = the
+  // first n_groups local stages); n_groups < 0: the batched plan with
+  // -n_groups vectors in one group (folded deep batch / EESD verify).
+  // Consecutive launches walk the stage's layers so no launch re-reads
+  // weights the previous one left in L2.
   if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "probe needs a transformer engine");
-  if (which < 0 || which > kMatHead || reps < 1) return fail(PPSD_EINVAL, "bad probe arguments");
+  if (which < 0 || which > kMatHeadV || reps < 1) return fail(PPSD_EINVAL, "bad probe arguments");
   const int G = e->hi - e->lo + 1;
-  if (n_groups < 1 || n_groups > G || n_groups > e->cfg.nslot) return fail(PPSD_EINVAL, "bad n_groups");
+  const bool batched = n_groups < 0;
+  const int nv = batched ? -n_groups : 1;
+  const int ng = batched ? 1 : n_groups;
+  if (ng < 1 || ng > G || ng > e->cfg.nslot || nv > kMaxVec) return fail(PPSD_EINVAL, "bad n_groups");
+  if ((which == kMatHeadV) != batched && which >= kMatHead) return fail(PPSD_EINVAL, "head probe: kMatHead per tick, kMatHeadV batched");
   CU(cudaSetDevice(e->device));
   Work w{};
-  w.G = n_groups;
-  for (int g = 0; g < n_groups; ++g) {
-    w.nv[g] = 1;
+  w.G = ng;
+  int nl = 1 << 30;
+  for (int g = 0; g < ng; ++g) {
+    w.nv[g] = nv;
     w.slot[g] = g;
     w.pos[g] = 0;
     w.first[g] = e->cfg.stage_first[e->lo + g];
     w.nl[g] = e->cfg.stage_layers[e->lo + g];
+    nl = std::min(nl, (int)w.nl[g]);
   }
   w.head_slot[0] = 0;
-  w.head_slot[1] = n_groups > 1 ? 1 : 0;
+  w.head_slot[1] = ng > 1 ? 1 : -1;
   CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
-  for (int i = 0; i < 3; ++i) CU(enqueue_gemv(e, e->d_work_ar, 0, which));
+  const bool head = which >= kMatHead;
+  auto launch = [&](int i) { return enqueue_gemv(e, e->d_work_ar, head ? 0 : i % nl, which, batched); };
+  for (int i = 0; i < 3; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev0, e->st));
-  for (int i = 0; i < reps; ++i) CU(enqueue_gemv(e, e->d_work_ar, 0, which));
+  for (int i = 0; i < reps; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev1, e->st));
   CU(cudaEventSynchronize(e->ev1));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
-  const GemvPlan& p = e->gp[which];
+  const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
   *avg_ms = ms / reps;
-  *bytes_per_launch = (double)p.R * p.K * 2.0 * (which == kMatHead ? 1 : n_groups);
+  *bytes_per_launch = (double)p.R * p.K * 2.0 * (head ? 1 : ng);
   return PPSD_OK;
 }
 

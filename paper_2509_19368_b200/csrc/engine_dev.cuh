@@ -56,6 +56,7 @@ struct TickCtx {
   int32_t fold;
   Work* work_deep;
   unsigned long long cond;  // cudaGraphConditionalHandle of the folded tick graph
+  int32_t has_cond;         // 0: deep part captured inline (PPSD_FOLD_COND=0, profiling)
 };
 
 constexpr int kBoxHeader = 4;

@@ -4,10 +4,13 @@
 // exactly once and x a handful of fp32 vectors; the roofline is HBM bytes.
 // One persistent CTA per SM (grid = #SMs, ~200 KB smem):
 //
-//   warp 8 (producer, one lane): cp.async.bulk (UBLKCP) of TR contiguous
-//       weight rows (48-96 KB per copy — measured: the per-SM bulk-copy
-//       engine needs few, large copies in flight) into an NS-deep smem ring,
-//       completion counted on per-stage mbarriers (expect_tx), L2 evict_first.
+//   warp 8 (producer, one lane): cp.async.bulk (UBLKCP) of up to SUB
+//       tiles of TR contiguous weight rows (48-96 KB per copy — measured: the
+//       per-SM bulk-copy engine needs few, large copies in flight; a stage
+//       never spans two problems) into an NS-deep smem ring, completion
+//       counted on per-stage mbarriers (expect_tx), L2 evict_first. TR is
+//       what the consumers' registers allow (fewer rows when M vectors'
+//       input slices live there too); SUB restores the copy size.
 //   warps 0-7 (consumers, 256 threads): thread t owns the 16-byte column
 //       vectors t, t+256, ... of every row; its slice of the normalised input
 //       vector lives in registers for the whole kernel. Per stage it issues
@@ -49,6 +52,16 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
 
 constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
+// d = a * b + c on both lanes (fma.rn.f32x2, sm_100: FFMA2)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mov.b64 rc, {%6, %7};\n fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // Reduce N per-lane values across the warp. Afterwards lane L holds the
 // warp total of value index L >> (5 - log2 N). Fixed shuffle tree: the
 // result is deterministic.
@@ -83,6 +96,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
   constexpr bool kHeadV = EPI == kMatHeadV;  // final head on the vectors of group 0
   constexpr bool kHead = kHead2 || kHeadV;
+  // M = 1 and the tick head: all loads of a tile first, release the stage,
+  // then the math (the ring refills during it). Batched plans: weights are
+  // loaded as the FMAs need them, so no register copy of the tile bounds TR,
+  // and the stage is released after its last tile (SUB >= 2 keeps the ring
+  // deep enough).
+  constexpr bool kLoadsFirst = M == 1 || kHead2;
   constexpr int NV = M * TR;                 // row partials per thread per stage
   constexpr int CHT = (128 / TR) < 1 ? 1 : (128 / TR);  // tiles per deferred epilogue
   constexpr int kMaxProb = 128;
@@ -94,8 +113,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   __shared__ int s_bi[8][M];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = a.K, R = a.R, NS = a.nstage;
-  const int stage_bytes = TR * K * 2;
+  const int K = a.K, R = a.R, NS = a.nstage, SUB = a.sub;
+  const int tile_bytes = TR * K * 2;
+  const int stage_bytes = SUB * tile_bytes;
   unsigned char* ring = smem;
   float* red = reinterpret_cast<float*>(smem + (size_t)NS * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(red + CHT * 8 * NV);
@@ -153,10 +173,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       const uint64_t pol = policy_evict_first();
       int cur_p = -1;
       const unsigned char* wb = nullptr;
-      for (int n = 0; n < ntiles; ++n) {
+      for (int n = 0, j = 0; n < ntiles; ++j) {
         const long long t = t0 + n;
         const int p = (int)(t / tpp);
         const int tile = (int)(t - (long long)p * tpp);
+        const int cnt = min(SUB, min(ntiles - n, tpp - tile));  // stage = tiles of one problem
         if (p != cur_p) {
           const __nv_bfloat16* w;
           if (kHead) {
@@ -168,11 +189,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           wb = reinterpret_cast<const unsigned char*>(w);
           cur_p = p;
         }
-        const int st = n % NS;
-        if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
-        mbar_expect_tx(&full[st], stage_bytes);
-        bulk_g2s(ring + (size_t)st * stage_bytes, wb + (size_t)tile * stage_bytes, stage_bytes,
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(&empty[st], ((j / NS) & 1) ^ 1);
+        mbar_expect_tx(&full[st], cnt * tile_bytes);
+        bulk_g2s(ring + (size_t)st * stage_bytes, wb + (size_t)tile * tile_bytes, cnt * tile_bytes,
                  &full[st], pol);
+        n += cnt;
       }
     }
     return;
@@ -194,14 +216,19 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
   int cur_v0 = 0;
   int chunk_n0 = 0;  // first tile of the current (not yet flushed) epilogue chunk
+  int sj = -1, s_off = 0, s_cnt = 0;  // ring stage, tile within it, its tile count
 
   if (ntiles > 0) {
     const int nvec = K >> 3;
-    float xr[M][VPT][8];
+    // input slices: vectors (m, m+1) share a float2 so the FMAs of a vector
+    // pair issue as one FFMA2 (fma.rn.f32x2: two independent fma.rn.f32,
+    // bit-identical to the scalar sequence)
+    float2 xr2[(M + 1) / 2][VPT][8];
+#define XR(m, u, e) (((m) & 1) ? xr2[(m) >> 1][u][e].y : xr2[(m) >> 1][u][e].x)
     int cur_p = -1;
+    int p = (int)(t0 / tpp);                 // problem of the current tile
+    int tip = (int)(t0 - (long long)p * tpp);  // tile index inside it
     for (int n = 0; n < ntiles; ++n) {
-      const long long t = t0 + n;
-      const int p = (int)(t / tpp);
       if (p != cur_p) {  // load + normalise this problem's input vectors
         cur_p = p;
         const float* nw[M];
@@ -245,14 +272,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
             if (src[m] && v < nvec) {
               const float4 lo = *reinterpret_cast<const float4*>(src[m] + v * 8);
               const float4 hi = *reinterpret_cast<const float4*>(src[m] + v * 8 + 4);
-              xr[m][u][0] = lo.x; xr[m][u][1] = lo.y; xr[m][u][2] = lo.z; xr[m][u][3] = lo.w;
-              xr[m][u][4] = hi.x; xr[m][u][5] = hi.y; xr[m][u][6] = hi.z; xr[m][u][7] = hi.w;
+              XR(m, u, 0) = lo.x; XR(m, u, 1) = lo.y; XR(m, u, 2) = lo.z; XR(m, u, 3) = lo.w;
+              XR(m, u, 4) = hi.x; XR(m, u, 5) = hi.y; XR(m, u, 6) = hi.z; XR(m, u, 7) = hi.w;
             } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) xr[m][u][e] = 0.f;
+              for (int e = 0; e < 8; ++e) XR(m, u, e) = 0.f;
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) ss = fmaf(xr[m][u][e], xr[m][u][e], ss);
+            for (int e = 0; e < 8; ++e) ss = fmaf(XR(m, u, e), XR(m, u, e), ss);
           }
           ss = warp_sum(ss);
           if (lane == 0) s_ss[warp][m] = ss;
@@ -273,42 +300,113 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
               const float4 w1 = *reinterpret_cast<const float4*>(nw[m] + v * 8 + 4);
               const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-              for (int e = 0; e < 8; ++e) xr[m][u][e] = (xr[m][u][e] * rstd) * wv[e];
+              for (int e = 0; e < 8; ++e) XR(m, u, e) = (XR(m, u, e) * rstd) * wv[e];
             }
           }
         }
         named_bar_sync(1, kGemvConsumers);
       }
 
-      // ---- stage: all shared loads first, release the slot, then math ----
-      const int st = n % NS;
-      mbar_wait(&full[st], (n / NS) & 1);
-      const unsigned char* tb = ring + (size_t)st * stage_bytes;
-      uint4 wv[TR][VPT];
+      // ---- tile: all shared loads first, release the stage after its last
+      // tile's loads, then math ----
+      if (s_off == s_cnt) {  // next ring stage (same partition rule as the producer)
+        ++sj;
+        s_off = 0;
+        s_cnt = min(SUB, min(ntiles - n, tpp - tip));
+        mbar_wait(&full[sj % NS], (sj / NS) & 1);
+      }
+      const int st = sj % NS;
+      const unsigned char* tb = ring + (size_t)st * stage_bytes + (size_t)s_off * tile_bytes;
+      auto wload = [&](int r, int u) {
+        const int v = tid + u * kGemvConsumers;
+        return v < nvec ? lds128(tb + (size_t)r * K * 2 + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+      };
+      uint4 wv[kLoadsFirst ? TR : 1][VPT];
+      if constexpr (kLoadsFirst) {
 #pragma unroll
-      for (int r = 0; r < TR; ++r)
+        for (int r = 0; r < TR; ++r)
 #pragma unroll
-        for (int u = 0; u < VPT; ++u) {
-          const int v = tid + u * kGemvConsumers;
-          wv[r][u] = v < nvec ? lds128(tb + (size_t)r * K * 2 + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
-        }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+          for (int u = 0; u < VPT; ++u) wv[r][u] = wload(r, u);
+        __syncwarp();
+        if (++s_off == s_cnt && lane == 0) mbar_arrive(&empty[st]);
+      }
+      // Every accumulator sums its (u, e) products in the same order in all
+      // three forms below, so the row results do not depend on M or TR.
       float acc[NV];
+      if constexpr (M >= 2 && !kHead2) {  // vector pairs: one FFMA2 per weight and pair
+        float2 ap[M / 2][TR];
 #pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+        for (int mp = 0; mp < M / 2; ++mp)
 #pragma unroll
-      for (int r = 0; r < TR; ++r) {
+          for (int r = 0; r < TR; ++r) ap[mp][r] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < VPT; ++u) {
-          const uint4 w = wv[r][u];
-          const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
-                               bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+        for (int r = 0; r < TR; ++r) {
 #pragma unroll
-          for (int m = 0; m < M; ++m) {
-            if (!mact[m]) continue;
+          for (int u = 0; u < VPT; ++u) {
+            const uint4 w = kLoadsFirst ? wv[kLoadsFirst ? r : 0][u] : wload(r, u);
+            const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                                 bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[m * TR + r] = fmaf(wf[e], xr[m][u][e], acc[m * TR + r]);
+            for (int mp = 0; mp < M / 2; ++mp) {
+              if (!mact[2 * mp] && !mact[2 * mp + 1]) continue;  // kHead2: either may be idle
+#pragma unroll
+              for (int e = 0; e < 8; ++e) ap[mp][r] = ffma2(make_float2(wf[e], wf[e]), xr2[mp][u][e], ap[mp][r]);
+            }
+          }
+        }
+        if constexpr (!kLoadsFirst) {
+          __syncwarp();
+          if (++s_off == s_cnt && lane == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int mp = 0; mp < M / 2; ++mp)
+#pragma unroll
+          for (int r = 0; r < TR; ++r) {
+            acc[(2 * mp) * TR + r] = ap[mp][r].x;
+            acc[(2 * mp + 1) * TR + r] = ap[mp][r].y;
+          }
+      } else if constexpr (M == 1 && TR % 2 == 0) {  // one vector: row pairs share an FFMA2
+        float2 ap[TR / 2];
+#pragma unroll
+        for (int rp = 0; rp < TR / 2; ++rp) ap[rp] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int rp = 0; rp < TR / 2; ++rp) {
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            const uint4 w0 = wv[2 * rp][u], w1 = wv[2 * rp + 1][u];
+            const float2 wf[8] = {
+                make_float2(bf16lo(w0.x), bf16lo(w1.x)), make_float2(bf16hi(w0.x), bf16hi(w1.x)),
+                make_float2(bf16lo(w0.y), bf16lo(w1.y)), make_float2(bf16hi(w0.y), bf16hi(w1.y)),
+                make_float2(bf16lo(w0.z), bf16lo(w1.z)), make_float2(bf16hi(w0.z), bf16hi(w1.z)),
+                make_float2(bf16lo(w0.w), bf16lo(w1.w)), make_float2(bf16hi(w0.w), bf16hi(w1.w))};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float xv = xr2[0][u][e].x;
+              ap[rp] = ffma2(wf[e], make_float2(xv, xv), ap[rp]);
+            }
+          }
+        }
+#pragma unroll
+        for (int rp = 0; rp < TR / 2; ++rp) {
+          acc[2 * rp] = ap[rp].x;
+          acc[2 * rp + 1] = ap[rp].y;
+        }
+      } else {  // scalar: TR = 1 rows, and the tick head (either vector may be idle)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+#pragma unroll
+          for (int u = 0; u < VPT; ++u) {
+            const uint4 w = wv[kLoadsFirst ? r : 0][u];
+            const float wf[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                                 bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (!mact[m]) continue;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[m * TR + r] = fmaf(wf[e], XR(m, u, e), acc[m * TR + r]);
+            }
           }
         }
       }
@@ -319,7 +417,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 
       // deferred epilogue over CHT tiles (or at a problem boundary: the
       // per-vector state above belongs to the current problem)
-      const bool last_of_problem = (n == ntiles - 1) || ((t0 + n + 1) / tpp != p);
+      const bool last_of_problem = (n == ntiles - 1) || (tip + 1 == tpp);
       if (ct == CHT - 1 || last_of_problem) {
         named_bar_sync(1, kGemvConsumers);
         const int n0 = chunk_n0;
@@ -407,7 +505,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         }
         named_bar_sync(1, kGemvConsumers);
       }
+      if (++tip == tpp) {
+        tip = 0;
+        ++p;
+      }
     }
+#undef XR
   }
 
   if (kHead) {  // deterministic first-index argmax across the CTAs of each problem
@@ -485,20 +588,25 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 namespace {
 constexpr int kVpts[] = {1, 2, 3, 4, 6, 7, 8, 14};
 constexpr size_t kRingBudget = 212 * 1024;
+constexpr size_t kMinCopy = 64 * 1024;  // bulk-copy bytes per stage to aim for
 
 // rows per stage: ~64-96 KB bulk copies at M=1 (tools/stream_bench.cu);
 // fewer rows when M vectors' input slices must also live in registers
-constexpr int tr_for(int vpt, int m) {
+// M >= 2 loads weights as the FMAs need them (gemv_kernel), so its rows per
+// tile are bounded by the accumulators + input slices only.
+constexpr int tr_for(int vpt, int m, int epi = -1) {
   if (m == 1) return vpt == 1 ? 16 : vpt <= 3 ? 8 : vpt <= 6 ? 4 : vpt <= 8 ? 2 : 1;
-  if (m == 2) return vpt <= 2 ? 8 : vpt <= 4 ? 4 : 1;
-  return vpt == 1 ? 8 : vpt == 2 ? 4 : 2;  // m == 4
+  if (m == 2 && epi == kMatHead) return vpt <= 2 ? 8 : 4;  // loads-first (kLoadsFirst)
+  if (m == 2) return vpt <= 4 ? 4 : vpt <= 8 ? 2 : 1;
+  if (epi == kMatHeadV) return vpt <= 2 ? 4 : 2;  // + the argmax state
+  return vpt <= 2 ? 8 : vpt <= 4 ? 4 : 2;  // m == 4
 }
 // vectors per weight pass of the batched (prefill / EESD) plans
 constexpr int m_batched(int vpt) { return vpt <= 4 ? 4 : vpt <= 8 ? 2 : 1; }
 
 template <int VPT, int M, int EPI>
 cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only) {
-  constexpr int TR = tr_for(VPT, M);
+  constexpr int TR = tr_for(VPT, M, EPI);
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return launch_pdl(fn, dim3(grid), dim3(kGemvThreads), smem, st, a);
@@ -551,7 +659,8 @@ cudaError_t dispatch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, c
 }  // namespace
 
 // Choose the (VPT, TR, M, NS) instantiation for a [R][K] matrix; 0 on success.
-int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, size_t* smem) {
+int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, int* sub,
+              size_t* smem) {
   if (K % 8 != 0 || K <= 0 || R <= 0) return -1;
   const int need = (K + 8 * kGemvConsumers - 1) / (8 * kGemvConsumers);
   int v = -1;
@@ -560,12 +669,17 @@ int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int
   if (v < 0) return -1;
   const int mm = mat == kMatHead ? 2 : mat == kMatHeadV ? 4 : batched ? m_batched(v) : 1;
   if ((mat == kMatHead || mat == kMatHeadV) && v > 4) return -1;
-  const int t = tr_for(v, mm);
+  const int t = tr_for(v, mm, mat);
   if (R % t != 0) return -1;
   if ((mat == kMatQKV || mat == kMatGU) && t < 2) return -1;
   const int cht = 128 / t < 1 ? 1 : 128 / t;
-  const size_t stage = (size_t)t * K * 2;
+  const size_t tile = (size_t)t * K * 2;
   const size_t red = (size_t)cht * 8 * mm * t * 4;
+  // copies of >= 64 KB per stage, keeping >= 2 stages (3 when they fit)
+  int sb = (int)((kMinCopy + tile - 1) / tile);
+  if (sb < 1) sb = 1;
+  while (sb > 1 && (kRingBudget - red) / (sb * tile) < 3 && (kRingBudget - red) / ((sb - 1) * tile) >= 3) --sb;
+  const size_t stage = (size_t)sb * tile;
   int ns = (int)((kRingBudget - red) / stage);
   if (ns > 6) ns = 6;
   if (ns < 2) return -1;
@@ -573,6 +687,7 @@ int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int
   *tr = t;
   *m = mm;
   *nstage = ns;
+  *sub = sb;
   *smem = stage * ns + red + 2 * ns * sizeof(uint64_t);
   return 0;
 }

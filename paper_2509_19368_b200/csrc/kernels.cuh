@@ -58,6 +58,7 @@ struct GemvArgs {
   const float* head_norm0;  // exit norm
   const float* head_norm1;  // final norm
   int32_t R, K, nstage;
+  int32_t sub;            // tiles (TR rows each) per bulk-copy stage
   Dims dm;
   float* x;   // [nslot][d]   residual stream (fp32)
   float* q;   // [nslot][H*hd]
@@ -132,7 +133,8 @@ cudaError_t launch_pdl(Kern fn, dim3 grid, dim3 block, size_t smem, cudaStream_t
 // A GEMV plan: `m` = vectors per weight pass (1 for the decode tick; up to 4
 // for batched prefill / EESD verify, where a group of nv vectors takes
 // ceil(nv/m) passes).
-int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, size_t* smem);
+int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, int* sub,
+              size_t* smem);
 cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st);
 cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);

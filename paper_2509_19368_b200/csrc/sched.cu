@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       wd->nl[0] = s.c.n_layers - s.c.shallow_layers;
       wd->nv[0] = s.fold_nb > 0 ? s.fold_nb : 1;
       wd->head_slot[0] = wd->head_slot[1] = -1;
-      if (s.fold_nb > 0) cudaGraphSetConditional(c.cond, 1u);
+      if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
       s_launch_slot = row;
       s_launch_pos = row >= 0 ? s.ch_pos[s.work[1]] : 0;
     } else {
