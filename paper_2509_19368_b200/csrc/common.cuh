@@ -85,6 +85,14 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "r"(smem_u32(p)));
   return v;
 }
+// 32-bit shared-window address form (no generic->shared conversion per load)
+__device__ __forceinline__ uint4 lds128s(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
 // programmatic dependent launch (griddepcontrol) — no-ops without the attribute
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {

@@ -52,6 +52,16 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
 
 constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
+// d = a * b on both lanes (mul.rn.f32x2, sm_100: FMUL2)
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 // d = a * b + c on both lanes (fma.rn.f32x2, sm_100: FFMA2)
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
@@ -91,8 +101,17 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
   return s;
 }
 
+// Consumer warps per CTA. A matrix must use the same NW (and so the same
+// per-row reduction tree) in every plan. Measured: 16 warps at K <= 8192
+// (VPT 1-2) did not beat 8 warps with twice the columns per thread (the
+// batched plans got slower: fewer rows per tile fit in 120 registers), so
+// every plan uses 8.
+constexpr int nw_for(int vpt) { return vpt > 0 ? 8 : 8; }
+
 template <int VPT, int TR, int M, int EPI>
-__global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__((nw_for(VPT) + 1) * 32, 1) gemv_kernel(const GemvArgs a) {
+  constexpr int NW = nw_for(VPT);  // consumer warps
+  constexpr int NC = NW * 32;      // consumer threads
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
   constexpr bool kHeadV = EPI == kMatHeadV;  // final head on the vectors of group 0
   constexpr bool kHead = kHead2 || kHeadV;
@@ -102,15 +121,19 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   // and the stage is released after its last tile (SUB >= 2 keeps the ring
   // deep enough).
   constexpr bool kLoadsFirst = M == 1 || kHead2;
+  // batched plans pair vectors (m, m+1) in FFMA2s; their partials are kept
+  // pair-adjacent: value index of (vector m, row r) in acc / red
+  constexpr bool kPairs = M >= 2 && !kHead2;
+  auto vidx = [](int m, int r) { return kPairs ? ((m >> 1) * TR + r) * 2 + (m & 1) : m * TR + r; };
   constexpr int NV = M * TR;                 // row partials per thread per stage
-  constexpr int CHT = (128 / TR) < 1 ? 1 : (128 / TR);  // tiles per deferred epilogue
+  constexpr int CHT = ((NW == 16 ? 64 : 128) / TR) < 1 ? 1 : ((NW == 16 ? 64 : 128) / TR);  // tiles per epilogue
   constexpr int kMaxProb = 128;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int s_pg[kMaxProb], s_pv[kMaxProb];  // problem = (group, first vector)
   __shared__ int s_np;
-  __shared__ float s_ss[8][M];
-  __shared__ float s_bv[8][M];
-  __shared__ int s_bi[8][M];
+  __shared__ float s_ss[NW][M];
+  __shared__ float s_bv[NW][M];
+  __shared__ int s_bi[NW][M];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = a.K, R = a.R, NS = a.nstage, SUB = a.sub;
@@ -118,7 +141,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   const int stage_bytes = SUB * tile_bytes;
   unsigned char* ring = smem;
   float* red = reinterpret_cast<float*>(smem + (size_t)NS * stage_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + CHT * 8 * NV);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + CHT * NW * NV);
   uint64_t* empty = full + NS;
   const Work* work = a.work;
 
@@ -138,7 +161,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
     s_np = np;
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 8);
+      mbar_init(&empty[i], NW);
     }
     fence_mbar_init();
   }
@@ -168,7 +191,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
   }
   const int ntiles = (int)(t1 - t0);
 
-  if (warp == 8) {  // ---------------- producer ----------------
+  if (warp == NW) {  // ---------------- producer ----------------
     if (lane == 0 && ntiles > 0) {
       const uint64_t pol = policy_evict_first();
       int cur_p = -1;
@@ -220,6 +243,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 
   if (ntiles > 0) {
     const int nvec = K >> 3;
+    // shared-memory addressing, fixed per thread: column vector tid + u*256
+    const uint32_t ring_s = smem_u32(ring);
+    const int K2 = K * 2;
+    uint32_t colb[VPT];
+    bool cvalid[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      colb[u] = (uint32_t)(tid + u * NC) * 16u;
+      cvalid[u] = tid + u * NC < nvec;
+    }
     // input slices: vectors (m, m+1) share a float2 so the FMAs of a vector
     // pair issue as one FFMA2 (fma.rn.f32x2: two independent fma.rn.f32,
     // bit-identical to the scalar sequence)
@@ -268,7 +301,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           float ss = 0.f;
 #pragma unroll
           for (int u = 0; u < VPT; ++u) {
-            const int v = tid + u * kGemvConsumers;
+            const int v = tid + u * NC;
             if (src[m] && v < nvec) {
               const float4 lo = *reinterpret_cast<const float4*>(src[m] + v * 8);
               const float4 hi = *reinterpret_cast<const float4*>(src[m] + v * 8 + 4);
@@ -284,17 +317,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           ss = warp_sum(ss);
           if (lane == 0) s_ss[warp][m] = ss;
         }
-        named_bar_sync(1, kGemvConsumers);
+        named_bar_sync(1, NC);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
           if (!nw[m]) continue;
           float tot = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) tot += s_ss[w][m];
+          for (int w = 0; w < NW; ++w) tot += s_ss[w][m];
           const float rstd = 1.0f / sqrtf(tot / (float)K + a.dm.eps);
 #pragma unroll
           for (int u = 0; u < VPT; ++u) {
-            const int v = tid + u * kGemvConsumers;
+            const int v = tid + u * NC;
             if (v < nvec) {
               const float4 w0 = *reinterpret_cast<const float4*>(nw[m] + v * 8);
               const float4 w1 = *reinterpret_cast<const float4*>(nw[m] + v * 8 + 4);
@@ -304,7 +337,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
             }
           }
         }
-        named_bar_sync(1, kGemvConsumers);
+        named_bar_sync(1, NC);
       }
 
       // ---- tile: all shared loads first, release the stage after its last
@@ -316,10 +349,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         mbar_wait(&full[sj % NS], (sj / NS) & 1);
       }
       const int st = sj % NS;
-      const unsigned char* tb = ring + (size_t)st * stage_bytes + (size_t)s_off * tile_bytes;
+      const uint32_t tb_s = ring_s + (uint32_t)(st * stage_bytes + s_off * tile_bytes);
       auto wload = [&](int r, int u) {
-        const int v = tid + u * kGemvConsumers;
-        return v < nvec ? lds128(tb + (size_t)r * K * 2 + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+        return cvalid[u] ? lds128s(tb_s + (uint32_t)(r * K2) + colb[u]) : make_uint4(0, 0, 0, 0);
       };
       uint4 wv[kLoadsFirst ? TR : 1][VPT];
       if constexpr (kLoadsFirst) {
@@ -330,15 +362,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         __syncwarp();
         if (++s_off == s_cnt && lane == 0) mbar_arrive(&empty[st]);
       }
-      // Every accumulator sums its (u, e) products in the same order in all
-      // three forms below, so the row results do not depend on M or TR.
+      // Every accumulator starts with the product of its first (u, e) term
+      // and adds the rest in (u, e) order in all three forms below, so row
+      // results do not depend on M, TR or the form.
       float acc[NV];
-      if constexpr (M >= 2 && !kHead2) {  // vector pairs: one FFMA2 per weight and pair
+      if constexpr (kPairs) {  // vector pairs: one FFMA2 per weight and pair
         float2 ap[M / 2][TR];
-#pragma unroll
-        for (int mp = 0; mp < M / 2; ++mp)
-#pragma unroll
-          for (int r = 0; r < TR; ++r) ap[mp][r] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < TR; ++r) {
 #pragma unroll
@@ -348,9 +377,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
                                  bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
 #pragma unroll
             for (int mp = 0; mp < M / 2; ++mp) {
-              if (!mact[2 * mp] && !mact[2 * mp + 1]) continue;  // kHead2: either may be idle
+              if (!mact[2 * mp]) {  // batched plans: active vectors are a prefix
+                if (u == 0) ap[mp][r] = make_float2(0.f, 0.f);
+                continue;
+              }
 #pragma unroll
-              for (int e = 0; e < 8; ++e) ap[mp][r] = ffma2(make_float2(wf[e], wf[e]), xr2[mp][u][e], ap[mp][r]);
+              for (int e = 0; e < 8; ++e)
+                ap[mp][r] = (u == 0 && e == 0) ? fmul2(make_float2(wf[e], wf[e]), xr2[mp][u][e])
+                                               : ffma2(make_float2(wf[e], wf[e]), xr2[mp][u][e], ap[mp][r]);
             }
           }
         }
@@ -362,13 +396,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         for (int mp = 0; mp < M / 2; ++mp)
 #pragma unroll
           for (int r = 0; r < TR; ++r) {
-            acc[(2 * mp) * TR + r] = ap[mp][r].x;
-            acc[(2 * mp + 1) * TR + r] = ap[mp][r].y;
+            acc[vidx(2 * mp, r)] = ap[mp][r].x;
+            acc[vidx(2 * mp + 1, r)] = ap[mp][r].y;
           }
       } else if constexpr (M == 1 && TR % 2 == 0) {  // one vector: row pairs share an FFMA2
         float2 ap[TR / 2];
-#pragma unroll
-        for (int rp = 0; rp < TR / 2; ++rp) ap[rp] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int rp = 0; rp < TR / 2; ++rp) {
 #pragma unroll
@@ -382,7 +414,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const float xv = xr2[0][u][e].x;
-              ap[rp] = ffma2(wf[e], make_float2(xv, xv), ap[rp]);
+              ap[rp] = (u == 0 && e == 0) ? fmul2(wf[e], make_float2(xv, xv))
+                                          : ffma2(wf[e], make_float2(xv, xv), ap[rp]);
             }
           }
         }
@@ -393,8 +426,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         }
       } else {  // scalar: TR = 1 rows, and the tick head (either vector may be idle)
 #pragma unroll
-        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-#pragma unroll
         for (int r = 0; r < TR; ++r) {
 #pragma unroll
           for (int u = 0; u < VPT; ++u) {
@@ -403,9 +434,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
                                  bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-              if (!mact[m]) continue;
+              if (!mact[m]) {
+                if (u == 0) acc[m * TR + r] = 0.f;
+                continue;
+              }
 #pragma unroll
-              for (int e = 0; e < 8; ++e) acc[m * TR + r] = fmaf(wf[e], XR(m, u, e), acc[m * TR + r]);
+              for (int e = 0; e < 8; ++e)
+                acc[m * TR + r] = (u == 0 && e == 0) ? __fmul_rn(wf[e], XR(m, u, e))
+                                                     : fmaf(wf[e], XR(m, u, e), acc[m * TR + r]);
             }
           }
         }
@@ -413,13 +449,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       const int ct = n - chunk_n0;
       const float s = transpose_reduce<NV>(acc, lane);
       constexpr int kShift = 5 - ilog2(NV);
-      if ((lane & ((1 << kShift) - 1)) == 0) red[(ct * 8 + warp) * NV + (lane >> kShift)] = s;
+      if ((lane & ((1 << kShift) - 1)) == 0) red[(ct * NW + warp) * NV + (lane >> kShift)] = s;
 
       // deferred epilogue over CHT tiles (or at a problem boundary: the
       // per-vector state above belongs to the current problem)
       const bool last_of_problem = (n == ntiles - 1) || (tip + 1 == tpp);
       if (ct == CHT - 1 || last_of_problem) {
-        named_bar_sync(1, kGemvConsumers);
+        named_bar_sync(1, NC);
         const int n0 = chunk_n0;
         chunk_n0 = n + 1;
         const int nrows = (ct + 1) * TR;
@@ -427,11 +463,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
           const int tt = rl / TR, r = rl % TR;
           float s = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) s += red[(tt * 8 + w) * NV + m * TR + r];
+          for (int w = 0; w < NW; ++w) s += red[(tt * NW + w) * NV + vidx(m, r)];
           return s;
         };
         if (EPI == kMatQKV || EPI == kMatGU) {
-          for (int pr = tid; pr < nrows / 2; pr += kGemvConsumers) {
+          for (int pr = tid; pr < nrows / 2; pr += NC) {
             const int rl = pr * 2;
             const long long tg = t0 + n0 + rl / TR;
             const int rr = (int)(tg - (long long)p * tpp) * TR + rl % TR;
@@ -483,7 +519,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
             }
           }
         } else {
-          for (int rl = tid; rl < nrows; rl += kGemvConsumers) {
+          for (int rl = tid; rl < nrows; rl += NC) {
             const long long tg = t0 + n0 + rl / TR;
             const int rr = (int)(tg - (long long)p * tpp) * TR + rl % TR;
 #pragma unroll
@@ -503,7 +539,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
             }
           }
         }
-        named_bar_sync(1, kGemvConsumers);
+        named_bar_sync(1, NC);
       }
       if (++tip == tpp) {
         tip = 0;
@@ -526,7 +562,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       }
       if (lane == 0) { s_bv[warp][m] = v; s_bi[warp][m] = i; }
     }
-    named_bar_sync(1, kGemvConsumers);
+    named_bar_sync(1, NC);
     // kHead2: one problem over the whole grid; kHeadV: this CTA's problem span
     const int v0 = kHeadV ? s_pv[hv_p] : 0;
     const int c0 = kHeadV ? hv_c0 : 0, c1 = kHeadV ? hv_c1 : (int)gridDim.x;
@@ -536,7 +572,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       for (int m = 0; m < M; ++m) {
         float v = s_bv[0][m];
         int i = s_bi[0][m];
-        for (int w = 1; w < 8; ++w)
+        for (int w = 1; w < NW; ++w)
           if (better(s_bv[w][m], s_bi[w][m], v, i)) { v = s_bv[w][m]; i = s_bi[w][m]; }
         a.head_part[((size_t)blockIdx.x * kMaxVec + v0 + m) * 2 + 0] = v;
         a.head_part[((size_t)blockIdx.x * kMaxVec + v0 + m) * 2 + 1] = __int_as_float(i);
@@ -544,14 +580,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
       __threadfence();
       s_last = atomicAdd(ticket, 1) == c1 - c0 - 1;
     }
-    named_bar_sync(1, kGemvConsumers);
+    named_bar_sync(1, NC);
     if (s_last) {  // the last CTA merges the per-CTA partials, all loads in parallel
       __threadfence();
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         float v = -FLT_MAX;
         int i = INT_MAX;
-        for (int b = c0 + tid; b < c1; b += kGemvConsumers) {
+        for (int b = c0 + tid; b < c1; b += NC) {
           const float bv = __ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 0]);
           const int bi = __float_as_int(__ldcg(&a.head_part[((size_t)b * kMaxVec + v0 + m) * 2 + 1]));
           if (better(bv, bi, v, i)) { v = bv; i = bi; }
@@ -564,14 +600,14 @@ __global__ void __launch_bounds__(kGemvThreads, 1) gemv_kernel(const GemvArgs a)
         }
         if (lane == 0) { s_bv[warp][m] = v; s_bi[warp][m] = i; }
       }
-      named_bar_sync(1, kGemvConsumers);
+      named_bar_sync(1, NC);
       if (tid == 0) {
         Work* wk = const_cast<Work*>(work);
         const int nv0 = kHeadV ? work->nv[0] : 0;
         for (int m = 0; m < M; ++m) {
           float v = s_bv[0][m];
           int i = s_bi[0][m];
-          for (int w = 1; w < 8; ++w)
+          for (int w = 1; w < NW; ++w)
             if (better(s_bv[w][m], s_bi[w][m], v, i)) { v = s_bv[w][m]; i = s_bi[w][m]; }
           if (kHead2) wk->head_out[m] = work->head_slot[m] >= 0 ? i : -1;
           else if (v0 + m < nv0) wk->vec_out[v0 + m] = i;
@@ -609,7 +645,7 @@ cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st
   constexpr int TR = tr_for(VPT, M, EPI);
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(fn, dim3(grid), dim3(kGemvThreads), smem, st, a);
+  return launch_pdl(fn, dim3(grid), dim3((nw_for(VPT) + 1) * 32), smem, st, a);
 }
 
 template <int VPT, int M>
@@ -662,8 +698,8 @@ cudaError_t dispatch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, c
 int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, int* sub,
               size_t* smem) {
   if (K % 8 != 0 || K <= 0 || R <= 0) return -1;
-  const int need = (K + 8 * kGemvConsumers - 1) / (8 * kGemvConsumers);
   int v = -1;
+  const int need = (K + 8 * 256 - 1) / (8 * 256);  // 8 consumer warps
   for (int c : kVpts)
     if (c >= need) { v = c; break; }
   if (v < 0) return -1;
@@ -672,9 +708,10 @@ int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int
   const int t = tr_for(v, mm, mat);
   if (R % t != 0) return -1;
   if ((mat == kMatQKV || mat == kMatGU) && t < 2) return -1;
-  const int cht = 128 / t < 1 ? 1 : 128 / t;
+  const int nw = nw_for(v), rows_chunk = nw == 16 ? 64 : 128;
+  const int cht = rows_chunk / t < 1 ? 1 : rows_chunk / t;
   const size_t tile = (size_t)t * K * 2;
-  const size_t red = (size_t)cht * 8 * mm * t * 4;
+  const size_t red = (size_t)cht * nw * mm * t * 4;
   // copies of >= 64 KB per stage, keeping >= 2 stages (3 when they fit)
   int sb = (int)((kMinCopy + tile - 1) / tile);
   if (sb < 1) sb = 1;
