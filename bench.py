@@ -223,17 +223,32 @@ def run_ours(args):
     assert ar == toks0, "PPSD must equal AR token-for-token"
     ar_tps = NEW_TOKENS / (np.median(ar_ms) / 1e3)
 
-    # roofline of the dominant kernel: the gate/up GEMV launch as the tick runs it
-    # (one launch covers the same layer slot of all 4 stages), CUDA events
+    # Roofline of the dominant kernel, timed live with CUDA events on the
+    # engine stream (ppsd_probe_gemv: back-to-back launches that walk the
+    # stage's layers, so no launch finds its weights in L2). Folded schedule:
+    # the gate/up GEMV of a shallow tick (one vector, 180 MB per launch; the
+    # largest share of the step in the launch list, profiles/); pipelined: the
+    # grouped gate/up launch over all 4 stages. `kernels` lists every layer
+    # GEMV as each schedule launches it (tick plan, and the folded deep batch
+    # of 4 vectors in one weight pass).
     hbm, peak_kind = peaks()
     reps = 50
-    gu_ms, gu_bytes = eng.probe_gemv(2, cfg.n_stages, reps)
+    folded = last0["schedule"] == "folded"
+    gu_ms, gu_bytes = eng.probe_gemv(2, 1 if folded else cfg.n_stages, reps)
     achieved = gu_bytes / (gu_ms / 1e3) / 1e9
+    kern = {}
+    for wi, name in enumerate(("qkv", "o", "gate_up", "down")):
+        for lab, g in (("tick", 1), ("tick_x4_stages", cfg.n_stages), ("batch4", -4)):
+            ms_, b_ = eng.probe_gemv(wi, g, 20)
+            kern[f"{name}_{lab}"] = {"us": round(ms_ * 1e3, 2), "GB/s": round(b_ / (ms_ / 1e3) / 1e9, 1)}
+    for lab, (wi, g) in (("head_tick", (4, 1)), ("head_batch4", (5, -4))):
+        ms_, b_ = eng.probe_gemv(wi, g, 20)
+        kern[lab] = {"us": round(ms_ * 1e3, 2), "GB/s": round(b_ / (ms_ / 1e3) / 1e9, 1)}
     step_bytes, breakdown = algorithmic_bytes(tr0, config, cfg, PROMPT_LEN, last0)
     step_gbs = step_bytes / (np.median(dec_ms) / 1e3) / 1e9
     alpha = m0.alpha_all_measured
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "gemv_gateup_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "gemv_gateup_m1_traffic.json" if folded else "gemv_gateup_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("bytes_per_launch")
@@ -259,8 +274,11 @@ def run_ours(args):
                 "note": "public decode_ppsd call incl. prefill of the 128-token prompt"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": "gemv_kernel<6,2,1,kMatGU> (gate/up, 4 stages x 180 MB per launch)",
-                     "peak_kind": peak_kind, "avg_ms": round(gu_ms, 4)},
+                     "kernel": ("gemv_kernel<2,8,1,kMatGU> (gate/up + SwiGLU, one vector, 180 MB per launch)"
+                                if folded else
+                                "gemv_kernel<2,8,1,kMatGU> (gate/up, 4 stages x 180 MB per launch)"),
+                     "algorithmic_bytes": gu_bytes, "peak_kind": peak_kind, "avg_ms": round(gu_ms, 4)},
+        "kernels": kern,
         "step_roofline": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / hbm, 4),
                           "bytes_per_step": step_bytes, **breakdown},
         "clocks": clk.summary(),
