@@ -108,7 +108,8 @@ typedef struct {
  *   FOLDED:    shallow stages + exit head at launch, deep stages of all
  *              in-flight chains in one batched weight pass when a verdict
  *              needs them (greedy, or sampling with exit_stage 1);
- *   AUTO:      FOLDED where it applies, else PIPELINED. */
+ *   AUTO:      FOLDED where it applies and the batched GEMVs fit their
+ *              registers (d_model <= 4096), else PIPELINED. */
 #define PPSD_SCHEDULE_AUTO 0
 #define PPSD_SCHEDULE_PIPELINED 1
 #define PPSD_SCHEDULE_FOLDED 2

@@ -38,14 +38,22 @@ def main():
         lm = ppsd.TransformerLM(config, seed=0, deep_scale=args.deep_scale, deep_from=E)
         cfg = ppsd.PipelineConfig(config.n_layers, E)
         eng = ppsd.engine_for(lm, cfg)
+        eng.set_schedule("pipelined")
         eng.decode(prompt, 64)  # warm-up (graphs, caches)
-        toks, m, _ = eng.decode(prompt, args.tokens)
+        tp, mp, trp = eng.decode(prompt, args.tokens)
+        pipe_ms = eng.last["decode_ms"]
+        eng.set_schedule("auto")
+        eng.decode(prompt, 64)
+        toks, m, tr = eng.decode(prompt, args.tokens)
         ppsd_ms = eng.last["decode_ms"]
+        sched = eng.last["schedule"]
+        assert tp == toks and mp == m and trp.to_csv() == tr.to_csv(), "schedules must agree"
         ar = eng.decode_ar(prompt, args.tokens)
         ar_ms = eng.last["decode_ms"]
         assert ar == toks, "PPSD must equal AR"
         row = dict(E=E, n_stages=cfg.n_stages, alpha_ppsd=m.alpha_all_measured, ticks=m.ticks,
-                   ppsd_tok_s=args.tokens / ppsd_ms * 1e3, ar_tok_s=args.tokens / ar_ms * 1e3,
+                   schedule=sched, ppsd_tok_s=args.tokens / ppsd_ms * 1e3,
+                   ppsd_pipelined_tok_s=args.tokens / pipe_ms * 1e3, ar_tok_s=args.tokens / ar_ms * 1e3,
                    ppsd_vs_ar=ar_ms / ppsd_ms, tick_speedup=m.speedup_vs_ar,
                    eq7=ppsd.ppsd_speedup(m.alpha_all_measured, config.n_layers, E))
         for g in [int(x) for x in args.gammas.split(",")]:

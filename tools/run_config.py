@@ -39,12 +39,19 @@ def main():
     ps = rng.split("prompt")
     prompt = [ps.randbelow(config.vocab) for _ in range(args.prompt)]
     eng = ppsd.engine_for(lm, cfg)
+    eng.set_schedule("pipelined")
     eng.decode(prompt, 32)  # warm-up
+    tp, mp, trp = eng.decode(prompt, args.tokens)
+    pipe = dict(eng.last)
+    eng.set_schedule("auto")
+    eng.decode(prompt, 32)
     toks, m, tr = eng.decode(prompt, args.tokens)
     pp = dict(eng.last)
+    assert tp == toks and mp == m and trp.to_csv() == tr.to_csv(), "schedules must agree"
     ar = eng.decode_ar(prompt, args.tokens)
     ar_ms = eng.last["decode_ms"]
     assert ar == toks, "PPSD must equal AR"
+    tr = trp  # the pipelined schedule's byte accounting (folded: see bench.py)
     fwd = sum(1 for r in tr if r.kind in ("ACTIVATION", "FINAL_TOKEN", "CHECK_TOKEN"))
     heads = len({r.tick for r in tr if r.kind in ("DRAFT_TOKEN", "FINAL_TOKEN", "CHECK_TOKEN")})
     kvb = config.kv_bytes_per_token_layer()
@@ -56,11 +63,13 @@ def main():
     row = dict(model=config.name, weights_gb=round((config.n_layers * config.layer_bytes() + 2 * config.head_bytes()) / 1e9, 2),
                exit=args.exit, n_stages=cfg.n_stages, deep_scale=args.deep_scale, init_s=round(init_s, 1),
                alpha=m.alpha_all_measured, ticks=m.ticks, stage_forwards=fwd,
-               ppsd_tok_s=round(args.tokens / pp["decode_ms"] * 1e3, 2),
+               schedule=pp["schedule"], ppsd_tok_s=round(args.tokens / pp["decode_ms"] * 1e3, 2),
+               ppsd_pipelined_tok_s=round(args.tokens / pipe["decode_ms"] * 1e3, 2),
+               deep_batches=pp["deep_batches"], deep_vectors=pp["deep_vectors"],
                ar_tok_s=round(args.tokens / ar_ms * 1e3, 2),
                ppsd_vs_ar=round(ar_ms / pp["decode_ms"], 4), tick_speedup=round(m.speedup_vs_ar, 4),
                eq7=round(ppsd.ppsd_speedup(m.alpha_all_measured, config.n_layers, args.exit), 4),
-               step_gbs=round(step_bytes / (pp["decode_ms"] / 1e3) / 1e9, 1),
+               pipelined_step_gbs=round(step_bytes / (pipe["decode_ms"] / 1e3) / 1e9, 1),
                prefill_ms=round(pp["prefill_ms"], 1))
     if args.gamma:
         et, em, _ = eng.decode_eesd(prompt, args.tokens, args.gamma)
