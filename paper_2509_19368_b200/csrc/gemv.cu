@@ -108,8 +108,19 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
 // every plan uses 8.
 constexpr int nw_for(int vpt) { return vpt > 0 ? 8 : 8; }
 
+// Register boost for the batched plans of wide-K matrices (the down
+// projection, VPT >= 5): their M=4 input slices need ~230 registers per
+// thread, but 9 warps cap every thread at 168 (allocation granularity is 4
+// warps). Those instantiations run a 4-warp producer warpgroup that hands its
+// registers to the consumers (setmaxnreg). Measured: the boost made the
+// K = 4096 batched plans slower, so only wide-K plans use it.
+template <int VPT, int M>
+constexpr bool reg_boost() { return VPT >= 5 && M >= 4; }
+template <int VPT, int M>
+constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M>() ? 4 : 1)) * 32; }
+
 template <int VPT, int TR, int M, int EPI>
-__global__ void __launch_bounds__((nw_for(VPT) + 1) * 32, 1) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const GemvArgs a) {
   constexpr int NW = nw_for(VPT);  // consumer warps
   constexpr int NC = NW * 32;      // consumer threads
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
@@ -191,8 +202,9 @@ __global__ void __launch_bounds__((nw_for(VPT) + 1) * 32, 1) gemv_kernel(const G
   }
   const int ntiles = (int)(t1 - t0);
 
-  if (warp == NW) {  // ---------------- producer ----------------
-    if (lane == 0 && ntiles > 0) {
+  if (warp >= NW) {  // ---------------- producer ----------------
+    if constexpr (reg_boost<VPT, M>()) setmaxnreg_dec<40>();
+    if (warp == NW && lane == 0 && ntiles > 0) {
       const uint64_t pol = policy_evict_first();
       int cur_p = -1;
       const unsigned char* wb = nullptr;
@@ -224,6 +236,7 @@ __global__ void __launch_bounds__((nw_for(VPT) + 1) * 32, 1) gemv_kernel(const G
   }
 
   // ---------------- consumers ----------------
+  if constexpr (reg_boost<VPT, M>()) setmaxnreg_inc<232>();
   pdl_wait();     // activations of the previous kernel are visible from here on
   pdl_trigger();  // ...so the next kernel may start streaming its weights
   float bestv[M];
@@ -635,17 +648,18 @@ constexpr int tr_for(int vpt, int m, int epi = -1) {
   if (m == 2 && epi == kMatHead) return vpt <= 2 ? 8 : 4;  // loads-first (kLoadsFirst)
   if (m == 2) return vpt <= 4 ? 4 : vpt <= 8 ? 2 : 1;
   if (epi == kMatHeadV) return vpt <= 2 ? 4 : 2;  // + the argmax state
-  return vpt <= 2 ? 8 : vpt <= 4 ? 4 : 2;  // m == 4
+  if (vpt >= 5) return 2;  // m == 4, register boost
+  return vpt <= 2 ? 8 : 4;  // m == 4
 }
 // vectors per weight pass of the batched (prefill / EESD) plans
-constexpr int m_batched(int vpt) { return vpt <= 4 ? 4 : vpt <= 8 ? 2 : 1; }
+constexpr int m_batched(int vpt) { return vpt <= 6 ? 4 : vpt <= 8 ? 2 : 1; }
 
 template <int VPT, int M, int EPI>
 cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st, bool attrs_only) {
   constexpr int TR = tr_for(VPT, M, EPI);
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(fn, dim3(grid), dim3((nw_for(VPT) + 1) * 32), smem, st, a);
+  return launch_pdl(fn, dim3(grid), dim3(gemv_threads<VPT, M>()), smem, st, a);
 }
 
 template <int VPT, int M>
