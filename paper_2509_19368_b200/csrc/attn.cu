@@ -1,208 +1,24 @@
-// attn.cu — split-K decode attention over the paged KV cache.
-//
-// Work item = (stage group, kv head, KV page). A KV page is kPage=64
-// positions of one kv head stored contiguously ([page][kvh][64][hd]); an item
-// pulls its K block and V block into shared memory with two 1-D bulk copies
-// (UBLKCP, one mbarrier) — one DRAM round trip per item instead of a chain of
-// dependent loads — then scores every q head that shares the kv head (GQA)
-// against the block, takes a chunk-local softmax and accumulates V from smem.
-// Page boundaries are absolute positions, so the partial results, and the
-// ordered merge done by the last CTA to finish a (chain, kv head), depend
-// only on the context length — never on how many pipeline stages share the
-// launch: PPSD and AR attention are bit-identical.
-#include <float.h>
-
-#include "kernels.cuh"
+// attn.cu — standalone split-K decode attention kernel: one 128-thread
+// worker (attn_core.cuh) per CTA. The O-projection GEMV runs the same worker
+// code fused (gemv.cu) where the grid may synchronise (engine.cu).
+#include "attn_core.cuh"
 
 namespace ppsd {
 
-template <typename T>
-__device__ __forceinline__ void unpack16(const uint4& v, float* out);
-template <>
-__device__ __forceinline__ void unpack16<float>(const uint4& v, float* out) {
-  out[0] = __uint_as_float(v.x); out[1] = __uint_as_float(v.y);
-  out[2] = __uint_as_float(v.z); out[3] = __uint_as_float(v.w);
-}
-template <>
-__device__ __forceinline__ void unpack16<__nv_bfloat16>(const uint4& v, float* out) {
-  out[0] = bf16lo(v.x); out[1] = bf16hi(v.x); out[2] = bf16lo(v.y); out[3] = bf16hi(v.y);
-  out[4] = bf16lo(v.z); out[5] = bf16hi(v.z); out[6] = bf16lo(v.w); out[7] = bf16hi(v.w);
-}
-__device__ __forceinline__ float tof(float v) { return v; }
-__device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
-
-constexpr int kAttnThreads = 128;
-
 template <int HD, typename KVT, int QPK>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
-  constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte vector
-  constexpr int LPT = HD / EPV;                // lanes per token
-  constexpr int TPW = 32 / LPT;                // tokens per warp pass
-  constexpr int BLK = kPage * HD;              // elements per K (or V) page block
-  static_assert(LPT >= 1 && LPT <= 32 && (32 % LPT) == 0, "head_dim / dtype combination");
   extern __shared__ __align__(128) unsigned char smem[];
-  KVT* ks = reinterpret_cast<KVT*>(smem);
-  KVT* vs = ks + BLK;
-  __shared__ float qs[QPK][HD];
-  __shared__ float sc[QPK][kPage];
-  __shared__ float s_m[QPK], s_l[QPK];
-  __shared__ int s_last;
-  __shared__ __align__(8) uint64_t bar;
-  constexpr int kMergePages = 32;  // contexts up to 2048 positions merge from smem
-  __shared__ float s_pm[QPK][kMergePages], s_pl[QPK][kMergePages];
-
-  const Work* w = a.work;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int H = a.dm.H, KVh = a.dm.KV;
-  const float scale = 1.0f / sqrtf((float)HD);
-  if (tid == 0) {
-    mbar_init(&bar, 1);
+  __shared__ AttnScratch<HD, QPK> S;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar, 1);
     fence_mbar_init();
   }
   pdl_wait();  // q / KV rows come from the preceding QKV kernel
   pdl_trigger();
   __syncthreads();
-
   uint32_t phase = 0;
-  for (int item = blockIdx.x;; item += gridDim.x) {
-    // items: (group, vector, kv head, page); vector v of group g sits at
-    // slot[g]+v and position pos[g]+v (batched prefill / EESD verify)
-    int g = -1, vv = 0, rem = item, nch = 0;
-    for (int gg = 0; gg < w->G && g < 0; ++gg) {
-      if (w->slot[gg] < 0 || a.layer_i >= w->nl[gg]) continue;
-      for (int v = 0; v < w->nv[gg]; ++v) {
-        nch = (w->pos[gg] + v + kPage) / kPage;  // ceil((pos+1)/kPage)
-        if (rem < nch * KVh) { g = gg; vv = v; break; }
-        rem -= nch * KVh;
-      }
-    }
-    if (g < 0) break;
-    const int kvh = rem / nch, c = rem - kvh * nch;
-    const int slot = w->slot[g] + vv, ctx = w->pos[g] + vv + 1;
-    const int n = min(kPage, ctx - c * kPage);
-    const LayerW& L = a.layers[w->first[g] + a.layer_i];
-    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
-      mbar_expect_tx(&bar, 2 * bytes);
-      bulk_g2s(ks, reinterpret_cast<const KVT*>(L.kc) + blk, bytes, &bar);
-      bulk_g2s(vs, reinterpret_cast<const KVT*>(L.vc) + blk, bytes, &bar);
-    }
-    const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
-    for (int i = tid; i < QPK * HD; i += kAttnThreads) qs[i / HD][i % HD] = qsrc[i];
-    __syncthreads();
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-
-    // scores: LPT lanes per token, one 16-byte K vector per lane
-    const int li = lane % LPT, tw = lane / LPT;
-    for (int base = warp * TPW; base < n; base += 4 * TPW) {
-      const int tt = base + tw;
-      float part[QPK];
-#pragma unroll
-      for (int i = 0; i < QPK; ++i) part[i] = 0.f;
-      if (tt < n) {
-        float kf[EPV];
-        unpack16<KVT>(lds128(ks + (size_t)tt * HD + li * EPV), kf);
-#pragma unroll
-        for (int i = 0; i < QPK; ++i)
-#pragma unroll
-          for (int e = 0; e < EPV; ++e) part[i] = fmaf(kf[e], qs[i][li * EPV + e], part[i]);
-      }
-#pragma unroll
-      for (int off = LPT / 2; off > 0; off >>= 1)
-#pragma unroll
-        for (int i = 0; i < QPK; ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], off);
-      if (li == 0 && tt < n)
-#pragma unroll
-        for (int i = 0; i < QPK; ++i) sc[i][tt] = part[i] * scale;
-    }
-    __syncthreads();
-
-    for (int i = warp; i < QPK; i += 4) {  // chunk-local softmax statistics
-      float mx = -FLT_MAX;
-      for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, sc[i][tt]);
-      mx = warp_max(mx);
-      float l = 0.f;
-      for (int tt = lane; tt < n; tt += 32) {
-        const float p = expf(sc[i][tt] - mx);
-        sc[i][tt] = p;
-        l += p;
-      }
-      l = warp_sum(l);
-      if (lane == 0) { s_m[i] = mx; s_l[i] = l; }
-    }
-    __syncthreads();
-
-    float* pbase = a.part + (((size_t)slot * H + (size_t)kvh * QPK) * a.max_pages) * (HD + 2);
-    for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-      const int i = idx / HD, d = idx - i * HD;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int tt = 0; tt < n; ++tt) acc = fmaf(sc[i][tt], tof(vs[(size_t)tt * HD + d]), acc);
-      pbase[((size_t)i * a.max_pages + c) * (HD + 2) + d] = acc;
-    }
-    if (tid < QPK) {
-      pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD] = s_m[tid];
-      pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD + 1] = s_l[tid];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(&a.cnt[slot * KVh + kvh], 1) == nch - 1;
-    }
-    __syncthreads();
-    if (s_last) {  // ordered merge of the page partials (page statistics staged in smem)
-      __threadfence();
-      if (nch <= kMergePages) {
-        for (int idx = tid; idx < QPK * nch; idx += kAttnThreads) {
-          const int i = idx / nch, cc = idx - i * nch;
-          const float* pb = pbase + ((size_t)i * a.max_pages + cc) * (HD + 2);
-          s_pm[i][cc] = __ldcg(pb + HD);
-          s_pl[i][cc] = __ldcg(pb + HD + 1);
-        }
-        __syncthreads();
-        for (int i = warp; i < QPK; i += 4) {
-          float M = -FLT_MAX;
-          for (int cc = lane; cc < nch; cc += 32) M = fmaxf(M, s_pm[i][cc]);
-          M = warp_max(M);
-          float Ls = 0.f;
-          for (int cc = lane; cc < nch; cc += 32) {
-            const float e = expf(s_pm[i][cc] - M);
-            s_pm[i][cc] = e;  // page weight
-            Ls = fmaf(s_pl[i][cc], e, Ls);
-          }
-          Ls = warp_sum(Ls);
-          if (lane == 0) s_l[i] = Ls;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-          const int i = idx / HD, d = idx - i * HD;
-          const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2) + d;
-          float O = 0.f;
-#pragma unroll 4
-          for (int cc = 0; cc < nch; ++cc) O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2)), s_pm[i][cc], O);
-          a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / s_l[i];
-        }
-      } else {
-        for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-          const int i = idx / HD, d = idx - i * HD;
-          const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2);
-          float M = -FLT_MAX;
-          for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(pb + (size_t)cc * (HD + 2) + HD));
-          float Ls = 0.f, O = 0.f;
-          for (int cc = 0; cc < nch; ++cc) {
-            const float e = expf(__ldcg(pb + (size_t)cc * (HD + 2) + HD) - M);
-            Ls = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + HD + 1), e, Ls);
-            O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2) + d), e, O);
-          }
-          a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / Ls;
-        }
-      }
-      if (tid == 0) a.cnt[slot * KVh + kvh] = 0;
-    }
-    __syncthreads();
-  }
+  attn_items<HD, KVT, QPK>(a, blockIdx.x, gridDim.x, threadIdx.x, reinterpret_cast<KVT*>(smem), S, phase,
+                           [] { __syncthreads(); });
 }
 
 namespace {

@@ -173,6 +173,9 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
 }
 
 static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
+  // PPSD_PROFILE_SKIP_ATTN=1: timing experiments only (wrong results)
+  static const bool skip = getenv("PPSD_PROFILE_SKIP_ATTN") && atoi(getenv("PPSD_PROFILE_SKIP_ATTN")) != 0;
+  if (skip) return cudaSuccess;
   AttnArgs a{};
   a.work = w;
   a.layer_i = layer_i;
