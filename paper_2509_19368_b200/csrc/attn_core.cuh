@@ -41,6 +41,9 @@ __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(
 constexpr int kAttnThreads = 128;  // one attention worker
 constexpr int kMergePages = 32;    // contexts up to 2048 positions merge from smem
 
+constexpr int kStageG = 32;      // groups staged in shared memory (more: read from global)
+constexpr int kStagePages = 64;  // page-table entries staged
+
 // per-worker shared scratch (besides the K/V page blocks)
 template <int HD, int QPK>
 struct AttnScratch {
@@ -50,6 +53,11 @@ struct AttnScratch {
   float s_pm[QPK][kMergePages], s_pl[QPK][kMergePages];
   int s_last;
   uint64_t bar;
+  // the work descriptor and page table, staged once per worker in one round
+  // trip (the item walk would otherwise chain dependent global loads)
+  int st_G;
+  int st_slot[kStageG], st_pos[kStageG], st_first[kStageG], st_nl[kStageG], st_nv[kStageG];
+  int st_page[kStagePages];
 };
 
 template <int HD, typename KVT>
@@ -75,29 +83,54 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
   const int H = a.dm.H, KVh = a.dm.KV;
   const float scale = 1.0f / sqrtf((float)HD);
 
+  // stage the descriptor + page table: independent loads, one round trip
+  if (tid < kStageG) {
+    S.st_slot[tid] = w->slot[tid];
+    S.st_pos[tid] = w->pos[tid];
+    S.st_first[tid] = w->first[tid];
+    S.st_nl[tid] = w->nl[tid];
+    S.st_nv[tid] = w->nv[tid];
+  }
+  if (tid == 0) S.st_G = w->G;
+  for (int i = tid; i < min(a.max_pages, kStagePages); i += kAttnThreads) S.st_page[i] = a.page_table[i];
+  sync();
+  const int G = S.st_G;
+  const bool staged = G <= kStageG;
+  auto wslot = [&](int g) { return staged ? S.st_slot[g] : w->slot[g]; };
+  auto wpos = [&](int g) { return staged ? S.st_pos[g] : w->pos[g]; };
+  auto wfirst = [&](int g) { return staged ? S.st_first[g] : w->first[g]; };
+  auto wnl = [&](int g) { return staged ? S.st_nl[g] : w->nl[g]; };
+  auto wnv = [&](int g) { return staged ? S.st_nv[g] : w->nv[g]; };
+
   for (int item = worker;; item += nworkers) {
     // items: (group, vector, kv head, page); vector v of group g sits at
     // slot[g]+v and position pos[g]+v (batched prefill / EESD / folded verify)
     int g = -1, vv = 0, rem = item, nch = 0;
-    for (int gg = 0; gg < w->G && g < 0; ++gg) {
-      if (w->slot[gg] < 0 || a.layer_i >= w->nl[gg]) continue;
-      for (int v = 0; v < w->nv[gg]; ++v) {
-        nch = (w->pos[gg] + v + kPage) / kPage;  // ceil((pos+1)/kPage)
+    for (int gg = 0; gg < G && g < 0; ++gg) {
+      if (wslot(gg) < 0 || a.layer_i >= wnl(gg)) continue;
+      const int nvg = wnv(gg), pg = wpos(gg);
+      for (int v = 0; v < nvg; ++v) {
+        nch = (pg + v + kPage) / kPage;  // ceil((pos+1)/kPage)
         if (rem < nch * KVh) { g = gg; vv = v; break; }
         rem -= nch * KVh;
       }
     }
     if (g < 0) break;
     const int kvh = rem / nch, c = rem - kvh * nch;
-    const int slot = w->slot[g] + vv, ctx = w->pos[g] + vv + 1;
+    const int slot = wslot(g) + vv, ctx = wpos(g) + vv + 1;
     const int n = min(kPage, ctx - c * kPage);
-    const LayerW& L = a.layers[w->first[g] + a.layer_i];
-    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;
+    // this layer's K / V caches: [k, v] per local layer, contiguous (engine.cu)
+    const int lloc = wfirst(g) + a.layer_i - a.first_local;
+    const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
+    const KVT* kc = reinterpret_cast<const KVT*>(kvl);
+    const KVT* vc = reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes);
+    const int page = c < kStagePages ? S.st_page[c] : a.page_table[c];
+    const size_t blk = ((size_t)page * KVh + kvh) * BLK;
     if (tid == 0) {
       const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
       mbar_expect_tx(&S.bar, 2 * bytes);
-      bulk_g2s(ks, reinterpret_cast<const KVT*>(L.kc) + blk, bytes, &S.bar);
-      bulk_g2s(vs, reinterpret_cast<const KVT*>(L.vc) + blk, bytes, &S.bar);
+      bulk_g2s(ks, kc + blk, bytes, &S.bar);
+      bulk_g2s(vs, vc + blk, bytes, &S.bar);
     }
     const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
     for (int i = tid; i < QPK * HD; i += kAttnThreads) S.qs[i / HD][i % HD] = qsrc[i];

@@ -187,6 +187,9 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   a.cnt = e->d_attn_cnt;
   a.page_table = e->d_page_table;
   a.max_pages = e->max_pages;
+  a.kv_base = e->d_kv;
+  a.kv_layer_bytes = (long long)e->max_pages * kPage * e->dm.KV * e->dm.hd * (e->dm.kv_bf16 ? 2 : 4);
+  a.first_local = e->first_local_layer;
   return attn_launch(a, attn_grid(e), e->st);
 }
 

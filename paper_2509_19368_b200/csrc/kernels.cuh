@@ -83,6 +83,10 @@ struct AttnArgs {
   int32_t* cnt;      // [nslot][KV]
   const int32_t* page_table;
   int32_t max_pages;
+  // KV pool: [local layer][k | v][pages][KV][kPage][hd], layer stride 2 * kv_layer_bytes
+  const void* kv_base;
+  long long kv_layer_bytes;
+  int32_t first_local;  // global index of the first local layer
 };
 
 // tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
