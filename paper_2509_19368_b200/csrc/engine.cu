@@ -547,7 +547,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   const int max_ctx = md->max_ctx > 0 ? md->max_ctx : 4096;
   e->md.max_ctx = max_ctx;
   const int nslot = e->cfg.nslot;
-  e->nbuf = std::max(nslot, (int)kMaxVec);
+  e->nbuf = std::max(nslot, std::max((int)kMaxVec, umma_n()));  // + a tcgen05 prefill chunk
 
   CU(dalloc(&e->d_sched, sizeof(Sched)));
   CU(dalloc(&e->d_work, sizeof(Work)));
@@ -571,8 +571,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.n_layers = md->n_layers;
   c.vocab = md->vocab;
   c.model_stages = e->cfg.S;
-  c.prefill_chunk = kMaxVec;
-  if (const char* v = getenv("PPSD_PREFILL_CHUNK")) c.prefill_chunk = std::min(std::max(atoi(v), 1), (int)kMaxVec);
+  c.prefill_chunk = kMaxVec;  // transformer engines: set after setup_umma
 
   if (md->kind == PPSD_MODEL_TOYLM) {
     if (md->vocab < 2) return fail(PPSD_EINVAL, "vocab must be >= 2");
@@ -674,6 +673,13 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     c.x = e->d_x;
     int rc = setup_umma(e, shapes);
     if (rc) return rc;
+    // prompt tokens per prefill chunk: one tcgen05 weight pass (umma_n()), or
+    // the batched-GEMV chunk
+    {
+      const int cmax = e->umma ? umma_n() : (int)kMaxVec;
+      c.prefill_chunk = cmax;
+      if (const char* v = getenv("PPSD_PREFILL_CHUNK")) c.prefill_chunk = std::min(std::max(atoi(v), 1), cmax);
+    }
     // folded schedule: single-device engine, every in-flight chain fits one batch
     e->schedule = pd->schedule;
     e->fold_ok = e->lo == 1 && e->hi == e->S && sched_fold_width(&e->cfg) <= kMaxVec &&

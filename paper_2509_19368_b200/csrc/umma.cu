@@ -2,12 +2,12 @@
 // batched prompt prefill on sm_100a.
 //
 // A prefill chunk multiplies every weight matrix W [R][K] (bf16, row-major)
-// by up to 16 token vectors. The bs=1 decode GEMV (gemv.cu) keeps each
+// by up to kUmN = 64 token vectors. The bs=1 decode GEMV (gemv.cu) keeps each
 // vector's input slice in registers, which caps it at 4 vectors per weight
 // pass; here the tokens are the N dimension of a UMMA and the weights are
 // streamed from HBM exactly once per chunk:
 //
-//   D[128 rows][16 tokens] (fp32, TMEM) += W_tile[128][K] . X[16][K]^T
+//   D[128 rows][64 tokens] (fp32, TMEM) += W_tile[128][K] . X[64][K]^T
 //
 // X is split into two bf16 halves (hi = bf16(x), lo = bf16(x - hi)) and both
 // are multiplied into the same accumulator, so the activations keep ~16
@@ -16,19 +16,19 @@
 //
 // One CTA per SM, 192 threads:
 //   warp 0 (one lane)   TMA producer: 2-D tensor copies with 128-byte swizzle
-//                       into a 5-deep ring of 40 KB stages (two 16 KB weight
-//                       boxes + four 2 KB activation boxes), mbarrier expect_tx.
+//                       into a 3-deep ring of 64 KB stages (two 16 KB weight
+//                       boxes + four 8 KB activation boxes), mbarrier expect_tx.
 //                       Weight boxes of the first stages are issued before
 //                       griddepcontrol.wait (weights never depend on the
 //                       previous kernel).
-//   warp 1              TMEM owner (alloc/dealloc, 32 columns = two 16-column
+//   warp 1              TMEM owner (alloc/dealloc, 128 columns = two 64-column
 //                       accumulators) and, on one lane, the MMA issuer:
-//                       tcgen05.mma.cta_group::1.kind::f16 M=128 N=16 K=16,
+//                       tcgen05.mma.cta_group::1.kind::f16 M=128 N=64 K=16,
 //                       smem descriptors in the canonical K-major SW128
 //                       layout, tcgen05.commit frees ring stages and
 //                       publishes finished accumulators.
-//   warps 2-5           epilogue: tcgen05.ld 32x32b.x16 (one TMEM lane = one
-//                       weight row per thread, 16 token columns), then the
+//   warps 2-5           epilogue: tcgen05.ld 32x32b.x16 x4 (one TMEM lane = one
+//                       weight row per thread, 64 token columns), then the
 //                       same fused epilogues as the decode GEMV (RoPE + KV
 //                       append, SwiGLU, residual add).
 //
@@ -48,9 +48,9 @@
 namespace ppsd {
 
 constexpr int kUmTileRows = 128;
-constexpr int kUmN = 16;
+constexpr int kUmN = 64;    // tokens per chunk (UMMA N); hi + lo halves = 2N operand rows
 constexpr int kUmKS = 128;  // K elements per ring stage
-constexpr int kUmStages = 5;
+constexpr int kUmStages = 3;
 constexpr int kUmABox = kUmTileRows * 64 * 2;  // 16 KB
 constexpr int kUmBBox = kUmN * 64 * 2;         // 2 KB
 constexpr int kUmStageBytes = 2 * kUmABox + 4 * kUmBBox;
@@ -101,16 +101,21 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// one accumulator row (this thread's weight row) x kUmN token columns
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&v)[kUmN]) {
+#pragma unroll
+  for (int c = 0; c < kUmN; c += 16) tmem_ld16_nowait(taddr + (uint32_t)c, v + c);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 // The CTA whose unit range [U*b/G, U*(b+1)/G) holds unit u.
@@ -123,13 +128,13 @@ __device__ __forceinline__ long long unit_start(int b, long long U, int G) { ret
 // fused epilogue on one weight row (`rr`, this thread) x nv token columns
 
 template <int EPI>
-__device__ __forceinline__ void um_epilogue_pairs(const UmmaArgs& a, int rr, const float (&y)[16], int lane) {
+__device__ __forceinline__ void um_epilogue_pairs(const UmmaArgs& a, int rr, const float (&y)[kUmN], int lane) {
   const Work* w = a.work;
   const int slot0 = w->slot[0], pos0 = w->pos[0], nv = w->nv[0];
   // row pairs (2i, 2i+1) sit on adjacent lanes
-  float yp[16];
+  float yp[kUmN];
 #pragma unroll
-  for (int n = 0; n < 16; ++n) yp[n] = __shfl_xor_sync(0xffffffffu, y[n], 1);
+  for (int n = 0; n < kUmN; ++n) yp[n] = __shfl_xor_sync(0xffffffffu, y[n], 1);
   if (lane & 1) return;
   if (EPI == kMatGU) {
     for (int n = 0; n < nv; ++n)
@@ -181,7 +186,7 @@ __device__ __forceinline__ void um_epilogue_pairs(const UmmaArgs& a, int rr, con
 // ---------------------------------------------------------------------------
 
 template <int EPI>
-__device__ __forceinline__ void um_epilogue(const UmmaArgs& a, int rr, const float (&y)[16], int lane) {
+__device__ __forceinline__ void um_epilogue(const UmmaArgs& a, int rr, const float (&y)[kUmN], int lane) {
   if constexpr (EPI == kMatO || EPI == kMatDown) {
     const Work* w = a.work;
     const int slot0 = w->slot[0], nv = w->nv[0];
@@ -230,8 +235,9 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
     }
     fence_mbar_init();
   }
-  if (warp == 1) {  // TMEM: 32 columns = two 16-column fp32 accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(s_taddr)));
+  if (warp == 1) {  // TMEM: 2 * kUmN columns = two kUmN-column fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_taddr)),
+                 "n"(2 * kUmN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -317,8 +323,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
       const int acc = seg & 1;
       mbar_wait(&acc_full[acc], (seg >> 1) & 1);
       tc_fence_after();
-      float y[16];
-      tmem_ld16(taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * kUmN), y);
+      float y[kUmN];
+      tmem_ld_row(taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(acc * kUmN), y);
       tc_fence_before();
       mbar_arrive(&acc_empty[acc]);
       const int rr = t * kUmTileRows + row;
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
       const int my_slot = (t == t_first) ? 0 : 1;
       float4* dst = reinterpret_cast<float4*>(a.ws + (((size_t)b * 2 + my_slot) * kUmTileRows + row) * kUmN);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dst[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+      for (int i = 0; i < kUmN / 4; ++i) dst[i] = make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
       __threadfence();
       named_bar_sync(1, 128);
       int ncontrib = 0;
@@ -340,9 +346,9 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
       named_bar_sync(1, 128);
       if (!s_last) continue;
       __threadfence();
-      float s[16];
+      float s[kUmN];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) s[i] = 0.f;
+      for (int i = 0; i < kUmN; ++i) s[i] = 0.f;
       for (int c = cf; c <= cl; ++c) {
         const long long cs = unit_start(c, U, G);
         if (unit_start(c + 1, U, G) == cs) continue;  // empty range
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
         const float4* src =
             reinterpret_cast<const float4*>(a.ws + (((size_t)c * 2 + slot) * kUmTileRows + row) * kUmN);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < kUmN / 4; ++i) {
           const float4 v = __ldcg(src + i);
           s[4 * i] += v.x;
           s[4 * i + 1] += v.y;
@@ -366,12 +372,12 @@ __global__ void __launch_bounds__(kUmThreads, 1) umma_gemm_kernel(const UmmaArgs
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(taddr));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(2 * kUmN));
   }
 }
 
 // Input staging: the chunk's vectors (RMS-normalised for QKV / GU) split into
-// bf16 hi/lo rows of the [32][K] activation operand. One CTA per token.
+// bf16 hi/lo rows of the [2 * kUmN][K] activation operand. One CTA per token.
 __global__ void __launch_bounds__(256) umma_prep_kernel(const UmmaArgs a) {
   pdl_wait();
   pdl_trigger();
