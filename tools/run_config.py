@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--gamma", type=int, default=0, help="also run EESD with this gamma")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--schedule", default="auto", choices=["auto", "pipelined", "folded"])
     args = ap.parse_args()
     config = {"7b": ppsd.TransformerConfig.llama2_7b, "13b": ppsd.TransformerConfig.llama2_13b,
               "70b": ppsd.TransformerConfig.llama2_70b}[args.model](max_ctx=args.prompt + args.tokens + 64)
@@ -43,7 +44,7 @@ def main():
     eng.decode(prompt, 32)  # warm-up
     tp, mp, trp = eng.decode(prompt, args.tokens)
     pipe = dict(eng.last)
-    eng.set_schedule("auto")
+    eng.set_schedule(args.schedule)
     eng.decode(prompt, 32)
     toks, m, tr = eng.decode(prompt, args.tokens)
     pp = dict(eng.last)
