@@ -13,12 +13,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
     mbar_init(&S.bar, 1);
     fence_mbar_init();
   }
-  pdl_wait();  // q / KV rows come from the preceding QKV kernel
-  pdl_trigger();
   __syncthreads();
   uint32_t phase = 0;
   attn_items<HD, KVT, QPK>(a, blockIdx.x, gridDim.x, threadIdx.x, reinterpret_cast<KVT*>(smem), S, phase,
-                           [] { __syncthreads(); });
+                           [] { __syncthreads(); },
+                           [] {  // q / this layer's KV rows come from the preceding QKV kernel
+                             pdl_wait();
+                             pdl_trigger();
+                           });
 }
 
 namespace {

@@ -69,9 +69,13 @@ constexpr size_t attn_kv_bytes() {
 // worker, worker + nworkers, ... `sync()` is a barrier over exactly these
 // 128 threads. The scratch mbarrier must have been initialised (count 1)
 // and fenced by the caller; `phase` carries its parity across calls.
-template <int HD, typename KVT, int QPK, class Sync>
+// `wait_inputs()` makes the producing kernel's q / K / V rows visible
+// (griddepcontrol.wait): the work descriptor (written by the scheduler >= 2
+// kernels earlier) is staged and the first item's K/V copy is issued before
+// it when that page holds no position this layer's QKV kernel writes.
+template <int HD, typename KVT, int QPK, class Sync, class Wait>
 __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid, KVT* ks,
-                           AttnScratch<HD, QPK>& S, uint32_t& phase, Sync sync) {
+                           AttnScratch<HD, QPK>& S, uint32_t& phase, Sync sync, Wait wait_inputs) {
   constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte vector
   constexpr int LPT = HD / EPV;                // lanes per token
   constexpr int TPW = 32 / LPT;                // tokens per warp pass
@@ -102,36 +106,56 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
   auto wnl = [&](int g) { return staged ? S.st_nl[g] : w->nl[g]; };
   auto wnv = [&](int g) { return staged ? S.st_nv[g] : w->nv[g]; };
 
-  for (int item = worker;; item += nworkers) {
-    // items: (group, vector, kv head, page); vector v of group g sits at
-    // slot[g]+v and position pos[g]+v (batched prefill / EESD / folded verify)
-    int g = -1, vv = 0, rem = item, nch = 0;
-    for (int gg = 0; gg < G && g < 0; ++gg) {
+  // items: (group, vector, kv head, page); vector v of group g sits at
+  // slot[g]+v and position pos[g]+v (batched prefill / EESD / folded verify)
+  struct Item {
+    int g, vv, kvh, c, nch;
+  };
+  auto decode = [&](int item, Item& it) -> bool {
+    int rem = item;
+    for (int gg = 0; gg < G; ++gg) {
       if (wslot(gg) < 0 || a.layer_i >= wnl(gg)) continue;
       const int nvg = wnv(gg), pg = wpos(gg);
       for (int v = 0; v < nvg; ++v) {
-        nch = (pg + v + kPage) / kPage;  // ceil((pos+1)/kPage)
-        if (rem < nch * KVh) { g = gg; vv = v; break; }
+        const int nch = (pg + v + kPage) / kPage;  // ceil((pos+1)/kPage)
+        if (rem < nch * KVh) {
+          it.g = gg;
+          it.vv = v;
+          it.nch = nch;
+          it.kvh = rem / nch;
+          it.c = rem - it.kvh * nch;
+          return true;
+        }
         rem -= nch * KVh;
       }
     }
-    if (g < 0) break;
-    const int kvh = rem / nch, c = rem - kvh * nch;
+    return false;
+  };
+  auto issue_copy = [&](const Item& it) {  // thread 0
+    const int ctx = wpos(it.g) + it.vv + 1;
+    const int n = min(kPage, ctx - it.c * kPage);
+    // this layer's K / V caches: [k, v] per local layer, contiguous (engine.cu)
+    const int lloc = wfirst(it.g) + a.layer_i - a.first_local;
+    const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
+    const int page = it.c < kStagePages ? S.st_page[it.c] : a.page_table[it.c];
+    const size_t blk = ((size_t)page * KVh + it.kvh) * BLK;
+    const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
+    mbar_expect_tx(&S.bar, 2 * bytes);
+    bulk_g2s(ks, reinterpret_cast<const KVT*>(kvl) + blk, bytes, &S.bar);
+    bulk_g2s(vs, reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes) + blk, bytes, &S.bar);
+  };
+  Item it;
+  bool have = decode(worker, it);
+  // a page entirely below the group's first written position is final
+  bool issued = have && (it.c + 1) * kPage <= wpos(it.g);
+  if (issued && tid == 0) issue_copy(it);
+  wait_inputs();
+
+  for (int item = worker; have; item += nworkers, have = decode(item, it), issued = false) {
+    const int g = it.g, vv = it.vv, kvh = it.kvh, c = it.c, nch = it.nch;
     const int slot = wslot(g) + vv, ctx = wpos(g) + vv + 1;
     const int n = min(kPage, ctx - c * kPage);
-    // this layer's K / V caches: [k, v] per local layer, contiguous (engine.cu)
-    const int lloc = wfirst(g) + a.layer_i - a.first_local;
-    const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
-    const KVT* kc = reinterpret_cast<const KVT*>(kvl);
-    const KVT* vc = reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes);
-    const int page = c < kStagePages ? S.st_page[c] : a.page_table[c];
-    const size_t blk = ((size_t)page * KVh + kvh) * BLK;
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
-      mbar_expect_tx(&S.bar, 2 * bytes);
-      bulk_g2s(ks, kc + blk, bytes, &S.bar);
-      bulk_g2s(vs, vc + blk, bytes, &S.bar);
-    }
+    if (!issued && tid == 0) issue_copy(it);
     const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
     for (int i = tid; i < QPK * HD; i += kAttnThreads) S.qs[i / HD][i % HD] = qsrc[i];
     sync();
@@ -199,6 +223,18 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
     if (S.s_last) {  // ordered merge of the page partials (page statistics staged in smem)
       __threadfence();
       if (nch <= kMergePages) {
+        // one (head, dim) per thread: its page partials are loaded before the
+        // page statistics are reduced (one L2 round trip for the merge)
+        constexpr bool kPre = QPK * HD <= kAttnThreads;
+        float pv[kPre ? kMergePages : 1];
+        if constexpr (kPre) {
+          if (tid < QPK * HD) {
+            const float* pb = pbase + (size_t)(tid / HD) * a.max_pages * (HD + 2) + (tid % HD);
+#pragma unroll
+            for (int cc = 0; cc < kMergePages; ++cc)
+              if (cc < nch) pv[cc] = __ldcg(pb + (size_t)cc * (HD + 2));
+          }
+        }
         for (int idx = tid; idx < QPK * nch; idx += kAttnThreads) {
           const int i = idx / nch, cc = idx - i * nch;
           const float* pb = pbase + ((size_t)i * a.max_pages + cc) * (HD + 2);
@@ -220,13 +256,24 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
           if (lane == 0) S.s_l[i] = Ls;
         }
         sync();
-        for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-          const int i = idx / HD, d = idx - i * HD;
-          const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2) + d;
-          float O = 0.f;
+        if constexpr (kPre) {
+          if (tid < QPK * HD) {
+            const int i = tid / HD, d = tid % HD;
+            float O = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < kMergePages; ++cc)
+              if (cc < nch) O = fmaf(pv[cc], S.s_pm[i][cc], O);
+            a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / S.s_l[i];
+          }
+        } else {
+          for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
+            const int i = idx / HD, d = idx - i * HD;
+            const float* pb = pbase + (size_t)i * a.max_pages * (HD + 2) + d;
+            float O = 0.f;
 #pragma unroll 4
-          for (int cc = 0; cc < nch; ++cc) O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2)), S.s_pm[i][cc], O);
-          a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / S.s_l[i];
+            for (int cc = 0; cc < nch; ++cc) O = fmaf(__ldcg(pb + (size_t)cc * (HD + 2)), S.s_pm[i][cc], O);
+            a.o[(size_t)slot * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / S.s_l[i];
+          }
         }
       } else {
         for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
