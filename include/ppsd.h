@@ -156,6 +156,13 @@ int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t
 int ppsd_set_schedule(ppsd_engine* e, int32_t schedule);
 int ppsd_get_schedule(ppsd_engine* e, int32_t greedy, int32_t* schedule);
 
+/* ToyLM.empirical_alpha / greedy_agreement (pkg/src/specpipe/toylm.py:160-192)
+ * on a ToyLM engine: for each of n_prefixes prefixes (row-major, prefix_len
+ * tokens each) out_minsum[i] = sum(min(p, q)) and out_agree[i] = (argmax p ==
+ * argmax q), p = exit head at exit_depth, q = full model. */
+int ppsd_toy_alignment(ppsd_engine* e, int32_t exit_depth, int32_t n_prefixes, int32_t prefix_len,
+                       const int32_t* prefixes, double* out_minsum, int32_t* out_agree);
+
 /* full-model autoregressive decode (the oracle / AR baseline); sampling mode
  * draws one commit-stream uniform per token (pipesim.py:397-406) */
 int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, const int32_t* prompt,

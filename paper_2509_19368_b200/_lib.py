@@ -76,6 +76,8 @@ EXPORTS = {
                               C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics),
                               C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
     "ppsd_set_schedule": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ppsd_toy_alignment": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "ppsd_get_schedule": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "ppsd_decode_ar": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32), C.c_int32,
                                  C.c_int32, C.POINTER(C.c_int32), C.POINTER(Metrics)]),

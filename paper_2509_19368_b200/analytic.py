@@ -79,3 +79,41 @@ def ppsd_over_eesd_lambda(params: SpeedupParams) -> float:
     s = n_stages(n, e)
     return (1.0 - a) * (g * e + n) / ((a * e + (1.0 - a) * s * e) * (1.0 - a ** (g + 1)))
 
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Wall-clock cost of one full-model forward and one draft forward
+    (analytic.py:22-36); t_draft = 0 is the free-drafts limit."""
+
+    t_target: float
+    t_draft: float
+
+    def __post_init__(self):
+        if self.t_target <= 0.0:
+            raise ValueError("t_target must be positive")
+        if self.t_draft < 0.0:
+            raise ValueError("t_draft must be non-negative")
+
+
+def overall_acceptance(alpha: float, gamma: int) -> float:
+    """expected_accept_len / gamma: accepted fraction of all drafted tokens."""
+    return expected_accept_len(alpha, gamma) / gamma
+
+
+def sd_gain(cost: CostModel, alpha: float, gamma: int) -> float:
+    """t_target / (gamma*t_draft + t_target) * (expected_accept_len + 1)."""
+    _alpha(alpha)
+    _gamma(gamma)
+    return cost.t_target / (gamma * cost.t_draft + cost.t_target) * (expected_accept_len(alpha, gamma) + 1.0)
+
+
+def eesd_best_gamma(alpha: float, n_layers: int, exit_depth: int, gamma_max: int = 64) -> int:
+    """Draft length in 1..gamma_max maximising eesd_speedup (first maximum)."""
+    _alpha(alpha)
+    best_g, best_v = 1, float("-inf")
+    for g in range(1, gamma_max + 1):
+        v = eesd_speedup(SpeedupParams(alpha, g, n_layers, exit_depth))
+        if v > best_v:
+            best_g, best_v = g, v
+    return best_g

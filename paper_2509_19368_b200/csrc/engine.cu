@@ -946,6 +946,59 @@ extern "C" int ppsd_get_schedule(ppsd_engine* e, int32_t greedy, int32_t* schedu
   return PPSD_OK;
 }
 
+// ToyLM.empirical_alpha / greedy_agreement (toylm.py:160-192): per-prefix
+// sum(min(p, q)) and argmax agreement of the exit head at exit_depth, for
+// n_prefixes prefixes of prefix_len tokens (row-major). The caller sums the
+// per-prefix values in order, as the reference does.
+extern "C" int ppsd_toy_alignment(ppsd_engine* e, int32_t exit_depth, int32_t n_prefixes, int32_t prefix_len,
+                                  const int32_t* prefixes, double* out_minsum, int32_t* out_agree) {
+  if (!e || !prefixes || !out_minsum || !out_agree) return fail(PPSD_EINVAL, "null argument");
+  if (e->md.kind != PPSD_MODEL_TOYLM) return fail(PPSD_EINVAL, "alignment needs a ToyLM engine");
+  if (n_prefixes < 1) return fail(PPSD_EINVAL, "n_prefixes must be >= 1");
+  if (prefix_len < 1) return fail(PPSD_EINVAL, "prefix must be non-empty");
+  if (exit_depth < 1 || exit_depth > e->md.n_layers)
+    return fail(PPSD_EINVAL, "exit_depth must lie in [1, " + std::to_string(e->md.n_layers) + "], got " +
+                                 std::to_string(exit_depth));
+  for (int64_t i = 0; i < (int64_t)n_prefixes * prefix_len; ++i)
+    if (prefixes[i] < 0 || prefixes[i] >= e->md.vocab) return fail(PPSD_EINVAL, "prefix token outside vocab");
+  CU(cudaSetDevice(e->device));
+  std::vector<uint64_t> pd(n_prefixes);
+  for (int i = 0; i < n_prefixes; ++i) {  // sequence digests (toylm.py:72-86)
+    uint64_t d = hmix64(e->md.toy_seed ^ kSeqSalt);
+    for (int j = 0; j < prefix_len; ++j) d = toy_extend(d, prefixes[(size_t)i * prefix_len + j]);
+    pd[i] = d;
+  }
+  const size_t V = (size_t)e->md.vocab;
+  uint64_t* d_pd = nullptr;
+  double *d_scr = nullptr, *d_ms = nullptr;
+  int* d_ag = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(d_pd);
+    cudaFree(d_scr);
+    cudaFree(d_ms);
+    cudaFree(d_ag);
+  };
+  if (cudaMalloc(&d_pd, sizeof(uint64_t) * n_prefixes) != cudaSuccess ||
+      cudaMalloc(&d_scr, sizeof(double) * 4 * V * n_prefixes) != cudaSuccess ||
+      cudaMalloc(&d_ms, sizeof(double) * n_prefixes) != cudaSuccess ||
+      cudaMalloc(&d_ag, sizeof(int) * n_prefixes) != cudaSuccess) {
+    cleanup();
+    return fail(PPSD_ECUDA, "alignment scratch allocation failed");
+  }
+  cudaError_t ce = cudaMemcpyAsync(d_pd, pd.data(), sizeof(uint64_t) * n_prefixes, cudaMemcpyHostToDevice, e->st);
+  if (ce == cudaSuccess) {
+    toy_alignment_kernel<<<n_prefixes, 256, 0, e->st>>>(d_pd, e->md.n_layers, exit_depth, e->md.vocab,
+                                                        e->md.toy_seed, e->md.toy_misalignment, d_scr, d_ms, d_ag);
+    ce = cudaGetLastError();
+  }
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(out_minsum, d_ms, sizeof(double) * n_prefixes, cudaMemcpyDeviceToHost, e->st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(out_agree, d_ag, sizeof(int) * n_prefixes, cudaMemcpyDeviceToHost, e->st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->st);
+  cleanup();
+  CU(ce);
+  return PPSD_OK;
+}
+
 extern "C" int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed, int32_t horizon,
                              int32_t force_reject, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
                              int64_t* trace_len) {

@@ -86,6 +86,9 @@ __global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
 __global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void p2p_wait_kernel(const TickCtx* ctxp);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);
+__global__ void toy_alignment_kernel(const uint64_t* pdig, int n_layers, int exit_depth, int vocab,
+                                     uint64_t toy_seed, double beta, double* scratch, double* minsum,
+                                     int* agree);
 __global__ void prefill_chunk_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void eesd_draft_begin_kernel(const TickCtx* ctxp, EesdState* es);
 __global__ void eesd_draft_end_kernel(const TickCtx* ctxp, EesdState* es);

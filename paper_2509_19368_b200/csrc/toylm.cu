@@ -131,4 +131,41 @@ __global__ void __launch_bounds__(256) toy_ar_kernel(const TickCtx* ctxp, int n_
   }
 }
 
+// Measured alignment of the exit head (toylm.py:160-192): for prefix i
+// (sequence digest pdig[i]) p = softmax(exit logits at layer E), q =
+// softmax(final logits); minsum[i] = sum(min(p, q)) in numpy's pairwise
+// order, agree[i] = argmax p == argmax q (first index among maxima). One CTA
+// per prefix; scratch = 4 * V doubles per prefix.
+__global__ void __launch_bounds__(256) toy_alignment_kernel(const uint64_t* pdig, int n_layers, int exit_depth,
+                                                            int vocab, uint64_t toy_seed, double beta,
+                                                            double* scratch, double* minsum, int* agree) {
+  (void)toy_seed;
+  const int i = blockIdx.x, V = vocab;
+  const bool exact = V <= kExactVocab;
+  double* zl = scratch + (size_t)i * 4 * V;
+  double* q = zl + V;
+  double* p = q + V;
+  double* w = p + V;
+  const uint64_t d0 = pdig[i];
+  const uint64_t fin = toy_advance(d0, 0, n_layers);
+  const uint64_t ex = toy_advance(d0, 0, exit_depth);
+  for (int v = threadIdx.x; v < V; v += blockDim.x) zl[v] = toy_logit(fin, v);
+  __syncthreads();
+  block_softmax(zl, nullptr, V, q, exact);
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) zl[v] = toy_exit_logit(fin, ex, beta, v);
+  __syncthreads();
+  block_softmax(zl, nullptr, V, p, exact);
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) w[v] = fmin(p[v], q[v]);
+  __syncthreads();
+  const double ms = block_sum(w, V, exact);
+  const int ap = block_argmax(V, [&](int v) { return p[v]; });
+  const int aq = block_argmax(V, [&](int v) { return q[v]; });
+  if (threadIdx.x == 0) {
+    minsum[i] = ms;
+    agree[i] = ap == aq;
+  }
+}
+
 }  // namespace ppsd

@@ -221,6 +221,25 @@ def engine_for(lm, cfg: PipelineConfig) -> Engine:
     raise TypeError(f"the B200 engine runs ToyLM or TransformerLM models, got {type(lm).__name__}")
 
 
+def toy_alignment(lm: ToyLM, exit_depth: int, prefixes):
+    """Per-prefix sum(min(p, q)) and argmax agreement of the ToyLM exit head
+    at exit_depth, computed on the GPU (ppsd_toy_alignment)."""
+    if not 1 <= exit_depth <= lm.n_layers:
+        raise ValueError(f"exit_depth must lie in [1, {lm.n_layers}], got {exit_depth}")
+    n, plen = len(prefixes), len(prefixes[0])
+    cfg = PipelineConfig(lm.n_layers, max(1, lm.n_layers // 2)) if lm.n_layers >= 2 else None
+    if cfg is None:
+        raise NotImplementedError("single-layer models are not supported by the engine")
+    eng = engine_for(lm, cfg)
+    flat = np.ascontiguousarray(np.asarray(prefixes, dtype=np.int32).reshape(-1))
+    minsum = np.zeros(n, dtype=np.float64)
+    agree = np.zeros(n, dtype=np.int32)
+    _lib.check(_lib.lib().ppsd_toy_alignment(eng.h, exit_depth, n, plen, flat.ctypes.data_as(C.POINTER(C.c_int32)),
+                                             minsum.ctypes.data_as(C.POINTER(C.c_double)),
+                                             agree.ctypes.data_as(C.POINTER(C.c_int32))), "toy_alignment")
+    return minsum.tolist(), agree.tolist()
+
+
 def _toy_ctx_for(lm: ToyLM, n_prompt: int, max_tokens: int, cfg: PipelineConfig) -> None:
     need = n_prompt + max_tokens + cfg.n_stages * cfg.hop_period + 2
     if need > 4096:

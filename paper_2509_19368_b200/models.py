@@ -54,6 +54,38 @@ class ToyLM:
                               max_ctx=max_ctx, toy_seed=self.seed & ((1 << 64) - 1),
                               toy_misalignment=float(self.misalignment))
 
+    # ---- measured alignment (toylm.py:153-192), evaluated on the GPU ----
+
+    EVAL_PREFIX_LEN = 8  # toylm.py:32
+
+    def _alignment(self, exit_depth: int, n_prefixes: int, eval_seed: int | None):
+        from .decode import toy_alignment
+        from .rng import RngStream, derive_seed
+
+        if n_prefixes < 1:
+            raise ValueError("n_prefixes must be >= 1")
+        if eval_seed is None:
+            eval_seed = derive_seed(self.seed, "empirical-alpha")
+        stream = RngStream(eval_seed)
+        prefixes = [[stream.randbelow(self.vocab) for _ in range(self.EVAL_PREFIX_LEN)]
+                    for _ in range(n_prefixes)]
+        return toy_alignment(self, exit_depth, prefixes)
+
+    def empirical_alpha(self, exit_depth: int, n_prefixes: int, eval_seed: int | None = None) -> float:
+        """Mean sum(min(p, q)) over seeded random prefixes: the acceptance
+        rate of sampling-mode verification (toylm.py:165-179)."""
+        minsum, _ = self._alignment(exit_depth, n_prefixes, eval_seed)
+        acc = 0.0
+        for v in minsum:  # the reference's left-to-right accumulation
+            acc += float(v)
+        return acc / n_prefixes
+
+    def greedy_agreement(self, exit_depth: int, n_prefixes: int, eval_seed: int | None = None) -> float:
+        """Fraction of seeded random prefixes whose exit-head and full-model
+        argmax agree: the greedy-mode acceptance rate (toylm.py:181-192)."""
+        _, agree = self._alignment(exit_depth, n_prefixes, eval_seed)
+        return int(sum(int(a) for a in agree)) / n_prefixes
+
 
 @dataclass(frozen=True)
 class TransformerConfig:

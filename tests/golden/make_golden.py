@@ -14,6 +14,9 @@ Fixture files:
   acceptance200.json  the 200-case sweep of test_acceptance.py:133-154
   eesd_toy.json       simulate_eesd with the toy greedy oracle + Bernoulli
   transformer.json    reference decode_ppsd driving oracle/transformer.py
+  harness.json        harness.run results rows (+ analytic column), ToyLM
+                      empirical_alpha / greedy_agreement, ConfigError messages,
+                      analytic_report
 """
 
 from __future__ import annotations
@@ -218,11 +221,85 @@ def make_sampling():
     return out
 
 
+HARNESS_RUNS = [
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=128, oracle="bernoulli", alpha=0.7, seed=1),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=96, oracle="toylm-greedy", beta=1.0, seed=2),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=96, oracle="toylm-sampling", beta=0.5, seed=3),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=64, exit_stage=2, oracle="toylm-greedy",
+         beta=1.5, seed=4),
+    dict(regime="ppsd", n_layers=33, exit_depth=8, horizon=80, comm_latency=1, oracle="bernoulli",
+         alpha=0.55, seed=5, steady_state=True),
+    dict(regime="eesd", n_layers=32, exit_depth=8, horizon=100, gamma=5, oracle="bernoulli", alpha=0.6,
+         seed=6),
+    dict(regime="eesd", n_layers=32, exit_depth=8, horizon=100, gamma=3, oracle="toylm-greedy", beta=1.0,
+         seed=7),
+    dict(regime="eesd", n_layers=32, exit_depth=8, horizon=60, gamma=4, exit_stage=2, oracle="bernoulli",
+         alpha=0.8, seed=8),
+    dict(regime="autoregressive", n_layers=32, exit_depth=8, horizon=50, seed=9),
+    dict(regime="autoregressive", n_layers=24, exit_depth=5, horizon=20, comm_latency=2, seed=10,
+         steady_state=True),
+    dict(regime="ppsd", n_layers=16, exit_depth=4, horizon=64, oracle="toylm-greedy", beta=0.0, vocab=64,
+         seed=11),
+]
+HARNESS_BAD = [
+    dict(regime="nope", n_layers=32, exit_depth=8, horizon=10),
+    dict(regime="ppsd", n_layers=32, exit_depth=40, horizon=10, oracle="bernoulli", alpha=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=0, oracle="bernoulli", alpha=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, exit_stage=4, oracle="bernoulli", alpha=0.5),
+    dict(regime="autoregressive", n_layers=32, exit_depth=8, horizon=10, gamma=3),
+    dict(regime="autoregressive", n_layers=32, exit_depth=8, horizon=10, beta=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="magic"),
+    dict(regime="eesd", n_layers=32, exit_depth=8, horizon=10, oracle="bernoulli", alpha=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, gamma=2, oracle="bernoulli", alpha=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="bernoulli"),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="bernoulli", alpha=1.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="bernoulli", alpha=0.5, beta=1.0),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="toylm-greedy", alpha=0.5),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="toylm-greedy", beta=-1.0),
+    dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=10, oracle="toylm-greedy", vocab=1),
+    dict(regime="ppsd", n_layers=32.0, exit_depth=8, horizon=10, oracle="bernoulli", alpha=0.5),
+    dict(regime="ppsd", n_layers=8, exit_depth=8, horizon=10, exit_stage=1, oracle="bernoulli", alpha=0.5),
+]
+
+
+def make_harness():
+    from specpipe import harness as H
+
+    runs = []
+    for kw in HARNESS_RUNS:
+        res = H.run(H.ExperimentConfig(**kw), want_trace=True)
+        runs.append(dict(config=kw, row=H.result_row(res), measured_alpha=res.measured_alpha,
+                         trace_csv=trace_text(res.trace)))
+    bad = []
+    for kw in HARNESS_BAD:
+        try:
+            H.ExperimentConfig(**kw)
+            bad.append(dict(config=kw, error=None))
+        except H.ConfigError as exc:
+            bad.append(dict(config=kw, field=exc.field, error=str(exc)))
+    align = []
+    for seed, beta, vocab, n, e in ((0, 1.0, 16, 32, 8), (3, 0.3, 16, 32, 4), (5, 2.0, 64, 24, 12), (9, 0.0, 16, 8, 2)):
+        lm = sp.ToyLM(n_layers=n, vocab=vocab, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        align.append(dict(n_layers=n, vocab=vocab, lm_seed=lm.seed, beta=beta, exit_depth=e,
+                          empirical_alpha=lm.empirical_alpha(e, 200), greedy_agreement=lm.greedy_agreement(e, 200),
+                          empirical_alpha_seeded=lm.empirical_alpha(e, 37, eval_seed=12345)))
+    reports = [dict(args=[a, g, n, e], text=H.analytic_report(a, g, n, e))
+               for a, g, n, e in ((0.7, 4, 32, 8), (1.0, 5, 32, 8), (0.0, 1, 40, 20), (0.55, 10, 80, 10))]
+    sweep = H.SweepSpec.from_dict(dict(base=dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=48,
+                                                 oracle="bernoulli", alpha=0.5, seed=3),
+                                       axes={"alpha": [0.3, 0.9], "exit_depth": [4, 8]}))
+    buf = io.StringIO()
+    H.write_results_csv(H.sweep(sweep), buf)
+    return [dict(kind="runs", cases=runs), dict(kind="bad", cases=bad), dict(kind="align", cases=align),
+            dict(kind="report", cases=reports), dict(kind="sweep", csv=buf.getvalue())]
+
+
 def main(argv):
-    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp"}
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness"}
     jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
             ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
-            ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling)]
+            ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling),
+            ("harness", "harness.json", make_harness)]
     for key, fname, fn in jobs:
         if key in which:
             data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",
