@@ -1,17 +1,20 @@
-"""Command line: `python -m paper_2509_19368_b200 decode ...`
+"""Command line: `python -m paper_2509_19368_b200 {analytic,run,sweep,decode,trace} ...`
 
-The `decode` subcommand keeps the flags, output and exit codes of the
-reference's `specpipe decode` (pkg/src/specpipe/cli.py:183-226, 264-280,
-284-291) and runs on the B200 engine. `--model` extends it to the
-transformer models (the reference only has the ToyLM).
+Keeps the subcommands, flags, output and exit codes of the reference's
+`specpipe` CLI (pkg/src/specpipe/cli.py:39-291); `run` / `sweep` / `trace`
+go through harness.py onto the GPU tick machine, `decode` runs on the B200
+engine. `decode --model` extends it to the transformer models (the reference
+only has the ToyLM). Config or usage errors: `error: ...` on stderr, exit 2.
 """
 
 from __future__ import annotations
 
 import argparse
+import json
 import sys
 
 from . import __version__
+from . import harness as H
 from .decode import decode_autoregressive, decode_eesd, decode_ppsd
 from .models import ToyLM, TransformerConfig, TransformerLM
 from .pipeline import PipelineConfig, default_prompt
@@ -80,11 +83,100 @@ def _cmd_decode(args) -> int:
     return 0
 
 
+_CONFIG_FIELDS = ("regime", "n_layers", "exit_depth", "exit_stage", "comm_latency", "horizon", "gamma", "oracle",
+                  "alpha", "beta", "vocab", "seed", "steady_state", "out", "trace_out")
+
+
+def _config_flags(p) -> None:
+    p.add_argument("--config", metavar="JSON", help="experiment config file")
+    p.add_argument("--regime", choices=H.REGIMES)
+    for name in ("n-layers", "exit-depth", "exit-stage", "comm-latency", "horizon", "gamma"):
+        p.add_argument(f"--{name}", type=int)
+    p.add_argument("--oracle", choices=H.ORACLES)
+    p.add_argument("--alpha", type=float)
+    p.add_argument("--beta", type=float)
+    p.add_argument("--vocab", type=int)
+    p.add_argument("--seed", type=int)
+    p.add_argument("--steady-state", action="store_const", const=True, default=None,
+                   help="subtract pipeline warm-up ticks from the rates")
+    p.add_argument("--out", help="write the results CSV here")
+    p.add_argument("--trace-out", help="write the event trace CSV here")
+    p.add_argument("--dump-config", action="store_true",
+                   help="print the effective config as JSON and exit without running")
+
+
+def _config(args) -> H.ExperimentConfig:
+    data = H.ExperimentConfig.from_json(args.config).to_dict() if args.config else {}
+    for name in _CONFIG_FIELDS:  # a flag wins over the file
+        v = getattr(args, name)
+        if v is not None:
+            data[name] = v
+    return H.ExperimentConfig.from_dict(data)
+
+
+def _cmd_analytic(args) -> int:
+    print(H.analytic_report(alpha=args.alpha, gamma=args.gamma, n_layers=args.n_layers,
+                            exit_depth=args.exit_depth, t_target=args.t_target, t_draft=args.t_draft))
+    return 0
+
+
+def _cmd_run(args, need_trace: bool = False) -> int:
+    cfg = _config(args)
+    if need_trace and not cfg.trace_out:
+        raise H.ConfigError("trace_out", "the trace subcommand needs --trace-out")
+    if args.dump_config:
+        print(json.dumps(cfg.to_dict(), indent=2, sort_keys=True))
+        return 0
+    res = H.run(cfg)
+    m = res.metrics
+    pairs = [("regime", cfg.regime), ("committed", m.committed_tokens), ("ticks", m.ticks),
+             ("accepts", m.accepts), ("rejects", m.rejects)]
+    if m.alpha_all_measured is not None:
+        pairs.append(("alpha_all", m.alpha_all_measured))
+    pairs += [("throughput", m.throughput), ("speedup_vs_ar", m.speedup_vs_ar)]
+    if res.analytic_speedup is not None:
+        pairs.append(("analytic_speedup", res.analytic_speedup))
+    _print_kv(pairs)
+    if cfg.out:
+        print(f"results -> {H.resolve_out_path(cfg.out)}")
+    if cfg.trace_out:
+        print(f"trace   -> {H.resolve_out_path(cfg.trace_out)}")
+    return 0
+
+
+def _cmd_sweep(args) -> int:
+    results = H.sweep(H.SweepSpec.from_json(args.config))
+    if args.out:
+        path = H.resolve_out_path(args.out)
+        H.write_results_csv(results, path)
+        print(f"{len(results)} rows -> {path}")
+    else:
+        print(H.RESULTS_HEADER)
+        for r in results:
+            print(H.result_row(r))
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2509_19368_b200",
                                      description="B200 engine for pipeline-parallel self-speculative decoding")
     parser.add_argument("--version", action="version", version=f"paper_2509_19368_b200 {__version__}")
     sub = parser.add_subparsers(dest="command", required=True)
+    pa = sub.add_parser("analytic", help="print closed-form quantities")
+    pa.add_argument("--alpha", type=float, required=True)
+    pa.add_argument("--gamma", type=int, required=True)
+    pa.add_argument("--n-layers", type=int, required=True)
+    pa.add_argument("--exit-depth", type=int, required=True)
+    pa.add_argument("--t-target", type=float, default=1.0)
+    pa.add_argument("--t-draft", type=float, default=None)
+    pa.set_defaults(func=_cmd_analytic)
+    pr = sub.add_parser("run", help="execute one experiment")
+    _config_flags(pr)
+    pr.set_defaults(func=_cmd_run)
+    ps = sub.add_parser("sweep", help="run a sweep spec")
+    ps.add_argument("--config", metavar="JSON", required=True, help="sweep spec file")
+    ps.add_argument("--out", help="combined results CSV (default: stdout)")
+    ps.set_defaults(func=_cmd_sweep)
     p = sub.add_parser("decode", help="decode with the pipelined schedule on the GPU")
     p.add_argument("--n-layers", type=int, required=True)
     p.add_argument("--exit-depth", type=int, required=True)
@@ -104,6 +196,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--max-ctx", type=int, default=1024)
     p.add_argument("--gamma", type=int, default=0, help="run the EESD baseline with this draft length instead")
     p.set_defaults(func=_cmd_decode)
+    pt = sub.add_parser("trace", help="run one experiment for its event trace")
+    _config_flags(pt)
+    pt.set_defaults(func=lambda a: _cmd_run(a, need_trace=True))
     return parser
 
 

@@ -14,6 +14,9 @@ Fixture files:
   acceptance200.json  the 200-case sweep of test_acceptance.py:133-154
   eesd_toy.json       simulate_eesd with the toy greedy oracle + Bernoulli
   transformer.json    reference decode_ppsd driving oracle/transformer.py
+  cli_decode.json     `specpipe decode` transcripts (stdout, exit code)
+  cli_harness.json    `specpipe analytic|run|sweep|trace` transcripts (stdout,
+                      stderr, exit code)
   harness.json        harness.run results rows (+ analytic column), ToyLM
                       empirical_alpha / greedy_agreement, ConfigError messages,
                       analytic_report
@@ -294,12 +297,74 @@ def make_harness():
             dict(kind="report", cases=reports), dict(kind="sweep", csv=buf.getvalue())]
 
 
+CLI_HARNESS = [
+    ["analytic", "--alpha", "0.7", "--gamma", "4", "--n-layers", "32", "--exit-depth", "8"],
+    ["analytic", "--alpha", "0.4", "--gamma", "6", "--n-layers", "40", "--exit-depth", "10", "--t-draft", "0.3"],
+    ["run", "--regime", "ppsd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "64", "--oracle",
+     "bernoulli", "--alpha", "0.6", "--seed", "4"],
+    ["run", "--regime", "ppsd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "64", "--oracle",
+     "toylm-greedy", "--beta", "1.0", "--seed", "2"],
+    ["run", "--regime", "eesd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "50", "--gamma", "4",
+     "--oracle", "toylm-greedy", "--beta", "0.5", "--steady-state"],
+    ["run", "--regime", "autoregressive", "--n-layers", "32", "--exit-depth", "8", "--horizon", "20"],
+    ["run", "--config", "{config_json}", "--horizon", "40"],
+    ["run", "--config", "{config_json}", "--dump-config"],
+    ["run", "--regime", "ppsd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "10"],
+    ["run", "--regime", "ppsd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "10", "--oracle",
+     "bernoulli", "--alpha", "2.0"],
+    ["trace", "--regime", "ppsd", "--n-layers", "32", "--exit-depth", "8", "--horizon", "10", "--oracle",
+     "bernoulli", "--alpha", "0.5"],
+    ["sweep", "--config", "{sweep_json}"],
+]
+CLI_CONFIG = dict(regime="ppsd", n_layers=24, exit_depth=6, horizon=30, oracle="toylm-sampling", beta=0.8, seed=5)
+CLI_SWEEP = dict(base=dict(regime="eesd", n_layers=32, exit_depth=8, horizon=40, gamma=3, oracle="bernoulli",
+                           alpha=0.5, seed=2), axes={"gamma": [2, 5], "alpha": [0.25, 0.75]})
+
+
+CLI_DECODE = [["decode", "--n-layers", "32", "--exit-depth", "8", "--beta", "1.0", "--mode", "greedy", "--max-tokens", "48", "--check-ar"], ["decode", "--n-layers", "32", "--exit-depth", "8", "--beta", "1.0", "--max-tokens", "48", "--seed", "3"], ["decode", "--n-layers", "33", "--exit-depth", "8", "--beta", "2.0", "--mode", "sampling", "--max-tokens", "40", "--prompt", "1,2,3", "--force-reject", "--check-ar"], ["decode", "--n-layers", "32", "--exit-depth", "8", "--exit-stage", "2", "--comm-latency", "1", "--beta", "0.5", "--mode", "greedy", "--max-tokens", "32"]]
+
+
+def make_cli_decode():
+    import subprocess
+
+    env = dict(os.environ, PYTHONPATH="/root/reference/pkg/src")
+    out = []
+    for argv in CLI_DECODE:
+        r = subprocess.run([sys.executable, "-m", "specpipe.cli", *argv], capture_output=True, text=True, env=env,
+                           cwd="/tmp", timeout=600)
+        out.append(dict(argv=argv, stdout=r.stdout, returncode=r.returncode))
+    return out
+
+
+def make_cli_harness():
+    import subprocess
+    import tempfile
+
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        paths = {"config_json": os.path.join(d, "config.json"), "sweep_json": os.path.join(d, "sweep.json")}
+        with open(paths["config_json"], "w") as fh:
+            fh.write(json.dumps(CLI_CONFIG))
+        with open(paths["sweep_json"], "w") as fh:
+            fh.write(json.dumps(CLI_SWEEP))
+        env = dict(os.environ, PYTHONPATH="/root/reference/pkg/src")
+        for argv in CLI_HARNESS:
+            real = [a.format(**paths) for a in argv]
+            r = subprocess.run([sys.executable, "-m", "specpipe.cli", *real], capture_output=True, text=True,
+                               env=env, cwd=d, timeout=600)
+            out.append(dict(argv=argv, stdout=r.stdout, stderr=r.stderr, returncode=r.returncode))
+    # file texts, not dicts: the fixture is dumped with sorted keys and the
+    # sweep axes' order is significant
+    return [dict(config_json=json.dumps(CLI_CONFIG), sweep_json=json.dumps(CLI_SWEEP), commands=out)]
+
+
 def main(argv):
-    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness"}
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness", "cli", "clidec"}
     jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
             ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
             ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling),
-            ("harness", "harness.json", make_harness)]
+            ("harness", "harness.json", make_harness), ("cli", "cli_harness.json", make_cli_harness),
+            ("clidec", "cli_decode.json", make_cli_decode)]
     for key, fname, fn in jobs:
         if key in which:
             data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",
