@@ -255,3 +255,27 @@ def test_eesd_lossless_vs_ar(gamma):
     toks, m, _ = ppsd.decode_eesd(lm, ppsd.PipelineConfig(6, 2), prompt, 100, gamma)
     assert toks[:100] == ar
     assert m.committed_tokens >= 100
+
+
+def test_folded_edge_cases():
+    """Folded ≡ pipelined on the edges: one-token prompt (no prefill), one
+    generated token, force_reject (every verdict a rollback), a context that
+    crosses a KV page inside a deep batch, max_ctx-bound runs."""
+    sh = dict(SHAPES["mid_gqa"])
+    sh["n_layers"] = 8
+    config = ppsd.TransformerConfig(**sh, kv_dtype="bf16", max_ctx=200)
+    lm = ppsd.TransformerLM(config, seed=9, deep_scale=0.4, deep_from=2)
+    cfg = ppsd.PipelineConfig(8, 2)
+    cases = [([5], 30, False), ([3, 1, 4], 1, False), ([2, 7], 40, True), (list(range(60)), 40, False),
+             ([11] * 3, 200 - 3 - cfg.n_stages * cfg.hop_period - 2, False)]
+    for prompt, n, fr in cases:
+        out = {}
+        for sched in ("pipelined", "folded"):
+            lm.schedule = sched
+            toks, m, tr = ppsd.decode_ppsd(lm, cfg, prompt, n, "greedy", ppsd.RngStream(0), force_reject=fr)
+            out[sched] = (toks, _metrics_list(m), tr.to_csv())
+        lm.schedule = "auto"
+        assert out["folded"] == out["pipelined"], (len(prompt), n, fr)
+        assert out["folded"][0] == ppsd.decode_autoregressive(lm, prompt, n, "greedy", ppsd.RngStream(0))
+    with pytest.raises(ValueError):
+        ppsd.decode_ppsd(lm, cfg, [1, 2], 200, "greedy", ppsd.RngStream(0))
