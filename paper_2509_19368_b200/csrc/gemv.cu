@@ -106,7 +106,7 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
 // (VPT 1-2) did not beat 8 warps with twice the columns per thread (the
 // batched plans got slower: fewer rows per tile fit in 120 registers), so
 // every plan uses 8.
-constexpr int nw_for(int vpt) { return vpt > 0 ? 8 : 8; }
+constexpr int nw_for(int /*vpt*/) { return 8; }
 
 // Register boost for the batched plans of wide-K matrices (the down
 // projection, VPT >= 5): their M=4 input slices need ~230 registers per
