@@ -178,6 +178,15 @@ int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32
                      ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
                      int64_t* trace_len);
 
+/* the same rounds in the given mode: greedy = 1 as above; greedy = 0 draws
+ * drafts, accept_draft verdicts, residual resamples and the bonus from the
+ * streams derive_seed(rng_seed, "draft" | "verify" | "commit") exactly as
+ * _ToyVerifier (pipesim.py:339-365, 475-541). */
+int ppsd_decode_eesd_mode(ppsd_engine* e, int32_t gamma, int32_t greedy, uint64_t rng_seed,
+                          const int32_t* prompt, int32_t n_prompt, int32_t horizon, int32_t* out_tokens,
+                          int32_t out_cap, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                          int64_t* trace_len);
+
 /* simulate_eesd with AcceptanceOracle.bernoulli (verify_seed =
  * derive_seed(rng.seed, "verify"), pipesim.py:467) */
 int ppsd_simulate_eesd(ppsd_engine* e, int32_t gamma, double alpha, uint64_t verify_seed,

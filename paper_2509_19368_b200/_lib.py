@@ -84,6 +84,9 @@ EXPORTS = {
     "ppsd_decode_eesd": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
                                    C.POINTER(C.c_int32), C.c_int32, C.POINTER(Metrics),
                                    C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
+    "ppsd_decode_eesd_mode": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.POINTER(C.c_int32),
+                                        C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.POINTER(Metrics),
+                                        C.POINTER(TraceRowC), C.c_int64, C.POINTER(C.c_int64)]),
     "ppsd_simulate_eesd": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.c_uint64, C.c_int32,
                                      C.POINTER(Metrics), C.POINTER(TraceRowC), C.c_int64,
                                      C.POINTER(C.c_int64)]),

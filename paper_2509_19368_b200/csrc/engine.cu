@@ -1090,14 +1090,14 @@ static int eesd_graph(ppsd_engine* e, int gamma, cudaGraphExec_t* out, int64_t* 
           const int m = enqueue_layers(e, e->d_work_ar, exit_layer, false);
           if (m < 0) return -1;
           if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
-          if (launch_pdl(eesd_draft_end_kernel, dim3(1), dim3(32), 0, e->st, ctx, es) != cudaSuccess) return -1;
+          if (launch_pdl(eesd_draft_end_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
           cnt += m + 3;
         }
         if (launch_pdl(eesd_verify_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
         const int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);  // batched verify
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work_ar, 0, kMatHeadV, true) != cudaSuccess) return -1;
-        if (launch_pdl(eesd_scan_kernel, dim3(1), dim3(32), 0, e->st, ctx, es) != cudaSuccess) return -1;
+        if (launch_pdl(eesd_scan_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
         return cnt + m + 3;
       },
       &g, &n);
@@ -1200,15 +1200,29 @@ static int run_eesd(ppsd_engine* e, int model, int gamma, const int32_t* prompt,
   return PPSD_OK;
 }
 
-extern "C" int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32_t n_prompt,
-                                int32_t horizon, int32_t* out_tokens, int32_t out_cap, ppsd_metrics* out,
-                                ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+extern "C" int ppsd_decode_eesd_mode(ppsd_engine* e, int32_t gamma, int32_t greedy, uint64_t rng_seed,
+                                     const int32_t* prompt, int32_t n_prompt, int32_t horizon, int32_t* out_tokens,
+                                     int32_t out_cap, ppsd_metrics* out, ppsd_trace_row* trace, int64_t trace_cap,
+                                     int64_t* trace_len) {
   if (!e || !out) return fail(PPSD_EINVAL, "null argument");
   if (e->md.kind == PPSD_MODEL_BERNOULLI) return fail(PPSD_EINVAL, "Bernoulli engines run ppsd_simulate_eesd");
   int rc = check_prompt(e, prompt, n_prompt);
   if (rc) return rc;
-  return run_eesd(e, 1, gamma, prompt, n_prompt, horizon, 0.0, 0, out_tokens, out_cap, out, trace, trace_cap,
-                  trace_len);
+  if (!greedy && gamma > std::max(e->cfg.nslot, (int)kMaxVec))
+    return fail(PPSD_EUNSUPPORTED, "sampling-mode EESD keeps each draft's distribution: gamma <= " +
+                                       std::to_string(std::max(e->cfg.nslot, (int)kMaxVec)));
+  CU(cudaSetDevice(e->device));
+  rc = set_mode(e, greedy, rng_seed);
+  if (rc) return rc;
+  return run_eesd(e, 1, gamma, prompt, n_prompt, horizon, 0.0, greedy ? 0 : e->verify_seed, out_tokens, out_cap,
+                  out, trace, trace_cap, trace_len);
+}
+
+extern "C" int ppsd_decode_eesd(ppsd_engine* e, int32_t gamma, const int32_t* prompt, int32_t n_prompt,
+                                int32_t horizon, int32_t* out_tokens, int32_t out_cap, ppsd_metrics* out,
+                                ppsd_trace_row* trace, int64_t trace_cap, int64_t* trace_len) {
+  return ppsd_decode_eesd_mode(e, gamma, 1, 0, prompt, n_prompt, horizon, out_tokens, out_cap, out, trace,
+                               trace_cap, trace_len);
 }
 
 extern "C" int ppsd_simulate_eesd(ppsd_engine* e, int32_t gamma, double alpha, uint64_t verify_seed,

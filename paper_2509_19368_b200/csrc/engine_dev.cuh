@@ -76,6 +76,7 @@ struct EesdState {
   uint64_t verify_counter;
   int32_t t, committed, accepts, rejects, drafted, done, error, len;  // len = sequence length
   int64_t trace_n;
+  uint64_t draft_counter, commit_counter;  // sampling mode (_ToyVerifier streams)
 };
 
 __global__ void sched_tick_kernel(const TickCtx* ctxp, int begin);

@@ -41,13 +41,6 @@ def _require_draft_head(cfg: PipelineConfig) -> int:
     return cfg.exit_stage
 
 
-def _greedy_only(mode: str) -> None:
-    if mode != "greedy":
-        raise NotImplementedError(
-            "sampling-mode verification is not implemented on the B200 engine yet "
-            "(greedy is the parity contract; SURVEY.md §8f-2)")
-
-
 class Engine:
     """One libppsd engine: a model (or the Bernoulli oracle) + a pipeline split."""
 
@@ -154,7 +147,8 @@ class Engine:
     def _eesd_rows(self, horizon: int, gamma: int):
         return np.zeros((horizon * (2 * gamma + self.cfg.n_stages + 1) + 8, 6), dtype=np.int32)
 
-    def decode_eesd(self, prompt, horizon: int, gamma: int, trace: bool = True):
+    def decode_eesd(self, prompt, horizon: int, gamma: int, trace: bool = True, mode: str = "greedy",
+                    rng_seed: int = 0):
         L = _lib.lib()
         p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
         cap_tok = horizon + gamma + 1
@@ -162,10 +156,11 @@ class Engine:
         m = _lib.Metrics()
         rows = self._eesd_rows(horizon, gamma) if trace else None
         n_rows = C.c_int64(0)
-        _lib.check(L.ppsd_decode_eesd(self.h, gamma, p, len(prompt), horizon,
-                                      out.ctypes.data_as(C.POINTER(C.c_int32)), cap_tok, C.byref(m),
-                                      rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
-                                      rows.shape[0] if trace else 0, C.byref(n_rows)), "decode_eesd")
+        _lib.check(L.ppsd_decode_eesd_mode(self.h, gamma, int(mode == "greedy"), rng_seed & ((1 << 64) - 1), p,
+                                           len(prompt), horizon, out.ctypes.data_as(C.POINTER(C.c_int32)), cap_tok,
+                                           C.byref(m),
+                                           rows.ctypes.data_as(C.POINTER(_lib.TraceRowC)) if trace else None,
+                                           rows.shape[0] if trace else 0, C.byref(n_rows)), "decode_eesd")
         metrics, tr = self._eesd_result(m, rows, n_rows.value)
         return out[:metrics.committed_tokens].tolist(), metrics, tr
 
@@ -340,21 +335,24 @@ def simulate_eesd(cfg: PipelineConfig, gamma: int, oracle: AcceptanceOracle, hor
         m, tr = _bernoulli_engine(cfg).simulate_eesd(gamma, oracle.alpha, rng.split("verify").seed, horizon,
                                                       trace=trace is not None)
     else:
-        _greedy_only("greedy" if oracle.greedy else "sampling")
         lm = oracle.lm
         prompt = default_prompt(lm.vocab, rng)
-        _, m, tr = engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma, trace=trace is not None)
+        _, m, tr = engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma, trace=trace is not None,
+                                                   mode="greedy" if oracle.greedy else "sampling",
+                                                   rng_seed=rng.seed)
     if trace is not None:
         trace._rows.extend(tr.rows())
     return m
 
 
-def decode_eesd(lm, cfg: PipelineConfig, prompt: list[int], horizon: int, gamma: int
-                ) -> tuple[list[int], RunMetrics, EventTrace]:
+def decode_eesd(lm, cfg: PipelineConfig, prompt: list[int], horizon: int, gamma: int, mode: str = "greedy",
+                rng: RngStream | None = None) -> tuple[list[int], RunMetrics, EventTrace]:
     """EESD with an explicit prompt, returning the committed tokens as well
     (the baseline next to decode_ppsd / decode_autoregressive in bench tools)."""
+    _check_mode(mode)
     _check_prompt(lm, prompt)
     if cfg.n_layers != lm.n_layers:
         raise ValueError(f"pipeline is {cfg.n_layers} layers deep but the model has {lm.n_layers}")
     _require_draft_head(cfg)
-    return engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma)
+    return engine_for(lm, cfg).decode_eesd(prompt, horizon, gamma, mode=mode,
+                                           rng_seed=rng.seed if rng is not None else 0)

@@ -13,6 +13,7 @@ Fixture files:
   bernoulli.json      simulate_ppsd (traced machine + untraced fast path)
   acceptance200.json  the 200-case sweep of test_acceptance.py:133-154
   eesd_toy.json       simulate_eesd with the toy greedy oracle + Bernoulli
+  eesd_sampling.json  simulate_eesd with the toy sampling oracle
   transformer.json    reference decode_ppsd driving oracle/transformer.py
   cli_decode.json     `specpipe decode` transcripts (stdout, exit code)
   cli_harness.json    `specpipe analytic|run|sweep|trace` transcripts (stdout,
@@ -224,6 +225,29 @@ def make_sampling():
     return out
 
 
+EESD_SAMPLING = [  # (lm seed, beta, cfg kwargs, gamma, horizon)
+    (1, 1.0, dict(n_layers=32, exit_depth=8), 3, 80),
+    (2, 0.5, dict(n_layers=32, exit_depth=8), 5, 100),
+    (3, 2.0, dict(n_layers=32, exit_depth=8), 8, 64),
+    (4, 1.0, dict(n_layers=32, exit_depth=8, exit_stage=2), 4, 60),
+    (5, 0.8, dict(n_layers=33, exit_depth=8, comm_latency=1), 6, 70),
+    (6, 0.0, dict(n_layers=16, exit_depth=4), 5, 50),
+]
+
+
+def make_eesd_sampling():
+    out = []
+    for seed, beta, cfgkw, gamma, horizon in EESD_SAMPLING:
+        lm = sp.ToyLM(n_layers=cfgkw["n_layers"], vocab=16, seed=sp.derive_seed(seed, "lm"), misalignment=beta)
+        tr = EventTrace()
+        m = sp.simulate_eesd(sp.PipelineConfig(**cfgkw), gamma, sp.AcceptanceOracle.toylm_sampling(lm), horizon,
+                             run_rng(seed), trace=tr)
+        out.append(dict(lm_seed=lm.seed, n_layers=cfgkw["n_layers"], vocab=16, beta=beta, cfg=cfgkw, gamma=gamma,
+                        horizon=horizon, rng_seed=run_rng(seed).seed, metrics=metrics_list(m),
+                        trace_csv=trace_text(tr)))
+    return out
+
+
 HARNESS_RUNS = [
     dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=128, oracle="bernoulli", alpha=0.7, seed=1),
     dict(regime="ppsd", n_layers=32, exit_depth=8, horizon=96, oracle="toylm-greedy", beta=1.0, seed=2),
@@ -243,6 +267,8 @@ HARNESS_RUNS = [
          steady_state=True),
     dict(regime="ppsd", n_layers=16, exit_depth=4, horizon=64, oracle="toylm-greedy", beta=0.0, vocab=64,
          seed=11),
+    dict(regime="eesd", n_layers=32, exit_depth=8, horizon=80, gamma=4, oracle="toylm-sampling", beta=0.7,
+         seed=12),
 ]
 HARNESS_BAD = [
     dict(regime="nope", n_layers=32, exit_depth=8, horizon=10),
@@ -359,12 +385,12 @@ def make_cli_harness():
 
 
 def main(argv):
-    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness", "cli", "clidec"}
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness", "cli", "clidec", "eesdsamp"}
     jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
             ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
             ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling),
             ("harness", "harness.json", make_harness), ("cli", "cli_harness.json", make_cli_harness),
-            ("clidec", "cli_decode.json", make_cli_decode)]
+            ("clidec", "cli_decode.json", make_cli_decode), ("eesdsamp", "eesd_sampling.json", make_eesd_sampling)]
     for key, fname, fn in jobs:
         if key in which:
             data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",

@@ -98,3 +98,42 @@ def test_transformer_sampling_folded_equals_pipelined():
     assert out["folded"] == out["pipelined"]
     assert 0 < out["folded"][1][2] < 60  # both verdict kinds occur
     assert ppsd.engine_for(lm, ppsd.PipelineConfig(8, 2, exit_stage=2)).schedule("sampling") == "pipelined"
+
+
+@pytest.mark.parametrize("case", load_golden("eesd_sampling.json"),
+                         ids=lambda c: f"g{c['gamma']}-s{c['cfg'].get('exit_stage', 1)}")
+def test_eesd_toy_sampling_matches_reference(case):
+    """simulate_eesd with a toy sampling oracle (pipesim.py:435-551 with
+    _ToyVerifier): drafts sampled from p, accept_draft / residual resample /
+    bonus from the verify and commit streams — metrics and trace bit-exact."""
+    lm = ppsd.ToyLM(case["n_layers"], case["vocab"], case["lm_seed"], case["beta"])
+    tr = ppsd.EventTrace()
+    m = ppsd.simulate_eesd(ppsd.PipelineConfig(**case["cfg"]), case["gamma"], ppsd.AcceptanceOracle.toylm_sampling(lm),
+                           case["horizon"], ppsd.RngStream(case["rng_seed"]), trace=tr)
+    assert _ml(m) == case["metrics"]
+    assert tr.to_csv() == case["trace_csv"]
+
+
+def test_transformer_eesd_sampling_first_token_law():
+    """Lossless sampling EESD on the transformer: the first committed token
+    follows the target q (accepted draft or residual resample)."""
+    config = ppsd.TransformerConfig(4, 256, 4, 4, 64, 704, 16, kv_dtype="fp32", max_ctx=128)
+    lm = ppsd.TransformerLM(config, seed=2, deep_scale=1.0, deep_from=2)
+    prompt = [3, 11, 7, 5]
+    cfg = ppsd.PipelineConfig(4, 2)
+    eng = ppsd.engine_for(lm, cfg)
+    eng.decode_ar(prompt, 1)
+    z = eng.read_logits(1).astype(np.float64)
+    q = np.exp(z - z.max())
+    q /= q.sum()
+    n = 3000
+    counts = np.zeros(config.vocab)
+    for i in range(n):
+        toks, _, _ = ppsd.decode_eesd(lm, cfg, prompt, 1, 3, mode="sampling",
+                                      rng=ppsd.RngStream(ppsd.derive_seed(i, "run")))
+        counts[toks[0]] += 1
+    tv = 0.5 * np.abs(counts / n - q).sum()
+    assert tv < 0.06, tv
+    a = ppsd.decode_eesd(lm, cfg, prompt, 30, 4, mode="sampling", rng=ppsd.RngStream(9))
+    b = ppsd.decode_eesd(lm, cfg, prompt, 30, 4, mode="sampling", rng=ppsd.RngStream(9))
+    assert a[0] == b[0] and a[2].to_csv() == b[2].to_csv()
