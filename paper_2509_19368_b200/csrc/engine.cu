@@ -137,7 +137,7 @@ extern "C" const char* ppsd_build_info(void) {
   return "libppsd sm_100a: tma-bulk gemv ring, split-K paged attention, device tick machine";
 }
 
-static int attn_grid(const ppsd_engine* e) { return 4 * e->num_sms; }
+static int attn_grid(const ppsd_engine* e) { return 8 * e->num_sms; }
 
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
