@@ -69,7 +69,22 @@ typedef struct {
   /* ToyLM (toylm.py:55-68) */
   uint64_t toy_seed;
   double toy_misalignment;
+  /* transformer exit head: 0 = norm head (exit RMSNorm + tied LM head);
+   * 1 = one decoder layer (ppsd_weights.exit_layer, its own KV cache) on the
+   * exit-layer state, then the norm head — the paper's main configuration
+   * (PAPER.md:404-408). Single-device engines only. */
+  int32_t exit_head_layer;
 } ppsd_model_desc;
+
+/* one decoder layer's weights (layouts as in ppsd_weights) */
+typedef struct {
+  const void* qkv;
+  const void* o;
+  const void* gu;
+  const void* down;
+  const float* attn_norm;
+  const float* mlp_norm;
+} ppsd_layer_weights;
 
 /* Transformer weights, device pointers in the engine's physical layout
  * (see DESIGN.md §"Data layout"): bf16 matrices row-major [rows][cols],
@@ -89,6 +104,7 @@ typedef struct {
   const float* const* mlp_norm;  /* [d] */
   const float* rope_cos;    /* [max_ctx][hd/2] */
   const float* rope_sin;
+  ppsd_layer_weights exit_layer;  /* exit_head_layer = 1: the exit head's decoder layer */
 } ppsd_weights;
 
 typedef struct {

@@ -28,7 +28,10 @@ bf16-representable, and identical on CPU and GPU. Layers >= deep_from have
 their residual writes (W_o, W_down) scaled by deep_scale: the misalignment
 knob of SURVEY.md §0.4 (the transformer analogue of ToyLM's β,
 `pkg/src/specpipe/toylm.py:10-13`). The exit head is a norm head: its own
-RMSNorm followed by the tied LM head.
+RMSNorm followed by the tied LM head — or, with `exit_head_at=kE`, one more
+decoder layer (init ids of layer index N, its own K/V per position) applied to
+the layer-kE state before that norm head: the exit head of the paper's main
+runs (PAPER.md:404-408).
 """
 
 from __future__ import annotations
@@ -114,7 +117,7 @@ def init_tensor(seed: int, tid: int, rows: int, cols: int, a32: np.float32,
 
 class Weights:
     def __init__(self, shape: ModelShape, seed: int, deep_scale: float = 1.0,
-                 deep_from: int | None = None, dtype=np.float64, threads: int = 8):
+                 deep_from: int | None = None, dtype=np.float64, threads: int = 8, head_layer: bool = False):
         s = shape
         self.shape = s
         deep_from = s.n_layers if deep_from is None else deep_from
@@ -134,6 +137,18 @@ class Weights:
                 wup=mk(layer_tid(layer, TID_WUP), s.ffn_dim, s.d_model, init_scale(s.d_model)),
                 wdown=mk(layer_tid(layer, TID_WDOWN), s.d_model, s.ffn_dim, init_scale(s.ffn_dim, ds)),
             ))
+        self.head = None
+        if head_layer:  # the exit head's decoder layer: layer index N, unscaled
+            n = s.n_layers
+            self.head = dict(
+                wq=mk(layer_tid(n, TID_WQ), qd, s.d_model, init_scale(s.d_model)),
+                wk=mk(layer_tid(n, TID_WK), kvd, s.d_model, init_scale(s.d_model)),
+                wv=mk(layer_tid(n, TID_WV), kvd, s.d_model, init_scale(s.d_model)),
+                wo=mk(layer_tid(n, TID_WO), s.d_model, qd, init_scale(qd)),
+                wgate=mk(layer_tid(n, TID_WGATE), s.ffn_dim, s.d_model, init_scale(s.d_model)),
+                wup=mk(layer_tid(n, TID_WUP), s.ffn_dim, s.d_model, init_scale(s.d_model)),
+                wdown=mk(layer_tid(n, TID_WDOWN), s.d_model, s.ffn_dim, init_scale(s.ffn_dim)),
+            )
         # norm weights are all ones (attn, mlp, final, exit)
 
 
@@ -146,12 +161,13 @@ def rope_tables(head_dim: int, theta: float, n_pos: int):
 
 
 class _Node:
-    __slots__ = ("parent", "tok", "pos", "kids", "k", "v", "hidden")
+    __slots__ = ("parent", "tok", "pos", "kids", "k", "v", "hidden", "kh", "vh", "head_hidden")
 
     def __init__(self, parent, tok, pos):
         self.parent, self.tok, self.pos = parent, tok, pos
         self.kids = {}
         self.k = self.v = self.hidden = None
+        self.kh = self.vh = self.head_hidden = None
 
 
 class _PState:
@@ -166,11 +182,14 @@ class TransformerOracle:
 
     def __init__(self, shape: ModelShape, seed: int = 0, deep_scale: float = 1.0,
                  deep_from: int | None = None, dtype=np.float64, max_ctx: int = 4096,
-                 threads: int = 8, weights: Weights | None = None, rope_fp32: bool = False):
+                 threads: int = 8, weights: Weights | None = None, rope_fp32: bool = False,
+                 exit_head_at: int | None = None):
         self.shape = shape
         self.n_layers, self.vocab = shape.n_layers, shape.vocab
         self.dtype = dtype
-        self.w = weights or Weights(shape, seed, deep_scale, deep_from, dtype, threads)
+        self.exit_head_at = exit_head_at
+        self.w = weights or Weights(shape, seed, deep_scale, deep_from, dtype, threads,
+                                    head_layer=exit_head_at is not None)
         cos, sin = rope_tables(shape.head_dim, shape.rope_theta, max_ctx)
         if rope_fp32:
             cos, sin = cos.astype(np.float32), sin.astype(np.float32)
@@ -180,6 +199,8 @@ class TransformerOracle:
         self._K = np.zeros((L, max_ctx, kvh, hd), dtype)
         self._V = np.zeros((L, max_ctx, kvh, hd), dtype)
         self._owner = [None] * max_ctx  # node currently materialised at each position
+        self._KH = np.zeros((max_ctx, kvh, hd), dtype)  # exit-head layer K/V
+        self._VH = np.zeros((max_ctx, kvh, hd), dtype)
         self.margins = {"exit": math.inf, "final": math.inf}
 
     # ---- protocol --------------------------------------------------------
@@ -223,6 +244,9 @@ class TransformerOracle:
 
     def exit_logits(self, node, layer: int) -> np.ndarray:
         self._ensure(node)
+        if self.exit_head_at is not None:
+            assert layer == self.exit_head_at, (layer, self.exit_head_at)
+            return self.w.lm_head @ self._rms(node.head_hidden)
         return self.w.lm_head @ self._rms(node.hidden[layer])
 
     def logits_for_prefix(self, tokens, layer=None):
@@ -262,13 +286,54 @@ class TransformerOracle:
         for a in fix:
             self._K[:, a.pos] = a.k
             self._V[:, a.pos] = a.v
+            if a.kh is not None:
+                self._KH[a.pos] = a.kh
+                self._VH[a.pos] = a.vh
             self._owner[a.pos] = a
         self._forward(path)
 
-    def _forward(self, path):
-        s, w = self.shape, self.w
+    def _layer(self, x, lw, Kst, Vst, p0, P, cos, sin):
+        """One decoder layer on the path rows x [P, d] at positions p0..; K/V
+        rows of the path go into Kst/Vst [pos, KV, hd] (the layer's cache)."""
+        s = self.shape
         H, KV, hd = s.n_heads, s.n_kv_heads, s.head_dim
         rep = H // KV
+        half = hd // 2
+        scale = 1.0 / math.sqrt(hd)
+        h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + s.rms_eps)
+        q = (h @ lw["wq"].T).reshape(P, H, hd)
+        k = (h @ lw["wk"].T).reshape(P, KV, hd)
+        v = (h @ lw["wv"].T).reshape(P, KV, hd)
+        q = np.concatenate([q[..., :half] * cos - q[..., half:] * sin,
+                            q[..., half:] * cos + q[..., :half] * sin], axis=-1)
+        k = np.concatenate([k[..., :half] * cos - k[..., half:] * sin,
+                            k[..., half:] * cos + k[..., :half] * sin], axis=-1)
+        Kst[p0:p0 + P] = k
+        Vst[p0:p0 + P] = v
+        Kc = Kst[:p0 + P]  # [T, KV, hd]
+        Vc = Vst[:p0 + P]
+        causal = np.tril(np.ones((P, P), bool))
+        o = np.empty((P, H, hd), self.dtype)
+        for hh in range(H):
+            kh = hh // rep
+            sc = (q[:, hh, :] @ Kc[:, kh, :].T) * scale  # [P, T]
+            if P > 1:
+                mask = np.ones((P, p0 + P), bool)
+                mask[:, p0:] = causal
+                sc = np.where(mask, sc, -np.inf)
+            sc = sc - sc.max(axis=1, keepdims=True)
+            e = np.exp(sc)
+            o[:, hh, :] = (e @ Vc[:, kh, :]) / e.sum(axis=1, keepdims=True)
+        x = x + o.reshape(P, H * hd) @ lw["wo"].T
+        h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + s.rms_eps)
+        g = h @ lw["wgate"].T
+        u = h @ lw["wup"].T
+        a = g / (1.0 + np.exp(-g)) * u
+        return x + a @ lw["wdown"].T, k, v
+
+    def _forward(self, path):
+        s, w = self.shape, self.w
+        KV, hd = s.n_kv_heads, s.head_dim
         p0 = path[0].pos
         P = len(path)
         pos = np.arange(p0, p0 + P)
@@ -277,44 +342,17 @@ class TransformerOracle:
         ks = np.empty((s.n_layers, P, KV, hd), self.dtype)
         vs = np.empty_like(ks)
         cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
-        half = hd // 2
-        scale = 1.0 / math.sqrt(hd)
-        causal = np.tril(np.ones((P, P), bool))
         for li, lw in enumerate(w.layers):
-            h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + s.rms_eps)
-            q = (h @ lw["wq"].T).reshape(P, H, hd)
-            k = (h @ lw["wk"].T).reshape(P, KV, hd)
-            v = (h @ lw["wv"].T).reshape(P, KV, hd)
-            q = np.concatenate([q[..., :half] * cos - q[..., half:] * sin,
-                                q[..., half:] * cos + q[..., :half] * sin], axis=-1)
-            k = np.concatenate([k[..., :half] * cos - k[..., half:] * sin,
-                                k[..., half:] * cos + k[..., :half] * sin], axis=-1)
-            ks[li], vs[li] = k, v
-            self._K[li, p0:p0 + P] = k
-            self._V[li, p0:p0 + P] = v
-            Kc = self._K[li, :p0 + P]  # [T, KV, hd]
-            Vc = self._V[li, :p0 + P]
-            o = np.empty((P, H, hd), self.dtype)
-            for hh in range(H):
-                kh = hh // rep
-                sc = (q[:, hh, :] @ Kc[:, kh, :].T) * scale  # [P, T]
-                if P > 1:
-                    mask = np.ones((P, p0 + P), bool)
-                    mask[:, p0:] = causal
-                    sc = np.where(mask, sc, -np.inf)
-                sc = sc - sc.max(axis=1, keepdims=True)
-                e = np.exp(sc)
-                o[:, hh, :] = (e @ Vc[:, kh, :]) / e.sum(axis=1, keepdims=True)
-            x = x + o.reshape(P, H * hd) @ lw["wo"].T
-            h = x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + s.rms_eps)
-            g = h @ lw["wgate"].T
-            u = h @ lw["wup"].T
-            a = g / (1.0 + np.exp(-g)) * u
-            x = x + a @ lw["wdown"].T
+            x, ks[li], vs[li] = self._layer(x, lw, self._K[li], self._V[li], p0, P, cos, sin)
             hid.append(x.copy())
+        head = None
+        if self.exit_head_at is not None:  # the exit head's layer on the layer-kE states
+            head, kh, vh = self._layer(hid[self.exit_head_at].copy(), w.head, self._KH, self._VH, p0, P, cos, sin)
         for i, n in enumerate(path):
             n.k, n.v = ks[:, i].copy(), vs[:, i].copy()
             n.hidden = [hl[i] for hl in hid]
+            if head is not None:
+                n.kh, n.vh, n.head_hidden = kh[i].copy(), vh[i].copy(), head[i]
             self._owner[n.pos] = n
 
 

@@ -27,8 +27,13 @@ class ModelDesc(C.Structure):
         ("head_dim", C.c_int32), ("ffn_dim", C.c_int32),
         ("rms_eps", C.c_float), ("rope_theta", C.c_float),
         ("kv_bf16", C.c_int32), ("max_ctx", C.c_int32),
-        ("toy_seed", C.c_uint64), ("toy_misalignment", C.c_double),
+        ("toy_seed", C.c_uint64), ("toy_misalignment", C.c_double), ("exit_head_layer", C.c_int32),
     ]
+
+
+class LayerWeights(C.Structure):
+    _fields_ = [("qkv", C.c_void_p), ("o", C.c_void_p), ("gu", C.c_void_p), ("down", C.c_void_p),
+                ("attn_norm", C.c_void_p), ("mlp_norm", C.c_void_p)]
 
 
 class Weights(C.Structure):
@@ -38,7 +43,7 @@ class Weights(C.Structure):
         ("w_qkv", C.POINTER(C.c_void_p)), ("w_o", C.POINTER(C.c_void_p)),
         ("w_gu", C.POINTER(C.c_void_p)), ("w_down", C.POINTER(C.c_void_p)),
         ("attn_norm", C.POINTER(C.c_void_p)), ("mlp_norm", C.POINTER(C.c_void_p)),
-        ("rope_cos", C.c_void_p), ("rope_sin", C.c_void_p),
+        ("rope_cos", C.c_void_p), ("rope_sin", C.c_void_p), ("exit_layer", LayerWeights),
     ]
 
 

@@ -173,6 +173,18 @@ __global__ void eesd_draft_begin_kernel(const TickCtx* ctxp, EesdState* es) {
     w->nl[0] = es->exit_layer;
     w->head_slot[0] = s_done ? -1 : 0;
     w->head_slot[1] = -1;
+    if (c.hl) {  // exit-head layer on a copy of the draft's exit state
+      Work* wh = c.work_head;
+      wh->G = 1;
+      wh->slot[0] = s_done ? -1 : c.head_row;
+      wh->src_slot = 0;
+      wh->pos[0] = s_j;
+      wh->first[0] = c.hl_layer;
+      wh->nl[0] = 1;
+      wh->nv[0] = 1;
+      wh->head_slot[0] = wh->head_slot[1] = -1;
+      w->head_slot[0] = s_done ? -1 : c.head_row;
+    }
   }
   __syncthreads();
   if (s_done) return;

@@ -60,6 +60,9 @@ struct ppsd_engine {
   Work* d_work = nullptr;
   Work* d_work_ar = nullptr;
   Work* d_work_deep = nullptr;  // folded schedule: the deep batch
+  Work* d_work_head = nullptr;  // exit-head layer (md.exit_head_layer)
+  Work* d_work_p2 = nullptr;    // prefill: layers after the exit (exit-head layer)
+  bool hl = false;              // exit head has a decoder layer
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
   int32_t* d_tokens = nullptr;
@@ -253,6 +256,17 @@ static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
   return n;
 }
 
+// Exit-head layer: copy the drafting chain's exit state into the head rows,
+// then run the head's decoder layer on the copies (prefill: the whole chunk,
+// tcgen05 when planned). Returns launches enqueued, or -1.
+static int enqueue_head_layer(ppsd_engine* e, bool prefill) {
+  if (launch_pdl(head_copy_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
+                 (const Work*)e->d_work_head) != cudaSuccess)
+    return -1;
+  const int m = prefill ? enqueue_prefill_layers(e, e->d_work_head, 1) : enqueue_layers(e, e->d_work_head, 1, false);
+  return m < 0 ? -1 : m + 1;
+}
+
 template <class F>
 static int capture(ppsd_engine* e, F body, cudaGraphExec_t* out, int64_t* nlaunch) {
   cudaGraph_t g = nullptr;
@@ -300,6 +314,11 @@ static int build_fold_graph(ppsd_engine* e) {
   if (ok) {
     const int m = enqueue_layers(e, e->d_work, shallow, false);
     need(m >= 0, "shallow layers");
+    n_outer += m;
+  }
+  if (ok && e->hl) {
+    const int m = enqueue_head_layer(e, false);
+    need(m >= 0, "exit-head layer");
     n_outer += m;
   }
   need(ok && enqueue_gemv(e, e->d_work, 0, kMatHead) == cudaSuccess, "exit head");
@@ -383,6 +402,11 @@ static int build_graphs(ppsd_engine* e) {
           int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
           n += m;
+          if (e->hl) {  // exit-head layer on a copy of the exit chain's state
+            m = enqueue_head_layer(e, false);
+            if (m < 0) return -1;
+            n += m;
+          }
           if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
           n += 1;
         } else if (kind == PPSD_MODEL_TOYLM) {
@@ -420,8 +444,20 @@ static int build_graphs(ppsd_engine* e) {
         if (launch_pdl(prefill_chunk_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
                        e->d_arctl) != cudaSuccess)
           return -1;
-        int m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
-        if (m < 0) return -1;
+        int m;
+        if (e->hl) {  // [0, split), head layer on copies of the chunk, [split, N)
+          const int split = e->h_ctx.hl_split;
+          m = enqueue_prefill_layers(e, e->d_work_ar, split);
+          if (m < 0) return -1;
+          const int mh = enqueue_head_layer(e, true);
+          if (mh < 0) return -1;
+          const int m2 = enqueue_prefill_layers(e, e->d_work_p2, e->n_local_layers - split);
+          if (m2 < 0) return -1;
+          m += mh + m2;
+        } else {
+          m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
+          if (m < 0) return -1;
+        }
         return m + 1;
       },
       &e->g_prefill, &e->prefill_launches);
@@ -484,7 +520,7 @@ static int setup_umma(ppsd_engine* e, const int (*shapes)[2]) {
   if (env && atoi(env) == 0) return PPSD_OK;
   for (int m = kMatQKV; m <= kMatDown; ++m)
     if (!umma_shape_ok(shapes[m][0], shapes[m][1])) return PPSD_OK;
-  const int L = e->md.n_layers;
+  const int L = (int)e->h_layers.size();  // + the exit-head layer
   const size_t mb = umma_map_bytes();
   std::vector<unsigned char> maps((size_t)L * 4 * mb, 0);
   for (int l = 0; l < L; ++l) {
@@ -553,6 +589,8 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   CU(dalloc(&e->d_work, sizeof(Work)));
   CU(dalloc(&e->d_work_ar, sizeof(Work)));
   CU(dalloc(&e->d_work_deep, sizeof(Work)));
+  CU(dalloc(&e->d_work_head, sizeof(Work)));
+  CU(dalloc(&e->d_work_p2, sizeof(Work)));
   CU(dalloc(&e->d_ctx, sizeof(TickCtx)));
   CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
   CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
@@ -564,6 +602,8 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.work = e->d_work;
   c.work_ar = e->d_work_ar;
   c.work_deep = e->d_work_deep;
+  c.work_head = e->d_work_head;
+  c.work_p2 = e->d_work_p2;
   c.tokens = e->d_tokens;
   c.model = md->kind;
   c.lo = e->lo;
@@ -635,12 +675,27 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     e->max_pages = (max_ctx + kPage - 1) / kPage;
     const size_t esz = d.kv_bf16 ? 2 : 4;
     const size_t per_layer = (size_t)e->max_pages * kPage * d.KV * d.hd * esz;
-    CU(cudaMalloc(&e->d_kv, per_layer * 2 * e->n_local_layers));
+    // exit-head layer: one more decoder layer (global index N) with its own KV
+    // (after the local layers in the pool) and activation rows from nbuf on
+    e->hl = md->exit_head_layer != 0;
+    if (e->hl) {
+      if (e->lo != 1 || e->hi != e->S)
+        return fail(PPSD_EUNSUPPORTED, "the exit-head layer needs every stage on one device");
+      const ppsd_layer_weights& X = w->exit_layer;
+      if (!X.qkv || !X.o || !X.gu || !X.down || !X.attn_norm || !X.mlp_norm)
+        return fail(PPSD_EINVAL, "missing exit-head layer weights");
+      c.hl = 1;
+      c.hl_layer = md->n_layers;
+      c.hl_split = e->cfg.shallow_layers;
+      c.head_row = e->nbuf;
+    }
+    const int kv_layers = e->n_local_layers + (e->hl ? 1 : 0);
+    CU(cudaMalloc(&e->d_kv, per_layer * 2 * kv_layers));
     std::vector<int32_t> pt(e->max_pages);
     for (int i = 0; i < e->max_pages; ++i) pt[i] = i;
     CU(dalloc(&e->d_page_table, sizeof(int32_t) * e->max_pages));
     CU(cudaMemcpy(e->d_page_table, pt.data(), sizeof(int32_t) * e->max_pages, cudaMemcpyHostToDevice));
-    e->h_layers.assign(md->n_layers, LayerW{});
+    e->h_layers.assign(md->n_layers + (e->hl ? 1 : 0), LayerW{});
     for (int l = 0; l < md->n_layers; ++l) {
       LayerW& L = e->h_layers[l];
       const int li = l - e->first_local_layer;
@@ -656,10 +711,23 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       L.kc = static_cast<char*>(e->d_kv) + per_layer * (2 * li);
       L.vc = static_cast<char*>(e->d_kv) + per_layer * (2 * li + 1);
     }
-    CU(dalloc(&e->d_layers, sizeof(LayerW) * md->n_layers));
-    CU(cudaMemcpy(e->d_layers, e->h_layers.data(), sizeof(LayerW) * md->n_layers, cudaMemcpyHostToDevice));
+    if (e->hl) {
+      LayerW& L = e->h_layers[md->n_layers];
+      const ppsd_layer_weights& X = w->exit_layer;
+      L.qkv = reinterpret_cast<const __nv_bfloat16*>(X.qkv);
+      L.o = reinterpret_cast<const __nv_bfloat16*>(X.o);
+      L.gu = reinterpret_cast<const __nv_bfloat16*>(X.gu);
+      L.down = reinterpret_cast<const __nv_bfloat16*>(X.down);
+      L.attn_norm = X.attn_norm;
+      L.mlp_norm = X.mlp_norm;
+      L.kc = static_cast<char*>(e->d_kv) + per_layer * (2 * e->n_local_layers);
+      L.vc = static_cast<char*>(e->d_kv) + per_layer * (2 * e->n_local_layers + 1);
+    }
+    CU(dalloc(&e->d_layers, sizeof(LayerW) * e->h_layers.size()));
+    CU(cudaMemcpy(e->d_layers, e->h_layers.data(), sizeof(LayerW) * e->h_layers.size(), cudaMemcpyHostToDevice));
     const int qd = d.H * d.hd;
-    const size_t nb = (size_t)e->nbuf;
+    // rows: chains / prefill chunk [0, nbuf); exit-head layer copies [nbuf, 2*nbuf)
+    const size_t nb = (size_t)e->nbuf * (e->hl ? 2 : 1);
     CU(dalloc(&e->d_x, sizeof(float) * nb * d.d));
     CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
@@ -1089,9 +1157,11 @@ static int eesd_graph(ppsd_engine* e, int gamma, cudaGraphExec_t* out, int64_t* 
           if (launch_pdl(eesd_draft_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
           const int m = enqueue_layers(e, e->d_work_ar, exit_layer, false);
           if (m < 0) return -1;
+          const int mh = e->hl ? enqueue_head_layer(e, false) : 0;  // exit-head layer on a copy
+          if (mh < 0) return -1;
           if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
           if (launch_pdl(eesd_draft_end_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
-          cnt += m + 3;
+          cnt += m + mh + 3;
         }
         if (launch_pdl(eesd_verify_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
         const int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);  // batched verify

@@ -57,6 +57,15 @@ struct TickCtx {
   Work* work_deep;
   unsigned long long cond;  // cudaGraphConditionalHandle of the folded tick graph
   int32_t has_cond;         // 0: deep part captured inline (PPSD_FOLD_COND=0, profiling)
+  // transformer-layer exit head (ppsd_model_desc.exit_head_layer): the draft
+  // is the norm head on that decoder layer's output for a COPY of the
+  // exit-layer state (rows head_row..), so the chain's own state continues
+  int32_t hl;               // 1: exit head has a decoder layer
+  int32_t hl_layer;         // its global layer index (= n_layers)
+  int32_t hl_split;         // layers before the exit (k*E): prefill runs [0, split), head, [split, N)
+  int32_t head_row;         // first activation row of the head layer
+  Work* work_head;          // the head layer's work (copy source in src_slot)
+  Work* work_p2;            // prefill: layers [split, N) of the chunk
 };
 
 constexpr int kBoxHeader = 4;
@@ -80,6 +89,7 @@ struct EesdState {
 };
 
 __global__ void sched_tick_kernel(const TickCtx* ctxp, int begin);
+__global__ void head_copy_kernel(const TickCtx* ctxp, const Work* wh);
 __global__ void ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void toy_tick_kernel(const TickCtx* ctxp);

@@ -26,6 +26,7 @@ struct Work {
   int32_t head_slot[2];         // [0] exit head input slot, [1] final head input slot
   int32_t head_out[2];          // argmax written by the head kernel
   int32_t vec_out[kMaxVec];     // kMatHeadV: argmax of each vector of group 0 (final head)
+  int32_t src_slot;             // exit-head layer (head_copy_kernel): first row copied into slot[0]
 };
 
 struct LayerW {

@@ -191,6 +191,18 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       wd->nv[0] = s.fold_nb > 0 ? s.fold_nb : 1;
       wd->head_slot[0] = wd->head_slot[1] = -1;
       if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
+      if (c.hl) {  // exit-head layer on a copy of the launched chain's exit state
+        Work* wh = c.work_head;
+        wh->G = 1;
+        wh->slot[0] = row >= 0 ? c.head_row : -1;
+        wh->src_slot = row;
+        wh->pos[0] = w->pos[0];
+        wh->first[0] = c.hl_layer;
+        wh->nl[0] = 1;
+        wh->nv[0] = 1;
+        wh->head_slot[0] = wh->head_slot[1] = -1;
+        w->head_slot[0] = row >= 0 ? c.head_row : -1;
+      }
       s_launch_slot = row;
       s_launch_pos = row >= 0 ? s.ch_pos[s.work[1]] : 0;
     } else {
@@ -206,6 +218,19 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       }
       w->head_slot[0] = (s.c.k >= c.lo && s.c.k <= c.hi) ? s.exit_slot : -1;
       w->head_slot[1] = (s.c.S >= c.lo && s.c.S <= c.hi) ? s.final_slot : -1;
+      if (c.hl) {  // exit-head layer on a copy of the exit chain's state (single device)
+        Work* wh = c.work_head;
+        const int ex = w->head_slot[0];
+        wh->G = 1;
+        wh->slot[0] = ex >= 0 ? c.head_row : -1;
+        wh->src_slot = ex;
+        wh->pos[0] = ex >= 0 ? s.c.n_prompt + s.ch_pos[ex] - 2 : 0;
+        wh->first[0] = c.hl_layer;
+        wh->nl[0] = 1;
+        wh->nv[0] = 1;
+        wh->head_slot[0] = wh->head_slot[1] = -1;
+        w->head_slot[0] = ex >= 0 ? c.head_row : -1;
+      }
       s_launch_slot = (s.launched && c.lo == 1) ? s.work[1] : -1;
       s_launch_pos = s_launch_slot >= 0 ? s.ch_pos[s_launch_slot] : 0;
     }
@@ -309,6 +334,22 @@ __global__ void __launch_bounds__(256) prefill_chunk_kernel(const TickCtx* ctxp,
     w->first[0] = ctl->first_layer;
     w->nl[0] = ctl->n_layers;
     w->head_slot[0] = w->head_slot[1] = -1;
+    if (c.hl) {  // [0, split) -> head layer on copies -> [split, N)
+      w->nl[0] = c.hl_split;
+      Work* wh = c.work_head;
+      wh->G = 1;
+      wh->slot[0] = n > 0 ? c.head_row : -1;
+      wh->src_slot = 0;
+      wh->nv[0] = n > 0 ? n : 1;
+      wh->pos[0] = j0;
+      wh->first[0] = c.hl_layer;
+      wh->nl[0] = 1;
+      wh->head_slot[0] = wh->head_slot[1] = -1;
+      Work* w2 = c.work_p2;
+      *w2 = *w;
+      w2->first[0] = ctl->first_layer + c.hl_split;
+      w2->nl[0] = ctl->n_layers - c.hl_split;
+    }
     ctl->j = j0 + (n > 0 ? n : 0);
     s_j0 = j0;
     s_n = n;
@@ -353,6 +394,22 @@ __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head) {
   if (threadIdx.x == 0) {
     if (with_head) c.tokens[j + 1] = tok;
     ctl->j = j + 1;
+  }
+}
+
+// Exit-head layer input: rows slot[0] .. +nv of `wh` = rows src_slot .. (the
+// exit-layer state of the drafting chain(s)); the head layer then runs on the
+// copies in place and the chains' own rows continue unchanged.
+__global__ void __launch_bounds__(256) head_copy_kernel(const TickCtx* ctxp, const Work* wh) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  const int dst = wh->slot[0], src = wh->src_slot, nv = wh->nv[0];
+  if (dst < 0 || src < 0) return;
+  for (int v = 0; v < nv; ++v) {
+    const float4* a = reinterpret_cast<const float4*>(c.x + (size_t)(src + v) * c.d);
+    float4* b = reinterpret_cast<float4*>(c.x + (size_t)(dst + v) * c.d);
+    for (int i = threadIdx.x; i < c.d / 4; i += blockDim.x) b[i] = a[i];
   }
 }
 

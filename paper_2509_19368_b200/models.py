@@ -167,10 +167,13 @@ class TransformerLM:
 
     def __init__(self, config: TransformerConfig, seed: int = 0, deep_scale: float = 1.0,
                  deep_from: int | None = None, device=None, layers: tuple[int, int] | None = None,
-                 need_embed: bool = True, need_head: bool = True):
+                 need_embed: bool = True, need_head: bool = True, exit_head: str = "norm"):
         import torch
 
+        if exit_head not in ("norm", "layer"):
+            raise ValueError(f"exit_head must be 'norm' or 'layer', got {exit_head!r}")
         self.config = config
+        self.exit_head = exit_head
         self.n_layers, self.vocab = config.n_layers, config.vocab
         self.seed, self.deep_scale = seed, float(deep_scale)
         self.deep_from = config.n_layers if deep_from is None else deep_from
@@ -217,13 +220,26 @@ class TransformerLM:
                 self.w_down[layer] = init(c.d_model, c.ffn_dim, 0, [layer_tid(layer, TID_WDOWN)],
                                           [init_scale(c.ffn_dim, ds)])
                 self.attn_norm[layer], self.mlp_norm[layer] = ones(), ones()
+            self.exit_layer_w = None
+            if exit_head == "layer":  # the exit head's decoder layer: layer index N in the init ids
+                n = c.n_layers
+                self.exit_layer_w = dict(
+                    qkv=init(qd + 2 * kvd, c.d_model, 1,
+                             [layer_tid(n, TID_WQ), layer_tid(n, TID_WK), layer_tid(n, TID_WV)], [s_d, s_d, s_d]),
+                    o=init(c.d_model, qd, 0, [layer_tid(n, TID_WO)], [init_scale(qd)]),
+                    gu=init(2 * c.ffn_dim, c.d_model, 2, [layer_tid(n, TID_WGATE), layer_tid(n, TID_WUP)],
+                            [s_d, s_d]),
+                    down=init(c.d_model, c.ffn_dim, 0, [layer_tid(n, TID_WDOWN)], [init_scale(c.ffn_dim)]),
+                    attn_norm=ones(), mlp_norm=ones())
             cos, sin = rope_tables(c.head_dim, c.rope_theta, c.max_ctx)
             self.rope_cos = torch.from_numpy(cos).to(dev)
             self.rope_sin = torch.from_numpy(sin).to(dev)
             torch.cuda.synchronize(dev)
 
     def model_desc(self, max_ctx: int | None = None) -> _lib.ModelDesc:
-        return self.config.to_desc()
+        d = self.config.to_desc()
+        d.exit_head_layer = int(self.exit_head == "layer")
+        return d
 
     def weights_struct(self) -> _lib.Weights:
         n = self.config.n_layers
@@ -234,12 +250,17 @@ class TransformerLM:
             self._keep.append(a)
             return a
 
+        xl = _lib.LayerWeights()
+        if self.exit_layer_w is not None:
+            X = self.exit_layer_w
+            xl = _lib.LayerWeights(qkv=ptr(X["qkv"]), o=ptr(X["o"]), gu=ptr(X["gu"]), down=ptr(X["down"]),
+                                   attn_norm=ptr(X["attn_norm"]), mlp_norm=ptr(X["mlp_norm"]))
         return _lib.Weights(embed=ptr(self.embed), lm_head=ptr(self.lm_head),
                             final_norm=ptr(self.final_norm), exit_norm=ptr(self.exit_norm),
                             w_qkv=arr(self.w_qkv), w_o=arr(self.w_o), w_gu=arr(self.w_gu),
                             w_down=arr(self.w_down), attn_norm=arr(self.attn_norm),
                             mlp_norm=arr(self.mlp_norm), rope_cos=ptr(self.rope_cos),
-                            rope_sin=ptr(self.rope_sin))
+                            rope_sin=ptr(self.rope_sin), exit_layer=xl)
 
     def weight_bytes(self) -> int:
         lo, hi = self.layer_range

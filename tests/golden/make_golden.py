@@ -15,6 +15,7 @@ Fixture files:
   eesd_toy.json       simulate_eesd with the toy greedy oracle + Bernoulli
   eesd_sampling.json  simulate_eesd with the toy sampling oracle
   transformer.json    reference decode_ppsd driving oracle/transformer.py
+  transformer_head.json  the same with a decoder-layer exit head (exit_head_at)
   cli_decode.json     `specpipe decode` transcripts (stdout, exit code)
   cli_harness.json    `specpipe analytic|run|sweep|trace` transcripts (stdout,
                       stderr, exit code)
@@ -183,6 +184,33 @@ def make_transformer():
                         cfg=cfgkw, prompt=prompt, max_tokens=n_tok, tokens=toks,
                         metrics=metrics_list(m), trace_csv=trace_text(tr),
                         min_margins=lm.margin_report()))
+        print(name, metrics_list(m), flush=True)
+    return out
+
+
+def make_transformer_head():
+    """As make_transformer, with the exit head of the paper's main runs: one
+    decoder layer on the exit-layer state, then the norm head."""
+    from oracle.transformer import TransformerOracle, tiny_config
+
+    out = []
+    for name, deep_scale, cfgkw, n_tok, seed in (
+        ("tiny_hl_ds010", 0.10, dict(n_layers=32, exit_depth=8), 96, 5),
+        ("tiny_hl_ds030", 0.30, dict(n_layers=32, exit_depth=8), 96, 6),
+        ("tiny_hl_deep_exit", 0.15, dict(n_layers=32, exit_depth=8, exit_stage=2), 64, 7),
+        ("tiny_hl_comm_lat", 0.20, dict(n_layers=32, exit_depth=8, comm_latency=1), 64, 8),
+    ):
+        mc = tiny_config()
+        cfg = sp.PipelineConfig(**cfgkw)
+        lm = TransformerOracle(mc, seed=seed, deep_scale=deep_scale, deep_from=8, dtype=np.float64,
+                               exit_head_at=cfg.exit_layer)
+        prompt = sp.default_prompt(mc.vocab, run_rng(seed))
+        toks, m, tr = sp.decode_ppsd(lm, cfg, prompt, n_tok, "greedy", run_rng(seed))
+        ar = sp.decode_autoregressive(lm, prompt, n_tok, "greedy", run_rng(seed))
+        assert toks == ar, name
+        out.append(dict(name=name, model=mc.to_dict(), seed=seed, deep_scale=deep_scale, deep_from=8,
+                        cfg=cfgkw, prompt=prompt, max_tokens=n_tok, tokens=toks, exit_head="layer",
+                        metrics=metrics_list(m), trace_csv=trace_text(tr), min_margins=lm.margin_report()))
         print(name, metrics_list(m), flush=True)
     return out
 
@@ -385,12 +413,14 @@ def make_cli_harness():
 
 
 def main(argv):
-    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness", "cli", "clidec", "eesdsamp"}
+    which = set(argv[1:]) or {"toy", "bern", "acc", "eesd", "tf", "samp", "harness", "cli", "clidec", "eesdsamp",
+                              "tfhead"}
     jobs = [("toy", "toylm_decode.json", make_toy), ("bern", "bernoulli.json", make_bernoulli),
             ("acc", "acceptance200.json", make_acceptance200), ("eesd", "eesd_toy.json", make_eesd),
             ("tf", "transformer.json", make_transformer), ("samp", "toylm_sampling.json", make_sampling),
             ("harness", "harness.json", make_harness), ("cli", "cli_harness.json", make_cli_harness),
-            ("clidec", "cli_decode.json", make_cli_decode), ("eesdsamp", "eesd_sampling.json", make_eesd_sampling)]
+            ("clidec", "cli_decode.json", make_cli_decode), ("eesdsamp", "eesd_sampling.json", make_eesd_sampling),
+            ("tfhead", "transformer_head.json", make_transformer_head)]
     for key, fname, fn in jobs:
         if key in which:
             data = dict(reference="specpipe " + sp.__version__, generator="tests/golden/make_golden.py",

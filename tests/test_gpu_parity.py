@@ -279,3 +279,47 @@ def test_folded_edge_cases():
         assert out["folded"][0] == ppsd.decode_autoregressive(lm, prompt, n, "greedy", ppsd.RngStream(0))
     with pytest.raises(ValueError):
         ppsd.decode_ppsd(lm, cfg, [1, 2], 200, "greedy", ppsd.RngStream(0))
+
+
+# ------------------------------------------------ decoder-layer exit head --
+
+@pytest.mark.parametrize("schedule", ["pipelined", "folded"])
+@pytest.mark.parametrize("case", load_golden("transformer_head.json"), ids=lambda c: c["name"])
+def test_head_layer_matches_reference_scheduler(case, schedule):
+    """Exit head = one decoder layer (own KV) + norm head, the paper's main
+    configuration: the reference decode_ppsd driving the fp64 oracle with that
+    head produced these tokens / counts / traces; the GPU matches exactly."""
+    lm = ppsd.TransformerLM(ppsd.TransformerConfig.tiny(), seed=case["seed"], deep_scale=case["deep_scale"],
+                            deep_from=case["deep_from"], exit_head="layer")
+    cfg = _cfg(case["cfg"])
+    lm.schedule = schedule
+    toks, m, tr = ppsd.decode_ppsd(lm, cfg, case["prompt"], case["max_tokens"], "greedy", ppsd.RngStream(0))
+    assert toks == case["tokens"]
+    assert _metrics_list(m) == case["metrics"]
+    assert tr.to_csv() == case["trace_csv"]
+
+
+@pytest.mark.parametrize("name", ["l7b_2layer", "mid_gqa"])
+def test_head_layer_lossless_and_schedules_agree(name):
+    """With the decoder-layer exit head: folded ≡ pipelined (tokens, metrics,
+    trace), PPSD ≡ AR and EESD ≡ AR token-for-token (the tcgen05 prefill also
+    fills the head layer's KV for the prompt)."""
+    sh = dict(SHAPES[name])
+    sh["n_layers"] = 8
+    config = ppsd.TransformerConfig(**sh, kv_dtype="bf16", max_ctx=512)
+    lm = ppsd.TransformerLM(config, seed=13, deep_scale=0.3, deep_from=2, exit_head="layer")
+    prompt = [int(t) for t in np.random.default_rng(3).integers(0, config.vocab, size=40)]
+    ar = ppsd.decode_autoregressive(lm, prompt, 64, "greedy", ppsd.RngStream(0))
+    for e, k, cl in ((2, 1, 0), (2, 2, 0), (4, 1, 1)):
+        cfg = ppsd.PipelineConfig(8, e, exit_stage=k, comm_latency=cl)
+        out = {}
+        for sched in ("pipelined", "folded"):
+            lm.schedule = sched
+            toks, m, tr = ppsd.decode_ppsd(lm, cfg, prompt, 64, "greedy", ppsd.RngStream(0))
+            out[sched] = (toks, _metrics_list(m), tr.to_csv())
+        lm.schedule = "auto"
+        assert out["folded"] == out["pipelined"], (e, k, cl)
+        assert out["folded"][0] == ar, (e, k, cl)
+        assert 0 < out["folded"][1][2] < 64  # accepts and rejects both occur
+    et, em, _ = ppsd.decode_eesd(lm, ppsd.PipelineConfig(8, 2), prompt, 64, 3)
+    assert et[:64] == ar
