@@ -29,11 +29,12 @@ def main():
     ap.add_argument("--gamma", type=int, default=0, help="also run EESD with this gamma")
     ap.add_argument("--out", default=None)
     ap.add_argument("--schedule", default="auto", choices=["auto", "pipelined", "folded"])
+    ap.add_argument("--exit-head", default="norm", choices=["norm", "layer"])
     args = ap.parse_args()
     config = {"7b": ppsd.TransformerConfig.llama2_7b, "13b": ppsd.TransformerConfig.llama2_13b,
               "70b": ppsd.TransformerConfig.llama2_70b}[args.model](max_ctx=args.prompt + args.tokens + 64)
     t0 = time.time()
-    lm = ppsd.TransformerLM(config, seed=0, deep_scale=args.deep_scale, deep_from=args.exit)
+    lm = ppsd.TransformerLM(config, seed=0, deep_scale=args.deep_scale, deep_from=args.exit, exit_head=args.exit_head)
     init_s = time.time() - t0
     cfg = ppsd.PipelineConfig(config.n_layers, args.exit)
     rng = ppsd.RngStream(ppsd.derive_seed(0, "run"))
@@ -61,7 +62,7 @@ def main():
     step_bytes = sum(cfg.stage_layers[r.stage - 1] for r in tr
                      if r.kind in ("ACTIVATION", "FINAL_TOKEN", "CHECK_TOKEN")) * config.layer_bytes() \
         + heads * config.head_bytes() + kv
-    row = dict(model=config.name, weights_gb=round((config.n_layers * config.layer_bytes() + 2 * config.head_bytes()) / 1e9, 2),
+    row = dict(model=config.name, exit_head=args.exit_head, weights_gb=round((config.n_layers * config.layer_bytes() + 2 * config.head_bytes()) / 1e9, 2),
                exit=args.exit, n_stages=cfg.n_stages, deep_scale=args.deep_scale, init_s=round(init_s, 1),
                alpha=m.alpha_all_measured, ticks=m.ticks, stage_forwards=fwd,
                schedule=pp["schedule"], ppsd_tok_s=round(args.tokens / pp["decode_ms"] * 1e3, 2),
