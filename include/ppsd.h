@@ -104,7 +104,7 @@ typedef struct {
   const float* const* mlp_norm;  /* [d] */
   const float* rope_cos;    /* [max_ctx][hd/2] */
   const float* rope_sin;
-  ppsd_layer_weights exit_layer;  /* exit_head_layer = 1: the exit head's decoder layer */
+  ppsd_layer_weights exit_layer;  /* exit_head_layer = 1: the exit head's decoder layer (exit stage's rank) */
 } ppsd_weights;
 
 typedef struct {

@@ -135,7 +135,8 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
     const int ctx = wpos(it.g) + it.vv + 1;
     const int n = min(kPage, ctx - it.c * kPage);
     // this layer's K / V caches: [k, v] per local layer, contiguous (engine.cu)
-    const int lloc = wfirst(it.g) + a.layer_i - a.first_local;
+    const int gl = wfirst(it.g) + a.layer_i;
+    const int lloc = gl == a.hl_global ? a.hl_local : gl - a.first_local;
     const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
     const int page = it.c < kStagePages ? S.st_page[it.c] : a.page_table[it.c];
     const size_t blk = ((size_t)page * KVh + it.kvh) * BLK;

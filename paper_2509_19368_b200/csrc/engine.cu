@@ -61,7 +61,8 @@ struct ppsd_engine {
   Work* d_work_ar = nullptr;
   Work* d_work_deep = nullptr;  // folded schedule: the deep batch
   Work* d_work_head = nullptr;  // exit-head layer (md.exit_head_layer)
-  Work* d_work_p2 = nullptr;    // prefill: layers after the exit (exit-head layer)
+  Work* d_work_p2 = nullptr;       // prefill: layers after the exit (exit-head layer)
+  Work* d_work_head_pf = nullptr;  // prefill's exit-head layer
   bool hl = false;              // exit head has a decoder layer
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
@@ -193,6 +194,8 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   a.kv_base = e->d_kv;
   a.kv_layer_bytes = (long long)e->max_pages * kPage * e->dm.KV * e->dm.hd * (e->dm.kv_bf16 ? 2 : 4);
   a.first_local = e->first_local_layer;
+  a.hl_global = e->hl ? e->md.n_layers : -1;
+  a.hl_local = e->n_local_layers;
   return attn_launch(a, attn_grid(e), e->st);
 }
 
@@ -260,10 +263,11 @@ static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
 // then run the head's decoder layer on the copies (prefill: the whole chunk,
 // tcgen05 when planned). Returns launches enqueued, or -1.
 static int enqueue_head_layer(ppsd_engine* e, bool prefill) {
-  if (launch_pdl(head_copy_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
-                 (const Work*)e->d_work_head) != cudaSuccess)
+  Work* wh = prefill ? e->d_work_head_pf : e->d_work_head;
+  if (launch_pdl(head_copy_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, (const Work*)wh) !=
+      cudaSuccess)
     return -1;
-  const int m = prefill ? enqueue_prefill_layers(e, e->d_work_head, 1) : enqueue_layers(e, e->d_work_head, 1, false);
+  const int m = prefill ? enqueue_prefill_layers(e, wh, 1) : enqueue_layers(e, wh, 1, false);
   return m < 0 ? -1 : m + 1;
 }
 
@@ -490,7 +494,8 @@ static void free_engine(ppsd_engine* e) {
                   (void*)e->d_umws, (void*)e->d_umcnt})
     if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
-  void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+  void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_work_head, e->d_work_p2,
+                  e->d_work_head_pf, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
                   e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
@@ -591,6 +596,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   CU(dalloc(&e->d_work_deep, sizeof(Work)));
   CU(dalloc(&e->d_work_head, sizeof(Work)));
   CU(dalloc(&e->d_work_p2, sizeof(Work)));
+  CU(dalloc(&e->d_work_head_pf, sizeof(Work)));
   CU(dalloc(&e->d_ctx, sizeof(TickCtx)));
   CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
   CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
@@ -604,6 +610,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.work_deep = e->d_work_deep;
   c.work_head = e->d_work_head;
   c.work_p2 = e->d_work_p2;
+  c.work_head_pf = e->d_work_head_pf;
   c.tokens = e->d_tokens;
   c.model = md->kind;
   c.lo = e->lo;
@@ -677,16 +684,16 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     const size_t per_layer = (size_t)e->max_pages * kPage * d.KV * d.hd * esz;
     // exit-head layer: one more decoder layer (global index N) with its own KV
     // (after the local layers in the pool) and activation rows from nbuf on
-    e->hl = md->exit_head_layer != 0;
+    // Across ranks only the rank that owns the exit stage k runs (and holds)
+    // the head layer; the replicated scheduler plans it there alone.
+    e->hl = md->exit_head_layer != 0 && e->cfg.k >= e->lo && e->cfg.k <= e->hi;
     if (e->hl) {
-      if (e->lo != 1 || e->hi != e->S)
-        return fail(PPSD_EUNSUPPORTED, "the exit-head layer needs every stage on one device");
       const ppsd_layer_weights& X = w->exit_layer;
       if (!X.qkv || !X.o || !X.gu || !X.down || !X.attn_norm || !X.mlp_norm)
         return fail(PPSD_EINVAL, "missing exit-head layer weights");
       c.hl = 1;
       c.hl_layer = md->n_layers;
-      c.hl_split = e->cfg.shallow_layers;
+      c.hl_split = e->cfg.shallow_layers - e->first_local_layer;  // local layers before the exit
       c.head_row = e->nbuf;
     }
     const int kv_layers = e->n_local_layers + (e->hl ? 1 : 0);
@@ -1405,6 +1412,11 @@ static int build_mr_graphs(ppsd_engine* e) {
       [&]() -> int {
         int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
         if (m < 0) return -1;
+        if (e->hl) {  // exit rank: head layer on a copy of the exit chain's state
+          const int mh = enqueue_head_layer(e, false);
+          if (mh < 0) return -1;
+          m += mh;
+        }
         if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
         if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
             cudaSuccess)
@@ -1429,8 +1441,20 @@ static int build_mr_graphs(ppsd_engine* e) {
         if (launch_pdl(mr_prefill_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx,
                        e->d_arctl) != cudaSuccess)
           return -1;
-        int m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
-        if (m < 0) return -1;
+        int m;
+        if (e->hl) {  // [0, split), head layer on a copy, [split, local end)
+          const int split = e->h_ctx.hl_split;
+          m = enqueue_prefill_layers(e, e->d_work_ar, split);
+          if (m < 0) return -1;
+          const int mh = enqueue_head_layer(e, true);
+          if (mh < 0) return -1;
+          const int m2 = enqueue_prefill_layers(e, e->d_work_p2, e->n_local_layers - split);
+          if (m2 < 0) return -1;
+          m += mh + m2;
+        } else {
+          m = enqueue_prefill_layers(e, e->d_work_ar, e->n_local_layers);
+          if (m < 0) return -1;
+        }
         if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 1) !=
             cudaSuccess)
           return -1;
@@ -1680,6 +1704,11 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
         [&]() -> int {
           int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
+          if (e->hl) {
+            const int mh = enqueue_head_layer(e, false);
+            if (mh < 0) return -1;
+            m += mh;
+          }
           if (enqueue_gemv(e, e->d_work, 0, kMatHead) != cudaSuccess) return -1;
           if (launch_pdl(pack_outbox_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, 0) !=
               cudaSuccess)

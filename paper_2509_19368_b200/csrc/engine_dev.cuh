@@ -66,6 +66,7 @@ struct TickCtx {
   int32_t head_row;         // first activation row of the head layer
   Work* work_head;          // the head layer's work (copy source in src_slot)
   Work* work_p2;            // prefill: layers [split, N) of the chunk
+  Work* work_head_pf;  // prefill's exit-head layer (the tick's work_head may already be planned)
 };
 
 constexpr int kBoxHeader = 4;

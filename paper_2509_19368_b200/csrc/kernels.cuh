@@ -88,6 +88,8 @@ struct AttnArgs {
   const void* kv_base;
   long long kv_layer_bytes;
   int32_t first_local;  // global index of the first local layer
+  int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
+  int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
 };
 
 // tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of

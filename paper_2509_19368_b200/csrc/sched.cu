@@ -304,6 +304,22 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
     w->first[0] = ctl->first_layer;
     w->nl[0] = ctl->n_layers;
     w->head_slot[0] = w->head_slot[1] = -1;
+    if (c.hl) {  // exit rank: [0, split) -> head layer on a copy -> [split, local end)
+      w->nl[0] = c.hl_split;
+      Work* wh = c.work_head_pf;
+      wh->G = 1;
+      wh->slot[0] = active ? c.head_row : -1;
+      wh->src_slot = 0;
+      wh->nv[0] = 1;
+      wh->pos[0] = active ? j : 0;
+      wh->first[0] = c.hl_layer;
+      wh->nl[0] = 1;
+      wh->head_slot[0] = wh->head_slot[1] = -1;
+      Work* w2 = c.work_p2;
+      *w2 = *w;
+      w2->first[0] = ctl->first_layer + c.hl_split;
+      w2->nl[0] = ctl->n_layers - c.hl_split;
+    }
     ctl->j = p + 1;
   }
   if (!active) return;
@@ -336,7 +352,7 @@ __global__ void __launch_bounds__(256) prefill_chunk_kernel(const TickCtx* ctxp,
     w->head_slot[0] = w->head_slot[1] = -1;
     if (c.hl) {  // [0, split) -> head layer on copies -> [split, N)
       w->nl[0] = c.hl_split;
-      Work* wh = c.work_head;
+      Work* wh = c.work_head_pf;
       wh->G = 1;
       wh->slot[0] = n > 0 ? c.head_row : -1;
       wh->src_slot = 0;

@@ -37,7 +37,8 @@ class StageShard:
     """The layers, heads and engine of one pipeline rank."""
 
     def __init__(self, config: TransformerConfig, cfg: PipelineConfig, rank: int, world: int, *,
-                 seed: int = 0, deep_scale: float = 1.0, deep_from: int | None = None, device=None):
+                 seed: int = 0, deep_scale: float = 1.0, deep_from: int | None = None, device=None,
+                 exit_head: str = "norm"):
         import torch
 
         self.cfg, self.rank, self.world = cfg, rank, world
@@ -48,7 +49,9 @@ class StageShard:
         k = cfg.exit_stage
         self.lm = TransformerLM(config, seed=seed, deep_scale=deep_scale, deep_from=deep_from,
                                 device=device, layers=layers, need_embed=(lo == 1),
-                                need_head=(lo <= k <= hi) or hi == cfg.n_stages)
+                                need_head=(lo <= k <= hi) or hi == cfg.n_stages,
+                                # the exit head's decoder layer lives on the exit stage's rank
+                                exit_head=exit_head if lo <= k <= hi else "norm")
         self.engine = Engine(self.lm.model_desc(), self.lm.weights_struct(), cfg,
                              device=self.lm.device.index, stage_range=(lo, hi))
         nbytes, stream = C.c_int64(), C.c_void_p()

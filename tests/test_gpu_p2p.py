@@ -65,6 +65,40 @@ def test_p2p_threads_equal_single_gpu(world, e, monkeypatch):
             assert tr.to_csv() == want_tr.to_csv()
 
 
+
+@pytest.mark.parametrize("world,k", [(2, 1), (4, 3)])
+def test_p2p_threads_decoder_layer_exit_head(world, k, monkeypatch):
+    """The Table-1 exit head over the peer-store transport: the exit rank runs
+    the head layer inside its tick graph (prefill included)."""
+    monkeypatch.setenv("PPSD_PDL", "0")
+    from paper_2509_19368_b200.distributed import StageShard, decode_ppsd_p2p, p2p_connect, p2p_prepare
+
+    config = ppsd.TransformerConfig(**CONFIG, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 2, exit_stage=k)
+    prompt = [int(t) for t in np.random.default_rng(9).integers(0, config.vocab, size=17)]
+    full = ppsd.TransformerLM(config, seed=4, deep_scale=0.3, deep_from=2, exit_head="layer")
+    want_t, want_m, want_tr = ppsd.decode_ppsd(full, cfg, prompt, 48, "greedy", ppsd.RngStream(0))
+    shards = [StageShard(config, cfg, r, world, seed=4, deep_scale=0.3, deep_from=2, exit_head="layer")
+              for r in range(world)]
+    xbufs = [p2p_prepare(s)[1] for s in shards]
+    for s in shards:
+        p2p_connect(s, local_xbufs=xbufs)
+    results = [None] * world
+
+    def run(i):
+        results[i] = decode_ppsd_p2p(shards[i], prompt, 48)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in threads), "p2p decode hung"
+    for toks, m, tr in results:
+        assert toks == want_t
+        assert m == want_m
+        assert tr.to_csv() == want_tr.to_csv()
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
