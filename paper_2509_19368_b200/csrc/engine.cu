@@ -1492,6 +1492,7 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
   rc = ensure_trace(e, max_ticks * (e->S + 2));
   if (rc) return rc;
   TickCtx& c = e->h_ctx;
+  c.fold = 0;
   c.trace = e->d_trace;
   c.trace_cap = e->trace_cap;
   c.outbox = reinterpret_cast<float*>(outbox);
@@ -1506,6 +1507,7 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
+  s.c.fold = 0;  // multi-rank runs use the pipelined tick graphs
   s.c.model = 1;
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;
@@ -1676,6 +1678,7 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
     }
   }
   TickCtx& c = e->h_ctx;
+  c.fold = 0;
   c.p2p = 1;
   c.peer_xbuf = e->d_peer_xbuf;
   c.my_xbuf = e->d_xbuf;
@@ -1739,6 +1742,7 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   const int64_t max_ticks = (int64_t)max_tokens * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
   if (max_ticks * (e->S + 2) > e->trace_cap) return fail(PPSD_ESTATE, "p2p trace reservation too small");
   TickCtx& c = e->h_ctx;
+  c.fold = 0;
   c.trace = e->d_trace;
   c.trace_cap = e->trace_cap;
   c.n_prompt = n_prompt;
@@ -1746,6 +1750,7 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
+  s.c.fold = 0;  // multi-rank runs use the pipelined tick graphs
   s.c.model = 1;
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;

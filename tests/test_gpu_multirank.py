@@ -43,7 +43,7 @@ def run_loopback(shards, prompt, max_tokens):
     return [s.end() for s in shards]
 
 
-@pytest.mark.parametrize("world,e", [(2, 2), (4, 2), (2, 3)])
+@pytest.mark.parametrize("world,e", [(1, 2), (2, 2), (4, 2), (2, 3)])
 def test_loopback_pipeline_equals_single_gpu(world, e):
     from paper_2509_19368_b200.distributed import StageShard
 
@@ -61,7 +61,7 @@ def test_loopback_pipeline_equals_single_gpu(world, e):
         assert tr.to_csv() == want_tr.to_csv()
 
 
-@pytest.mark.parametrize("world,e,k", [(2, 2, 1), (4, 2, 1), (2, 2, 2), (4, 2, 3)])
+@pytest.mark.parametrize("world,e,k", [(1, 2, 1), (2, 2, 1), (4, 2, 1), (2, 2, 2), (4, 2, 3)])
 def test_loopback_decoder_layer_exit_head(world, e, k):
     """Table-1 exit head (a decoder layer before the exit norm) across ranks:
     only the exit stage's rank holds and runs it, prefill included."""
@@ -74,7 +74,7 @@ def test_loopback_decoder_layer_exit_head(world, e, k):
     want_toks, want_m, want_tr = ppsd.decode_ppsd(full, cfg, prompt, 64, "greedy", ppsd.RngStream(0))
     shards = [StageShard(config, cfg, r, world, seed=6, deep_scale=0.3, deep_from=e, exit_head="layer")
               for r in range(world)]
-    assert sum(s.lm.exit_layer_w is not None for s in shards) == 1
+    assert sum(s.lm.exit_layer_w is not None for s in shards) == 1  # the exit stage's rank
     for toks, m, tr in run_loopback(shards, prompt, 64):
         assert toks == want_toks
         assert m == want_m
