@@ -225,6 +225,13 @@ int ppsd_simulate(ppsd_engine* e, double alpha, uint64_t verify_seed, int32_t ho
  * stage_owner[st] (st = 1..S, index 0 unused) is the rank owning stage st.
  * outbox / inbox are device buffers owned by the caller. */
 int ppsd_exchange_info(ppsd_engine* e, int64_t* outbox_bytes, void** cuda_stream);
+/* Decode mode of the next ppsd_step_begin (default greedy). Sampling
+ * (pipesim.py:412-414 mode "sampling", streams derive_seed(rng_seed, "draft" |
+ * "verify" | "commit")): boxes grow by the exit and final logits (2 * vocab
+ * fp32 after the activation) and every rank runs the same draws from the
+ * owners' logits, so tokens, metrics and trace equal the single-device
+ * sampling decode. NCCL / caller exchange only (not the peer-store path). */
+int ppsd_step_mode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed);
 int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
                     int32_t force_reject, const int32_t* stage_owner, int32_t world, int32_t rank,
                     void* outbox, void* inbox);

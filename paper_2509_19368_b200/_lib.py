@@ -99,6 +99,7 @@ EXPORTS = {
                                 C.POINTER(Metrics), C.POINTER(TraceRowC), C.c_int64,
                                 C.POINTER(C.c_int64)]),
     "ppsd_exchange_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_void_p)]),
+    "ppsd_step_mode": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
     "ppsd_step_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "ppsd_prefill_steps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),

@@ -111,6 +111,8 @@ struct ppsd_engine {
   EesdState* d_eesd = nullptr;
   int64_t compute_launches = 0, finish_launches = 0, mr_prefill_launches = 0;
   int mr_world = 0, mr_rank = 0, mr_stop = 0, mr_n_prompt = 0;
+  int mr_greedy = 1;          // ppsd_step_mode
+  uint64_t mr_rng_seed = 0;
   int64_t mr_launches = 0, mr_ticks_launched = 0;
   // NVLink peer-store transport
   float* d_xbuf = nullptr;          // [2][world][box] + world flags, shared via IPC
@@ -1470,6 +1472,13 @@ extern "C" int ppsd_exchange_info(ppsd_engine* e, int64_t* outbox_bytes, void** 
   return PPSD_OK;
 }
 
+extern "C" int ppsd_step_mode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "multi-rank needs a transformer engine");
+  e->mr_greedy = greedy ? 1 : 0;
+  e->mr_rng_seed = rng_seed;
+  return PPSD_OK;
+}
+
 extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
                                int32_t force_reject, const int32_t* stage_owner, int32_t world, int32_t rank,
                                void* outbox, void* inbox) {
@@ -1498,6 +1507,13 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
   c.outbox = reinterpret_cast<float*>(outbox);
   c.inbox = reinterpret_cast<const float*>(inbox);
   c.box_words = kBoxHeader + e->dm.d;
+  c.greedy = e->mr_greedy;
+  c.box_logits = e->mr_greedy ? 0 : 1;
+  if (!e->mr_greedy) {
+    c.box_words += 2 * e->dm.V;
+    c.draft_seed = derive_seed_str(e->mr_rng_seed, "draft");
+    c.commit_seed = derive_seed_str(e->mr_rng_seed, "commit");
+  }
   c.rank = rank;
   c.world = world;
   c.owner_k = stage_owner[e->cfg.k];
@@ -1512,6 +1528,7 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;
   s.c.n_prompt = n_prompt;
+  s.c.verify_seed = e->mr_greedy ? 0 : derive_seed_str(e->mr_rng_seed, "verify");
   sched_reset(&s);
   ArCtl ctl{0, e->first_local_layer, e->n_local_layers, 0};
   CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
@@ -1730,6 +1747,8 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
 extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
                                int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out, ppsd_trace_row* trace,
                                int64_t trace_cap, int64_t* trace_len) {
+  if (e && !e->mr_greedy)
+    return fail(PPSD_EUNSUPPORTED, "sampling across ranks runs over the all-gather exchange (ppsd_step_*)");
   if (!e || !e->g_p2p_tick) return fail(PPSD_ESTATE, "call ppsd_p2p_connect first");
   int rc = check_prompt(e, prompt, n_prompt);
   if (rc) return rc;
@@ -1747,6 +1766,7 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   c.trace_cap = e->trace_cap;
   c.n_prompt = n_prompt;
   c.greedy = 1;
+  c.box_logits = 0;
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;

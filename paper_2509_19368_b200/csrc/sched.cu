@@ -145,6 +145,18 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
   }
   __syncthreads();
   if (!begin && !c.greedy && s.c.model != 0) {
+    if (inbox && c.box_logits) {
+      // replicated sampling: every rank draws from the owners' logits, so the
+      // draft / verify / commit streams advance identically everywhere
+      float* l = const_cast<float*>(c.logits32);
+      const float* ex = inbox + (size_t)c.owner_k * c.box_words + kBoxHeader + c.d;
+      const float* fi = inbox + (size_t)c.owner_S * c.box_words + kBoxHeader + c.d + c.vocab;
+      for (int i = threadIdx.x; i < c.vocab; i += blockDim.x) {
+        l[i] = ex[i];
+        l[c.vocab + i] = fi[i];
+      }
+      __syncthreads();
+    }
     int e = -1, ok = -1, f = -1;
     sampling_tick(c, s, &e, &ok, &f);
     if (threadIdx.x == 0) {
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
   }
   if (threadIdx.x == 0) {
     int exit_tok = s_exit_tok, final_tok = s_final_tok;
-    if (inbox) {  // replicated scheduler: head results come from their owners' boxes
+    if (inbox && c.greedy) {  // replicated scheduler: head results come from their owners' boxes
       exit_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_k * c.box_words)[0];
       final_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_S * c.box_words)[1];
     }
@@ -267,6 +279,13 @@ __global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, i
   if (send) {
     const float* x = c.x + (size_t)slot * c.d;
     for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.outbox[kBoxHeader + i] = x[i];
+  }
+  if (c.box_logits && !prefill) {  // sampling: the exit / final logits of the heads this rank owns
+    float* dst = c.outbox + kBoxHeader + c.d;
+    if (w->head_slot[0] >= 0)
+      for (int i = threadIdx.x; i < c.vocab; i += blockDim.x) dst[i] = c.logits32[i];
+    if (w->head_slot[1] >= 0)
+      for (int i = threadIdx.x; i < c.vocab; i += blockDim.x) dst[c.vocab + i] = c.logits32[c.vocab + i];
   }
   if (c.p2p) {  // NVLink peer stores into every rank's exchange buffer + release flags
     __syncthreads();

@@ -16,7 +16,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .decode import Engine
+from .decode import Engine, _check_mode
 from .models import TransformerConfig, TransformerLM
 from .pipeline import EventTrace, PipelineConfig, make_metrics
 
@@ -58,10 +58,16 @@ class StageShard:
         _lib.check(_lib.lib().ppsd_exchange_info(self.engine.h, C.byref(nbytes), C.byref(stream)),
                    "exchange_info")
         self.stream_ptr = stream.value
-        words = nbytes.value // 4
-        self.outbox = torch.zeros(words, dtype=torch.float32, device=self.lm.device)
-        self.inbox = torch.zeros(world, words, dtype=torch.float32, device=self.lm.device)
+        self.greedy_words = nbytes.value // 4
+        self._boxes(self.greedy_words)
         self.stages = (lo, hi)
+
+    def _boxes(self, words: int):
+        import torch
+
+        if getattr(self, "outbox", None) is None or self.outbox.numel() != words:
+            self.outbox = torch.zeros(words, dtype=torch.float32, device=self.lm.device)
+            self.inbox = torch.zeros(self.world, words, dtype=torch.float32, device=self.lm.device)
 
     def torch_stream(self):
         import torch
@@ -69,8 +75,17 @@ class StageShard:
         return torch.cuda.ExternalStream(self.stream_ptr, device=self.lm.device)
 
     # -- the per-rank protocol ------------------------------------------
-    def begin(self, prompt, max_tokens: int, force_reject: bool = False) -> int:
+    def begin(self, prompt, max_tokens: int, force_reject: bool = False, mode: str = "greedy",
+              rng=None) -> int:
+        """Sampling (pipesim.py:412-414): boxes also carry the exit / final
+        logits and every rank makes the same draws (include/ppsd.h
+        ppsd_step_mode); rng is the decode's RngStream."""
+        _check_mode(mode)
         L = _lib.lib()
+        greedy = mode == "greedy"
+        seed = 0 if rng is None else rng.seed
+        _lib.check(L.ppsd_step_mode(self.engine.h, int(greedy), seed & ((1 << 64) - 1)), "step_mode")
+        self._boxes(self.greedy_words + (0 if greedy else 2 * self.lm.vocab))
         p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
         own = (C.c_int32 * len(self.owner))(*self.owner)
         _lib.check(L.ppsd_step_begin(self.engine.h, p, len(prompt), max_tokens, int(bool(force_reject)),
@@ -128,12 +143,13 @@ def nccl_exchange(shard: StageShard, group=None):
 
 
 def decode_ppsd_pipelined(shard: StageShard, prompt, max_tokens: int, exchange=None, *,
-                          force_reject: bool = False):
-    """Greedy PPSD decode with this rank's stages; every rank calls it with the
-    same arguments. Returns (tokens, RunMetrics, EventTrace), identical on all
-    ranks and identical to the single-GPU `decode_ppsd`."""
+                          force_reject: bool = False, mode: str = "greedy", rng=None):
+    """PPSD decode with this rank's stages (greedy, or sampling with the
+    decode's RngStream); every rank calls it with the same arguments. Returns
+    (tokens, RunMetrics, EventTrace), identical on all ranks and identical to
+    the single-GPU `decode_ppsd`."""
     exchange = exchange or nccl_exchange(shard)
-    steps = shard.begin(prompt, max_tokens, force_reject)
+    steps = shard.begin(prompt, max_tokens, force_reject, mode=mode, rng=rng)
     for _ in range(steps):
         shard.prefill_compute()
         exchange()
@@ -213,6 +229,7 @@ def decode_ppsd_p2p(shard: StageShard, prompt, max_tokens: int, *, force_reject:
     """The pipelined decode over the peer-store transport (after p2p_connect);
     every rank calls it with the same arguments."""
     L = _lib.lib()
+    _lib.check(L.ppsd_step_mode(shard.engine.h, 1, 0), "step_mode")  # greedy over peer stores
     p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
     out = np.zeros(max_tokens, dtype=np.int32)
     m = _lib.Metrics()

@@ -10,10 +10,10 @@ pytestmark = pytest.mark.gpu
 ppsd = pytest.importorskip("paper_2509_19368_b200")
 
 
-def run_loopback(shards, prompt, max_tokens):
+def run_loopback(shards, prompt, max_tokens, mode="greedy", seed=0):
     import torch
 
-    steps = [s.begin(prompt, max_tokens) for s in shards]
+    steps = [s.begin(prompt, max_tokens, mode=mode, rng=ppsd.RngStream(seed)) for s in shards]
     assert len(set(steps)) == 1
 
     def exchange():
@@ -79,3 +79,27 @@ def test_loopback_decoder_layer_exit_head(world, e, k):
         assert toks == want_toks
         assert m == want_m
         assert tr.to_csv() == want_tr.to_csv()
+
+
+@pytest.mark.parametrize("world,e,k", [(2, 2, 1), (2, 2, 2), (4, 2, 3)])
+def test_loopback_sampling_equals_single_gpu(world, e, k):
+    """Sampling mode across ranks: the boxes carry the exit / final logits and
+    every rank makes the same draft / verify / commit draws, so tokens,
+    metrics and trace equal the single-device sampling decode."""
+    from paper_2509_19368_b200.distributed import StageShard
+
+    config = ppsd.TransformerConfig(8, 512, 8, 8, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, e, exit_stage=k)
+    prompt = [int(t) for t in np.random.default_rng(5).integers(0, config.vocab, size=15)]
+    full = ppsd.TransformerLM(config, seed=8, deep_scale=0.3, deep_from=e)
+    want = ppsd.decode_ppsd(full, cfg, prompt, 48, "sampling", ppsd.RngStream(21))
+    shards = [StageShard(config, cfg, r, world, seed=8, deep_scale=0.3, deep_from=e) for r in range(world)]
+    for toks, m, tr in run_loopback(shards, prompt, 48, mode="sampling", seed=21):
+        assert toks == want[0]
+        assert m == want[1]
+        assert tr.to_csv() == want[2].to_csv()
+    assert 0 < want[1].accepts < 48  # both verdicts occur
+    # back to greedy on the same shards
+    gt, gm, gtr = ppsd.decode_ppsd(full, cfg, prompt, 32, "greedy", ppsd.RngStream(0))
+    for toks, m, tr in run_loopback(shards, prompt, 32):
+        assert toks == gt and m == gm and tr.to_csv() == gtr.to_csv()
