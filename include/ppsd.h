@@ -230,7 +230,8 @@ int ppsd_exchange_info(ppsd_engine* e, int64_t* outbox_bytes, void** cuda_stream
  * "verify" | "commit")): boxes grow by the exit and final logits (2 * vocab
  * fp32 after the activation) and every rank runs the same draws from the
  * owners' logits, so tokens, metrics and trace equal the single-device
- * sampling decode. NCCL / caller exchange only (not the peer-store path). */
+ * sampling decode. Applies to ppsd_step_begin and ppsd_p2p_decode (the
+ * peer-store buffers are sized for the larger box). */
 int ppsd_step_mode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed);
 int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
                     int32_t force_reject, const int32_t* stage_owner, int32_t world, int32_t rank,

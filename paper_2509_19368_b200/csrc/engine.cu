@@ -1514,6 +1514,7 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
     c.draft_seed = derive_seed_str(e->mr_rng_seed, "draft");
     c.commit_seed = derive_seed_str(e->mr_rng_seed, "commit");
   }
+  c.box_used = c.box_words;
   c.rank = rank;
   c.world = world;
   c.owner_k = stage_owner[e->cfg.k];
@@ -1636,7 +1637,7 @@ extern "C" int ppsd_p2p_prepare(ppsd_engine* e, int32_t world, void* ipc_handle,
   if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "p2p needs a transformer engine");
   if (world < 1 || world > e->S) return fail(PPSD_EINVAL, "bad world size");
   CU(cudaSetDevice(e->device));
-  const int box = kBoxHeader + e->dm.d;
+  const int box = kBoxHeader + e->dm.d + 2 * e->dm.V;  // stride: room for sampling's logits
   if (!e->d_xbuf || e->p2p_world != world) {
     if (e->d_xbuf) CU(cudaFree(e->d_xbuf));
     size_t bytes = sizeof(float) * 2 * (size_t)world * box + sizeof(uint64_t) * world;
@@ -1681,7 +1682,7 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
   }
   if (!e->d_peer_xbuf) CU(dalloc(&e->d_peer_xbuf, sizeof(float*) * kMaxStages));
   CU(cudaMemcpy(e->d_peer_xbuf, peers.data(), sizeof(float*) * world, cudaMemcpyHostToDevice));
-  if (!e->d_p2p_outbox) CU(dalloc(&e->d_p2p_outbox, sizeof(float) * (kBoxHeader + e->dm.d)));
+  if (!e->d_p2p_outbox) CU(dalloc(&e->d_p2p_outbox, sizeof(float) * (kBoxHeader + e->dm.d + 2 * e->dm.V)));
   if (!e->d_xcount) CU(dalloc(&e->d_xcount, sizeof(uint64_t)));
   if (!e->d_xerr) CU(dalloc(&e->d_xerr, sizeof(int32_t)));
   {  // everything a decode up to max_ctx can need, allocated now
@@ -1703,7 +1704,8 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
   c.xerr = e->d_xerr;
   c.outbox = e->d_p2p_outbox;
   c.inbox = nullptr;
-  c.box_words = kBoxHeader + e->dm.d;
+  c.box_words = kBoxHeader + e->dm.d + 2 * e->dm.V;
+  c.box_used = kBoxHeader + e->dm.d;
   c.rank = rank;
   c.world = world;
   c.owner_k = stage_owner[e->cfg.k];
@@ -1747,8 +1749,6 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
 extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int32_t max_tokens,
                                int32_t force_reject, int32_t* out_tokens, ppsd_metrics* out, ppsd_trace_row* trace,
                                int64_t trace_cap, int64_t* trace_len) {
-  if (e && !e->mr_greedy)
-    return fail(PPSD_EUNSUPPORTED, "sampling across ranks runs over the all-gather exchange (ppsd_step_*)");
   if (!e || !e->g_p2p_tick) return fail(PPSD_ESTATE, "call ppsd_p2p_connect first");
   int rc = check_prompt(e, prompt, n_prompt);
   if (rc) return rc;
@@ -1765,8 +1765,13 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   c.trace = e->d_trace;
   c.trace_cap = e->trace_cap;
   c.n_prompt = n_prompt;
-  c.greedy = 1;
-  c.box_logits = 0;
+  c.greedy = e->mr_greedy;
+  c.box_logits = e->mr_greedy ? 0 : 1;
+  c.box_used = kBoxHeader + e->dm.d + (e->mr_greedy ? 0 : 2 * e->dm.V);
+  if (!e->mr_greedy) {
+    c.draft_seed = derive_seed_str(e->mr_rng_seed, "draft");
+    c.commit_seed = derive_seed_str(e->mr_rng_seed, "commit");
+  }
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
@@ -1775,6 +1780,7 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;
   s.c.n_prompt = n_prompt;
+  s.c.verify_seed = e->mr_greedy ? 0 : derive_seed_str(e->mr_rng_seed, "verify");
   sched_reset(&s);
   char* pin = e->h_p2p_pin;
   TickCtx* pin_ctx = reinterpret_cast<TickCtx*>(pin);

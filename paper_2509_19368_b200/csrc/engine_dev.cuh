@@ -32,6 +32,7 @@ struct TickCtx {
   const float* inbox;   // world boxes, all-gathered by the caller
   int32_t box_words;
   int32_t box_logits;  // sampling across ranks: boxes also carry the exit and final logits [2][V]
+  int32_t box_used;    // words of a box written / published (<= box_words, the stride)
   int32_t rank, world;
   int32_t owner_k, owner_S, owner_prev;  // ranks owning the exit stage, stage S, stage lo-1
   int32_t n_prompt;

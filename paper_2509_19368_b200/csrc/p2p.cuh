@@ -42,7 +42,7 @@ __device__ inline uint64_t p2p_publish(const TickCtx& c) {
   const size_t slot = ((e & 1) * c.world + c.rank) * (size_t)c.box_words;
   for (int r = 0; r < c.world; ++r) {
     float* dst = c.peer_xbuf[r] + slot;
-    for (int i = threadIdx.x; i < c.box_words; i += blockDim.x) dst[i] = c.outbox[i];
+    for (int i = threadIdx.x; i < c.box_used; i += blockDim.x) dst[i] = c.outbox[i];
   }
   __threadfence_system();  // every storing thread orders its box stores before the flag
   __syncthreads();

@@ -225,11 +225,15 @@ def p2p_setup_group(shard: StageShard, group=None):
     p2p_connect(shard, handles=handles)
 
 
-def decode_ppsd_p2p(shard: StageShard, prompt, max_tokens: int, *, force_reject: bool = False):
-    """The pipelined decode over the peer-store transport (after p2p_connect);
-    every rank calls it with the same arguments."""
+def decode_ppsd_p2p(shard: StageShard, prompt, max_tokens: int, *, force_reject: bool = False,
+                    mode: str = "greedy", rng=None):
+    """The pipelined decode over the peer-store transport (after p2p_connect),
+    greedy or sampling (the boxes then carry the owners' logits); every rank
+    calls it with the same arguments."""
+    _check_mode(mode)
     L = _lib.lib()
-    _lib.check(L.ppsd_step_mode(shard.engine.h, 1, 0), "step_mode")  # greedy over peer stores
+    seed = 0 if rng is None else rng.seed
+    _lib.check(L.ppsd_step_mode(shard.engine.h, int(mode == "greedy"), seed & ((1 << 64) - 1)), "step_mode")
     p = (C.c_int32 * len(prompt))(*[int(t) for t in prompt])
     out = np.zeros(max_tokens, dtype=np.int32)
     m = _lib.Metrics()

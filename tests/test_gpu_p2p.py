@@ -99,6 +99,39 @@ def test_p2p_threads_decoder_layer_exit_head(world, k, monkeypatch):
         assert m == want_m
         assert tr.to_csv() == want_tr.to_csv()
 
+
+def test_p2p_threads_sampling(monkeypatch):
+    """Sampling over the peer-store transport, then greedy again on the same
+    connected engines (the exchange numbers keep increasing across calls)."""
+    monkeypatch.setenv("PPSD_PDL", "0")
+    from paper_2509_19368_b200.distributed import StageShard, decode_ppsd_p2p, p2p_connect, p2p_prepare
+
+    config = ppsd.TransformerConfig(**CONFIG, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 2)
+    prompt = [int(t) for t in np.random.default_rng(13).integers(0, config.vocab, size=15)]
+    full = ppsd.TransformerLM(config, seed=5, deep_scale=0.3, deep_from=2)
+    shards = [StageShard(config, cfg, r, 2, seed=5, deep_scale=0.3, deep_from=2) for r in range(2)]
+    xbufs = [p2p_prepare(s)[1] for s in shards]
+    for s in shards:
+        p2p_connect(s, local_xbufs=xbufs)
+    for mode, seed in (("sampling", 17), ("greedy", 0), ("sampling", 3)):
+        want_t, want_m, want_tr = ppsd.decode_ppsd(full, cfg, prompt, 40, mode, ppsd.RngStream(seed))
+        results = [None] * 2
+
+        def run(i):
+            results[i] = decode_ppsd_p2p(shards[i], prompt, 40, mode=mode, rng=ppsd.RngStream(seed))
+
+        threads = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert not any(t.is_alive() for t in threads), "p2p decode hung"
+        for toks, m, tr in results:
+            assert toks == want_t, mode
+            assert m == want_m, mode
+            assert tr.to_csv() == want_tr.to_csv(), mode
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
