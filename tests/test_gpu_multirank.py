@@ -10,10 +10,10 @@ pytestmark = pytest.mark.gpu
 ppsd = pytest.importorskip("paper_2509_19368_b200")
 
 
-def run_loopback(shards, prompt, max_tokens, mode="greedy", seed=0):
+def run_loopback(shards, prompt, max_tokens, mode="greedy", seed=0, force_reject=False):
     import torch
 
-    steps = [s.begin(prompt, max_tokens, mode=mode, rng=ppsd.RngStream(seed)) for s in shards]
+    steps = [s.begin(prompt, max_tokens, force_reject, mode=mode, rng=ppsd.RngStream(seed)) for s in shards]
     assert len(set(steps)) == 1
 
     def exchange():
@@ -103,3 +103,22 @@ def test_loopback_sampling_equals_single_gpu(world, e, k):
     gt, gm, gtr = ppsd.decode_ppsd(full, cfg, prompt, 32, "greedy", ppsd.RngStream(0))
     for toks, m, tr in run_loopback(shards, prompt, 32):
         assert toks == gt and m == gm and tr.to_csv() == gtr.to_csv()
+
+
+@pytest.mark.parametrize("mode,comm,force", [("greedy", 1, False), ("greedy", 0, True), ("sampling", 2, False),
+                                            ("sampling", 0, True)])
+def test_loopback_comm_latency_and_force_reject(mode, comm, force):
+    """Hop latency (comm_latency ticks per stage boundary) and force_reject
+    across ranks, greedy and sampling."""
+    from paper_2509_19368_b200.distributed import StageShard
+
+    config = ppsd.TransformerConfig(8, 512, 8, 8, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 2, comm_latency=comm)
+    prompt = [int(t) for t in np.random.default_rng(17).integers(0, config.vocab, size=13)]
+    full = ppsd.TransformerLM(config, seed=9, deep_scale=0.3, deep_from=2)
+    want = ppsd.decode_ppsd(full, cfg, prompt, 32, mode, ppsd.RngStream(4), force_reject=force)
+    shards = [StageShard(config, cfg, r, 2, seed=9, deep_scale=0.3, deep_from=2) for r in range(2)]
+    for toks, m, tr in run_loopback(shards, prompt, 32, mode=mode, seed=4, force_reject=force):
+        assert toks == want[0]
+        assert m == want[1]
+        assert tr.to_csv() == want[2].to_csv()
