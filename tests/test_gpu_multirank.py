@@ -81,8 +81,9 @@ def test_loopback_decoder_layer_exit_head(world, e, k):
         assert tr.to_csv() == want_tr.to_csv()
 
 
-@pytest.mark.parametrize("world,e,k", [(2, 2, 1), (2, 2, 2), (4, 2, 3)])
-def test_loopback_sampling_equals_single_gpu(world, e, k):
+@pytest.mark.parametrize("world,e,k,head", [(2, 2, 1, "norm"), (2, 2, 2, "norm"), (4, 2, 3, "norm"),
+                                             (2, 2, 1, "layer"), (4, 2, 3, "layer")])
+def test_loopback_sampling_equals_single_gpu(world, e, k, head):
     """Sampling mode across ranks: the boxes carry the exit / final logits and
     every rank makes the same draft / verify / commit draws, so tokens,
     metrics and trace equal the single-device sampling decode."""
@@ -91,9 +92,10 @@ def test_loopback_sampling_equals_single_gpu(world, e, k):
     config = ppsd.TransformerConfig(8, 512, 8, 8, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
     cfg = ppsd.PipelineConfig(8, e, exit_stage=k)
     prompt = [int(t) for t in np.random.default_rng(5).integers(0, config.vocab, size=15)]
-    full = ppsd.TransformerLM(config, seed=8, deep_scale=0.3, deep_from=e)
+    full = ppsd.TransformerLM(config, seed=8, deep_scale=0.3, deep_from=e, exit_head=head)
     want = ppsd.decode_ppsd(full, cfg, prompt, 48, "sampling", ppsd.RngStream(21))
-    shards = [StageShard(config, cfg, r, world, seed=8, deep_scale=0.3, deep_from=e) for r in range(world)]
+    shards = [StageShard(config, cfg, r, world, seed=8, deep_scale=0.3, deep_from=e, exit_head=head)
+              for r in range(world)]
     for toks, m, tr in run_loopback(shards, prompt, 48, mode="sampling", seed=21):
         assert toks == want[0]
         assert m == want[1]
