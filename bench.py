@@ -330,7 +330,19 @@ def run_pipelined(args, world, rank, local):
     shard = D.StageShard(config, cfg, rank, world, seed=SEED, deep_scale=args.deep_scale,
                          deep_from=exit_depth, device=local)
     if transport == "p2p":
-        D.p2p_setup_group(shard)
+        # peer mapping failures (no P2P between the devices) fall back to the
+        # NCCL all-gather on every rank, decided collectively
+        ok = 1
+        try:
+            D.p2p_setup_group(shard)
+        except Exception as ex:  # noqa: BLE001
+            ok = 0
+            print(f"rank {rank}: peer-store transport unavailable ({ex}); using nccl", file=sys.stderr)
+        flag = torch.tensor([ok], dtype=torch.int32, device=reduce_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            transport = "nccl"
+    if transport == "p2p":
 
         def decode(prompt):
             return D.decode_ppsd_p2p(shard, prompt, NEW_TOKENS)
