@@ -10,6 +10,31 @@
 
 namespace ppsd {
 
+// Exit-head layer (md.exit_head_layer): one decoder layer (global index
+// c.hl_layer, its own KV) run on copies of rows [src, src + nv) placed at
+// c.head_row; src < 0 plans no work. Thread 0 only.
+__device__ void plan_head_layer(const TickCtx& c, Work* wh, int src, int pos, int nv) {
+  wh->G = 1;
+  wh->slot[0] = src >= 0 ? c.head_row : -1;
+  wh->src_slot = src;
+  wh->pos[0] = src >= 0 ? pos : 0;
+  wh->first[0] = c.hl_layer;
+  wh->nl[0] = 1;
+  wh->nv[0] = nv;
+  wh->head_slot[0] = wh->head_slot[1] = -1;
+}
+
+// Prefill with the exit-head layer: w runs layers [first, first + split),
+// the head layer runs on copies of its rows, w2 runs the rest. Thread 0 only.
+__device__ void split_prefill(const TickCtx& c, const ArCtl* ctl, Work* w, bool active, int pos, int nv) {
+  w->nl[0] = c.hl_split;
+  plan_head_layer(c, c.work_head_pf, active ? 0 : -1, pos, nv);
+  Work* w2 = c.work_p2;
+  *w2 = *w;
+  w2->first[0] = ctl->first_layer + c.hl_split;
+  w2->nl[0] = ctl->n_layers - c.hl_split;
+}
+
 // Sampling mode, run by the whole block before sched_finish (pipesim.py:346-365):
 // the draft for this tick's exit chain is drawn from p = softmax(exit logits)
 // (p kept per chain for its verdict), and the verdict for the chain at stage S
@@ -204,15 +229,7 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       wd->head_slot[0] = wd->head_slot[1] = -1;
       if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
       if (c.hl) {  // exit-head layer on a copy of the launched chain's exit state
-        Work* wh = c.work_head;
-        wh->G = 1;
-        wh->slot[0] = row >= 0 ? c.head_row : -1;
-        wh->src_slot = row;
-        wh->pos[0] = w->pos[0];
-        wh->first[0] = c.hl_layer;
-        wh->nl[0] = 1;
-        wh->nv[0] = 1;
-        wh->head_slot[0] = wh->head_slot[1] = -1;
+        plan_head_layer(c, c.work_head, row, w->pos[0], 1);
         w->head_slot[0] = row >= 0 ? c.head_row : -1;
       }
       s_launch_slot = row;
@@ -230,17 +247,9 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       }
       w->head_slot[0] = (s.c.k >= c.lo && s.c.k <= c.hi) ? s.exit_slot : -1;
       w->head_slot[1] = (s.c.S >= c.lo && s.c.S <= c.hi) ? s.final_slot : -1;
-      if (c.hl) {  // exit-head layer on a copy of the exit chain's state (single device)
-        Work* wh = c.work_head;
+      if (c.hl) {  // exit-head layer on a copy of the exit chain's state (exit stage's rank)
         const int ex = w->head_slot[0];
-        wh->G = 1;
-        wh->slot[0] = ex >= 0 ? c.head_row : -1;
-        wh->src_slot = ex;
-        wh->pos[0] = ex >= 0 ? s.c.n_prompt + s.ch_pos[ex] - 2 : 0;
-        wh->first[0] = c.hl_layer;
-        wh->nl[0] = 1;
-        wh->nv[0] = 1;
-        wh->head_slot[0] = wh->head_slot[1] = -1;
+        plan_head_layer(c, c.work_head, ex, ex >= 0 ? s.c.n_prompt + s.ch_pos[ex] - 2 : 0, 1);
         w->head_slot[0] = ex >= 0 ? c.head_row : -1;
       }
       s_launch_slot = (s.launched && c.lo == 1) ? s.work[1] : -1;
@@ -324,20 +333,7 @@ __global__ void __launch_bounds__(256) mr_prefill_begin_kernel(const TickCtx* ct
     w->nl[0] = ctl->n_layers;
     w->head_slot[0] = w->head_slot[1] = -1;
     if (c.hl) {  // exit rank: [0, split) -> head layer on a copy -> [split, local end)
-      w->nl[0] = c.hl_split;
-      Work* wh = c.work_head_pf;
-      wh->G = 1;
-      wh->slot[0] = active ? c.head_row : -1;
-      wh->src_slot = 0;
-      wh->nv[0] = 1;
-      wh->pos[0] = active ? j : 0;
-      wh->first[0] = c.hl_layer;
-      wh->nl[0] = 1;
-      wh->head_slot[0] = wh->head_slot[1] = -1;
-      Work* w2 = c.work_p2;
-      *w2 = *w;
-      w2->first[0] = ctl->first_layer + c.hl_split;
-      w2->nl[0] = ctl->n_layers - c.hl_split;
+      split_prefill(c, ctl, w, active, j, 1);
     }
     ctl->j = p + 1;
   }
@@ -370,20 +366,7 @@ __global__ void __launch_bounds__(256) prefill_chunk_kernel(const TickCtx* ctxp,
     w->nl[0] = ctl->n_layers;
     w->head_slot[0] = w->head_slot[1] = -1;
     if (c.hl) {  // [0, split) -> head layer on copies -> [split, N)
-      w->nl[0] = c.hl_split;
-      Work* wh = c.work_head_pf;
-      wh->G = 1;
-      wh->slot[0] = n > 0 ? c.head_row : -1;
-      wh->src_slot = 0;
-      wh->nv[0] = n > 0 ? n : 1;
-      wh->pos[0] = j0;
-      wh->first[0] = c.hl_layer;
-      wh->nl[0] = 1;
-      wh->head_slot[0] = wh->head_slot[1] = -1;
-      Work* w2 = c.work_p2;
-      *w2 = *w;
-      w2->first[0] = ctl->first_layer + c.hl_split;
-      w2->nl[0] = ctl->n_layers - c.hl_split;
+      split_prefill(c, ctl, w, n > 0, j0, n > 0 ? n : 1);
     }
     ctl->j = j0 + (n > 0 ? n : 0);
     s_j0 = j0;
