@@ -124,3 +124,21 @@ def test_loopback_comm_latency_and_force_reject(mode, comm, force):
         assert toks == want[0]
         assert m == want[1]
         assert tr.to_csv() == want[2].to_csv()
+
+
+@pytest.mark.parametrize("n_prompt,max_tokens,mode", [(1, 1, "greedy"), (1, 9, "sampling"), (2, 1, "sampling"),
+                                                      (3, 5, "greedy")])
+def test_loopback_edge_lengths(n_prompt, max_tokens, mode):
+    """One-token prompts (no prefill step), one-token decodes, both modes."""
+    from paper_2509_19368_b200.distributed import StageShard
+
+    config = ppsd.TransformerConfig(8, 512, 8, 8, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 2)
+    prompt = [int(t) for t in np.random.default_rng(23).integers(0, config.vocab, size=n_prompt)]
+    full = ppsd.TransformerLM(config, seed=3, deep_scale=0.3, deep_from=2)
+    want = ppsd.decode_ppsd(full, cfg, prompt, max_tokens, mode, ppsd.RngStream(6))
+    shards = [StageShard(config, cfg, r, 4, seed=3, deep_scale=0.3, deep_from=2) for r in range(4)]
+    for toks, m, tr in run_loopback(shards, prompt, max_tokens, mode=mode, seed=6):
+        assert toks == want[0]
+        assert m == want[1]
+        assert tr.to_csv() == want[2].to_csv()
