@@ -82,6 +82,12 @@ void ppsdh_finish(void* p, int exit_tok, int final_tok) {
   sched_finish(&h->s, exit_tok, final_tok, h->tokens, h->pdig, h->trace, h->cap);
 }
 
+// sampling: the verdict (final_ok) and committed token come from the model side
+void ppsdh_finish_sampled(void* p, int exit_tok, int final_tok, int final_ok) {
+  HostSched* h = (HostSched*)p;
+  sched_finish(&h->s, exit_tok, final_tok, h->tokens, h->pdig, h->trace, h->cap, final_ok);
+}
+
 // folded schedule (sched.h: sched_fold_plan)
 void ppsdh_set_fold(void* p, int on) { ((HostSched*)p)->s.c.fold = on; }
 int ppsdh_fold_width(void* p) { return sched_fold_width(&((HostSched*)p)->s.c); }

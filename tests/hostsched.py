@@ -39,6 +39,7 @@ def lib():
         L.ppsdh_destroy.argtypes = [C.c_void_p]
         L.ppsdh_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.ppsdh_finish.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ppsdh_finish_sampled.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
         L.ppsdh_set_fold.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_fold_width.argtypes = [C.c_void_p]
         L.ppsdh_fold_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
@@ -92,8 +93,11 @@ class HostSched:
         lib().ppsdh_fold_plan(self.h, out)
         return list(out)
 
-    def finish(self, exit_tok=-1, final_tok=-1):
-        lib().ppsdh_finish(self.h, exit_tok, final_tok)
+    def finish(self, exit_tok=-1, final_tok=-1, final_ok=None):
+        if final_ok is None:
+            lib().ppsdh_finish(self.h, exit_tok, final_tok)
+        else:
+            lib().ppsdh_finish_sampled(self.h, exit_tok, final_tok, int(final_ok))
 
     def chain_pos(self, slot):
         return lib().ppsdh_chain_pos(self.h, slot)
