@@ -44,6 +44,7 @@ static int fail(int code, const std::string& msg) {
 
 struct GemvPlan {
   int vpt = 0, tr = 0, m = 1, ns = 0, sub = 1, R = 0, K = 0;
+  int ksplit = 0, K_full = 0;  // K split across the two grid halves (K = K_full / 2)
   size_t smem = 0;
 };
 
@@ -63,6 +64,8 @@ struct ppsd_engine {
   Work* d_work_head = nullptr;  // exit-head layer (md.exit_head_layer)
   Work* d_work_p2 = nullptr;       // prefill: layers after the exit (exit-head layer)
   Work* d_work_head_pf = nullptr;  // prefill's exit-head layer
+  float* d_part = nullptr;         // K-split down projection: second half's row sums
+  int32_t* d_part_flag = nullptr;  // ... and their per-chunk flags
   bool hl = false;              // exit head has a decoder layer
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
@@ -175,6 +178,10 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   a.page_table = e->d_page_table;
   a.head_part = e->d_head_part;
   a.head_cnt = e->d_head_cnt;
+  a.ksplit = p.ksplit;
+  a.k_ld = p.K_full;
+  a.part_buf = e->d_part;
+  a.part_flag = e->d_part_flag;
   return gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st);
 }
 
@@ -497,7 +504,7 @@ static void free_engine(ppsd_engine* e) {
     if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_work_head, e->d_work_p2,
-                  e->d_work_head_pf, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+                  e->d_work_head_pf, e->d_part, e->d_part_flag, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
                   e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
@@ -661,7 +668,15 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         if ((m == kMatHead && b) || (m == kMatHeadV && !b)) continue;
         GemvPlan& p = b ? e->gpb[m] : e->gp[m];
         p.R = shapes[m][0];
-        p.K = shapes[m][1];
+        p.K = p.K_full = shapes[m][1];
+        // Wide down projections (K > 8192): each grid half streams one column
+        // half (half the input slice per thread: no register boost in the
+        // 4-vector plan), in every plan, so M = 1 and batched results agree.
+        static const bool split_on = !(getenv("PPSD_DOWN_SPLIT") && getenv("PPSD_DOWN_SPLIT")[0] == '0');
+        if (m == kMatDown && split_on && p.K > 8192 && (p.K / 2) % 8 == 0 && e->num_sms % 2 == 0) {
+          p.ksplit = 1;
+          p.K = p.K / 2;
+        }
         if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.sub, &p.smem) != 0)
           return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
                                              std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
@@ -741,6 +756,10 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_h, sizeof(float) * nb * d.ffn));
+    if (e->gp[kMatDown].ksplit) {
+      CU(dalloc(&e->d_part, sizeof(float) * nb * d.d));
+      CU(dalloc(&e->d_part_flag, sizeof(int32_t) * (size_t)e->num_sms * kSplitChunks));
+    }
     CU(dalloc(&e->d_logits, sizeof(float) * (kMaxVec + 1) * (size_t)d.V));  // folded: exit + batch rows
     CU(dalloc(&e->d_attn_part, sizeof(float) * nb * d.H * e->max_pages * (d.hd + 2)));
     CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * nb * d.KV));
@@ -1384,7 +1403,7 @@ extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, 
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
   const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
   *avg_ms = ms / reps;
-  *bytes_per_launch = (double)p.R * p.K * 2.0 * (head ? 1 : ng);
+  *bytes_per_launch = (double)p.R * (p.ksplit ? p.K_full : p.K) * 2.0 * (head ? 1 : ng);
   return PPSD_OK;
 }
 

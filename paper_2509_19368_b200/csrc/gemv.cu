@@ -114,13 +114,13 @@ constexpr int nw_for(int /*vpt*/) { return 8; }
 // warps). Those instantiations run a 4-warp producer warpgroup that hands its
 // registers to the consumers (setmaxnreg). Measured: the boost made the
 // K = 4096 batched plans slower, so only wide-K plans use it.
-template <int VPT, int M>
-constexpr bool reg_boost() { return VPT >= 5 && M >= 4; }
-template <int VPT, int M>
-constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M>() ? 4 : 1)) * 32; }
+template <int VPT, int M, int EPI = -1>
+constexpr bool reg_boost() { return (VPT >= 5 || (VPT == 3 && EPI == kMatDown)) && M >= 4; }
+template <int VPT, int M, int EPI = -1>
+constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M, EPI>() ? 4 : 1)) * 32; }
 
 template <int VPT, int TR, int M, int EPI>
-__global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(const GemvArgs a) {
   constexpr int NW = nw_for(VPT);  // consumer warps
   constexpr int NC = NW * 32;      // consumer threads
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
@@ -184,6 +184,11 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
     return;
   }
   const int tpp = R / TR;
+  // K split: CTA kb of each grid half takes the same tiles, half kh its columns
+  const bool ksplit = EPI == kMatDown && a.ksplit;
+  const int kG = ksplit ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int kh = ksplit && (int)blockIdx.x >= kG ? 1 : 0;
+  const int kb = (int)blockIdx.x - kh * kG;
   long long t0, t1;
   int hv_p = 0, hv_c0 = 0, hv_c1 = 0;  // kHeadV: this CTA's problem and its CTA span
   if (kHeadV) {
@@ -197,13 +202,13 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
     t1 = (long long)hv_p * tpp + (long long)tpp * (bl + 1) / nc;
   } else {
     const long long T = (long long)np * tpp;
-    t0 = T * blockIdx.x / gridDim.x;
-    t1 = T * (blockIdx.x + 1) / gridDim.x;
+    t0 = T * kb / kG;
+    t1 = T * (kb + 1) / kG;
   }
   const int ntiles = (int)(t1 - t0);
 
   if (warp >= NW) {  // ---------------- producer ----------------
-    if constexpr (reg_boost<VPT, M>()) setmaxnreg_dec<40>();
+    if constexpr (reg_boost<VPT, M, EPI>()) setmaxnreg_dec<40>();
     if (warp == NW && lane == 0 && ntiles > 0) {
       const uint64_t pol = policy_evict_first();
       int cur_p = -1;
@@ -227,8 +232,15 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
         const int st = j % NS;
         if (j >= NS) mbar_wait(&empty[st], ((j / NS) & 1) ^ 1);
         mbar_expect_tx(&full[st], cnt * tile_bytes);
-        bulk_g2s(ring + (size_t)st * stage_bytes, wb + (size_t)tile * tile_bytes, cnt * tile_bytes,
-                 &full[st], pol);
+        if (ksplit) {  // this half's columns of each row: one copy per row
+          const unsigned char* src = wb + ((size_t)tile * TR * a.k_ld + (size_t)kh * K) * 2;
+          for (int r = 0; r < cnt * TR; ++r)
+            bulk_g2s(ring + (size_t)st * stage_bytes + (size_t)r * K * 2, src + (size_t)r * a.k_ld * 2, K * 2,
+                     &full[st], pol);
+        } else {
+          bulk_g2s(ring + (size_t)st * stage_bytes, wb + (size_t)tile * tile_bytes, cnt * tile_bytes, &full[st],
+                   pol);
+        }
         n += cnt;
       }
     }
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
   }
 
   // ---------------- consumers ----------------
-  if constexpr (reg_boost<VPT, M>()) setmaxnreg_inc<232>();
+  if constexpr (reg_boost<VPT, M, EPI>()) setmaxnreg_inc<232>();
   pdl_wait();     // activations of the previous kernel are visible from here on
   pdl_trigger();  // ...so the next kernel may start streaming its weights
   float bestv[M];
@@ -253,6 +265,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
   int cur_v0 = 0;
   int chunk_n0 = 0;  // first tile of the current (not yet flushed) epilogue chunk
   int sj = -1, s_off = 0, s_cnt = 0;  // ring stage, tile within it, its tile count
+  int nchunk = 0;                     // K split: epilogue chunks so far (flag index)
 
   if (ntiles > 0) {
     const int nvec = K >> 3;
@@ -305,7 +318,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
               if (EPI == kMatQKV) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.attn_norm; }
               if (EPI == kMatGU) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.mlp_norm; }
               if (EPI == kMatO) src[m] = a.o + (size_t)s * a.dm.H * a.dm.hd;
-              if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn;
+              if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn + (size_t)kh * K;
             }
           }
         }
@@ -469,6 +482,15 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
       const bool last_of_problem = (n == ntiles - 1) || (tip + 1 == tpp);
       if (ct == CHT - 1 || last_of_problem) {
         named_bar_sync(1, NC);
+        int* kflag = ksplit ? a.part_flag + (size_t)kb * kSplitChunks + (nchunk++ % kSplitChunks) : nullptr;
+        if (ksplit && kh == 0) {  // wait for the second half's row sums of this chunk
+          if (tid == 0) {
+            const uint64_t tw = globaltimer();
+            while (ld_acquire_gpu(kflag) == 0)
+              if (globaltimer() - tw > 2000000000ull) break;  // 2 s: wrong result, never a hang
+          }
+          named_bar_sync(1, NC);
+        }
         const int n0 = chunk_n0;
         chunk_n0 = n + 1;
         const int nrows = (ct + 1) * TR;
@@ -546,13 +568,22 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M>(), 1) gemv_kernel(const G
                   bestv[m] = y;
                   besti[m] = rr;
                 }
+              } else if (ksplit) {
+                float* pb = a.part_buf + (size_t)vslot[m] * a.dm.d + rr;
+                if (kh) *pb = y;
+                else a.x[(size_t)vslot[m] * a.dm.d + rr] += y + __ldcg(pb);
               } else {
                 a.x[(size_t)vslot[m] * a.dm.d + rr] += y;
               }
             }
           }
         }
+        if (ksplit && kh == 1) __threadfence();  // row sums before the flag
         named_bar_sync(1, NC);
+        if (ksplit && tid == 0) {
+          if (kh == 1) st_release_gpu(kflag, 1);
+          else *kflag = 0;  // consumed: ready for the next launch
+        }
       }
       if (++tip == tpp) {
         tip = 0;
@@ -659,7 +690,7 @@ cudaError_t launch_one(const GemvArgs& a, size_t smem, int grid, cudaStream_t st
   constexpr int TR = tr_for(VPT, M, EPI);
   auto fn = gemv_kernel<VPT, TR, M, EPI>;
   if (attrs_only) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(fn, dim3(grid), dim3(gemv_threads<VPT, M>()), smem, st, a);
+  return launch_pdl(fn, dim3(grid), dim3(gemv_threads<VPT, M, EPI>()), smem, st, a);
 }
 
 template <int VPT, int M>

@@ -71,7 +71,15 @@ struct GemvArgs {
   const int32_t* page_table;
   float* head_part;  // [grid][kMaxVec][2] (value, index-as-float bits)
   int32_t* head_cnt; // [kMaxVec] arrival tickets
+  // K split (wide down projections, ksplit = 1): the two halves of the grid
+  // stream the two column halves [h*K, h*K + K) of rows k_ld long; the
+  // second half publishes its row sums (part_buf + part_flag), the first
+  // adds them in fixed order before the residual add
+  int32_t ksplit, k_ld;
+  float* part_buf;     // [nslot][d]
+  int32_t* part_flag;  // [grid/2][kSplitChunks]
 };
+constexpr int kSplitChunks = 64;  // epilogue chunks per CTA pair
 
 struct AttnArgs {
   const Work* work;
