@@ -115,7 +115,7 @@ constexpr int nw_for(int /*vpt*/) { return 8; }
 // registers to the consumers (setmaxnreg). Measured: the boost made the
 // K = 4096 batched plans slower, so only wide-K plans use it.
 template <int VPT, int M, int EPI = -1>
-constexpr bool reg_boost() { return (VPT >= 5 || (VPT == 3 && EPI == kMatDown)) && M >= 4; }
+constexpr bool reg_boost() { return (VPT >= 5 || (VPT >= 3 && EPI == kMatDown)) && M >= 4; }
 template <int VPT, int M, int EPI = -1>
 constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M, EPI>() ? 4 : 1)) * 32; }
 
