@@ -40,6 +40,15 @@ DEEP_SCALE = 0.08   # residual scale of layers >= E: measured alpha ~0.73 (paper
 SEED = 0
 
 
+def bench_prompt(vocab, n=PROMPT_LEN, seed=SEED):
+    """The bench's synthetic prompt: n ids from the seeded `prompt` stream of
+    RngStream(derive_seed(seed, "run")) (pipesim.default_prompt's stream)."""
+    import paper_2509_19368_b200 as ppsd
+
+    pstream = ppsd.RngStream(ppsd.derive_seed(seed, "run")).split("prompt")
+    return [pstream.randbelow(vocab) for _ in range(n)]
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:

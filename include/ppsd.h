@@ -273,6 +273,17 @@ int ppsd_init_weight(void* dst_bf16, int32_t layout, int64_t rows, int64_t cols,
  * head (length vocab) — debugging / tolerance tests. */
 int ppsd_read_logits(ppsd_engine* e, int32_t which, float* out);
 
+/* Logits tap (parity tests): while set, single-rank ppsd_decode calls on a
+ * transformer engine copy every exit / final head's fp32 logits row into
+ * dev_tap[(pos * 2 + which) * vocab] (device buffer, which 0 = exit, 1 =
+ * final; pos = the generated position the row predicts, 1 .. max_pos). Rows
+ * of flushed chains are overwritten by the committed prefix's rows, so after
+ * a decode every position holds the logits its verdict / draft used. The
+ * scheduler kernel does the copies; the graphs are unchanged. NULL clears it.
+ * Replaces nothing in the reference: it is the GPU side of the logits
+ * tolerance check (the reference's ProbVecs, pipesim.py:743, :714). */
+int ppsd_set_logits_tap(ppsd_engine* e, float* dev_tap, int32_t max_pos);
+
 /* Kernel-time probe for the roofline: times `reps` launches of the engine's
  * dominant layer GEMV (gate/up) with CUDA events on the engine stream. */
 int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps,

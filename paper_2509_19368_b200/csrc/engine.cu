@@ -65,7 +65,8 @@ struct ppsd_engine {
   Work* d_work_p2 = nullptr;       // prefill: layers after the exit (exit-head layer)
   Work* d_work_head_pf = nullptr;  // prefill's exit-head layer
   float* d_part = nullptr;         // K-split down projection: second half's row sums
-  int32_t* d_part_flag = nullptr;  // ... and their per-chunk flags
+  int32_t* d_part_flag = nullptr;  // ... and their per-chunk sequence numbers
+  int32_t* d_kerr = nullptr;       // sticky GEMV error word (K-split wait timeout)
   bool hl = false;              // exit head has a decoder layer
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
@@ -182,6 +183,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   a.k_ld = p.K_full;
   a.part_buf = e->d_part;
   a.part_flag = e->d_part_flag;
+  a.err = e->d_kerr;
   return gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st);
 }
 
@@ -504,7 +506,7 @@ static void free_engine(ppsd_engine* e) {
     if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_work_head, e->d_work_p2,
-                  e->d_work_head_pf, e->d_part, e->d_part_flag, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+                  e->d_work_head_pf, e->d_part, e->d_part_flag, e->d_kerr, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
                   e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
@@ -610,6 +612,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   CU(dalloc(&e->d_arctl, sizeof(ArCtl)));
   CU(dalloc(&e->d_tokens, sizeof(int32_t) * (max_ctx + 8)));
   CU(dalloc(&e->d_eesd, sizeof(EesdState)));
+  CU(dalloc(&e->d_kerr, sizeof(int32_t)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&e->h_sched), sizeof(Sched)));
 
   TickCtx& c = e->h_ctx;
@@ -661,6 +664,10 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         (need_head && !w->lm_head))
       return fail(PPSD_EINVAL, "missing transformer weights");
     const int Rq = (d.H + 2 * d.KV) * d.hd;
+    // PPSD_DOWN_SPLIT (read per engine, recorded in the plan): 0 disables
+    // the K split of the down projection (DESIGN.md environment knobs)
+    const char* dsv = getenv("PPSD_DOWN_SPLIT");
+    const bool split_on = !(dsv && dsv[0] == '0') && e->lo == 1 && e->hi == e->S && ppsd::g_pdl;
     const int shapes[kNumMats][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d},
                                      {d.d, d.ffn}, {d.V, d.d}, {d.V, d.d}};
     for (int m = 0; m < kNumMats; ++m) {
@@ -670,9 +677,11 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         p.R = shapes[m][0];
         p.K = p.K_full = shapes[m][1];
         // Wide down projections (K > 8192): each grid half streams one column
-        // half (half the input slice per thread: no register boost in the
-        // 4-vector plan), in every plan, so M = 1 and batched results agree.
-        static const bool split_on = !(getenv("PPSD_DOWN_SPLIT") && getenv("PPSD_DOWN_SPLIT")[0] == '0');
+        // half (half the input slice per thread), in every plan, so M = 1 and
+        // batched results agree. The two halves exchange row sums through
+        // spin-waits, so the split runs only where the engine's grid owns the
+        // device: not for stage-subset engines (several may share one GPU)
+        // and not without PDL (PPSD_PDL=0 is the shared-device mode).
         if (m == kMatDown && split_on && p.K > 8192 && (p.K / 2) % 8 == 0 && e->num_sms % 2 == 0) {
           p.ksplit = 1;
           p.K = p.K / 2;
@@ -680,7 +689,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.sub, &p.smem) != 0)
           return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
                                              std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
-        CU(gemv_set_attrs(p.vpt, p.m, m, p.smem));
+        CU(gemv_set_attrs(p.vpt, p.m, m, p.ksplit, p.smem));
       }
     }
     {
@@ -758,7 +767,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_h, sizeof(float) * nb * d.ffn));
     if (e->gp[kMatDown].ksplit) {
       CU(dalloc(&e->d_part, sizeof(float) * nb * d.d));
-      CU(dalloc(&e->d_part_flag, sizeof(int32_t) * (size_t)e->num_sms * kSplitChunks));
+      CU(dalloc(&e->d_part_flag, sizeof(int32_t) * 2 * (size_t)e->num_sms * kSplitChunks));
     }
     CU(dalloc(&e->d_logits, sizeof(float) * (kMaxVec + 1) * (size_t)d.V));  // folded: exit + batch rows
     CU(dalloc(&e->d_attn_part, sizeof(float) * nb * d.H * e->max_pages * (d.hd + 2)));
@@ -827,6 +836,18 @@ extern "C" int ppsd_engine_destroy(ppsd_engine* e) {
 
 // ---------------------------------------------------------------------------
 // decode
+
+// Sticky GEMV error word (K-split wait timeout, gemv.cu): a decode whose
+// down projection gave up waiting for its partner's row sums is reported
+// as PPSD_ESTATE, never returned as tokens. Called after the stream drained.
+static int check_kerr(ppsd_engine* e) {
+  if (!e->gp[kMatDown].ksplit) return PPSD_OK;  // the only writer
+  int32_t v = 0;
+  CU(cudaMemcpy(&v, e->d_kerr, sizeof(v), cudaMemcpyDeviceToHost));
+  if (v == 0) return PPSD_OK;
+  CU(cudaMemset(e->d_kerr, 0, sizeof(v)));
+  return fail(PPSD_ESTATE, "K-split down projection: partner row sums timed out (results discarded)");
+}
 
 static int check_prompt(const ppsd_engine* e, const int32_t* prompt, int n_prompt) {
   if (n_prompt <= 0 || !prompt) return fail(PPSD_EINVAL, "prompt must be non-empty");
@@ -959,6 +980,7 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   CU(cudaStreamSynchronize(e->st));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  if (int rc = check_kerr(e)) return rc;
   if (s.error & kErrOrder) return fail(PPSD_ESTATE, "verdicts must land in position order");
   if (s.error & kErrTransit) return fail(PPSD_ESTATE, "transit queue overflow");
   if (s.error & kErrTrace) return fail(PPSD_ESTATE, "trace buffer too small");
@@ -1144,6 +1166,7 @@ extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, uint64_t rng_seed,
     launches += (int64_t)max_tokens * e->ar_launches;
   }
   CU(cudaEventSynchronize(e->ev1));
+  if (int rc2 = check_kerr(e)) return rc2;
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
   out->decode_ms = ms;
@@ -1270,6 +1293,7 @@ static int run_eesd(ppsd_engine* e, int model, int gamma, const int32_t* prompt,
   }
   CU(cudaEventRecord(e->ev1, e->st));
   CU(cudaEventSynchronize(e->ev1));
+  if (int rc2 = check_kerr(e)) return rc2;
   if (st.error & kErrTrace) return fail(PPSD_ESTATE, "trace buffer too small");
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
@@ -1399,11 +1423,23 @@ extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, 
   for (int i = 0; i < reps; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev1, e->st));
   CU(cudaEventSynchronize(e->ev1));
+  if (int rc = check_kerr(e)) return rc;
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
   const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
   *avg_ms = ms / reps;
   *bytes_per_launch = (double)p.R * (p.ksplit ? p.K_full : p.K) * 2.0 * (head ? 1 : ng);
+  return PPSD_OK;
+}
+
+extern "C" int ppsd_set_logits_tap(ppsd_engine* e, float* dev_tap, int32_t max_pos) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "logits tap needs a transformer engine");
+  if (dev_tap && max_pos < 1) return fail(PPSD_EINVAL, "max_pos must be >= 1");
+  e->h_ctx.tap = dev_tap;
+  e->h_ctx.tap_max = dev_tap ? max_pos : 0;
+  CU(cudaSetDevice(e->device));
+  CU(cudaMemcpyAsync(e->d_ctx, &e->h_ctx, sizeof(TickCtx), cudaMemcpyHostToDevice, e->st));
+  CU(cudaStreamSynchronize(e->st));
   return PPSD_OK;
 }
 

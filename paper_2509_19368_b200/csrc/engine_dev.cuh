@@ -69,6 +69,13 @@ struct TickCtx {
   Work* work_head;          // the head layer's work (copy source in src_slot)
   Work* work_p2;            // prefill: layers [split, N) of the chunk
   Work* work_head_pf;  // prefill's exit-head layer (the tick's work_head may already be planned)
+  // logits tap (ppsd_set_logits_tap, parity tests): single-rank transformer
+  // decodes copy the exit / final logits row each head produced into
+  // tap[(pos * 2 + which) * vocab], pos = the generated position it predicts
+  // (1 .. tap_max); a later row for the same position overwrites, so after
+  // the run each position holds the rows of its committed prefix
+  float* tap;
+  int32_t tap_max;
 };
 
 constexpr int kBoxHeader = 4;

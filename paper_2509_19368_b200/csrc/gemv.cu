@@ -108,14 +108,15 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
 // every plan uses 8.
 constexpr int nw_for(int /*vpt*/) { return 8; }
 
-// Register boost for the batched plans of wide-K matrices (the down
-// projection, VPT >= 5): their M=4 input slices need ~230 registers per
-// thread, but 9 warps cap every thread at 168 (allocation granularity is 4
-// warps). Those instantiations run a 4-warp producer warpgroup that hands its
-// registers to the consumers (setmaxnreg). Measured: the boost made the
-// K = 4096 batched plans slower, so only wide-K plans use it.
+// Register boost for the batched plans of wide-K matrices (VPT >= 5, and
+// the K-split down projection from VPT 3 on): their M=4 input slices need
+// ~230 registers per thread, but 9 warps cap every thread at 168 (allocation
+// granularity is 4 warps). Those instantiations run a 4-warp producer
+// warpgroup that hands its registers to the consumers (setmaxnreg).
+// Measured: the boost made the K = 4096 batched plans slower, so only wide-K
+// plans and the split down projection (13B K/2 = 6912: no spills) use it.
 template <int VPT, int M, int EPI = -1>
-constexpr bool reg_boost() { return (VPT >= 5 || (VPT >= 3 && EPI == kMatDown)) && M >= 4; }
+constexpr bool reg_boost() { return (VPT >= 5 || (VPT >= 3 && EPI == kMatDownS)) && M >= 4; }
 template <int VPT, int M, int EPI = -1>
 constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M, EPI>() ? 4 : 1)) * 32; }
 
@@ -126,6 +127,8 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (m=0) + final (m=1) head
   constexpr bool kHeadV = EPI == kMatHeadV;  // final head on the vectors of group 0
   constexpr bool kHead = kHead2 || kHeadV;
+  constexpr bool kDown = EPI == kMatDown || EPI == kMatDownS;
+  constexpr bool ksplit = EPI == kMatDownS;  // K split across the grid halves
   // M = 1 and the tick head: all loads of a tile first, release the stage,
   // then the math (the ring refills during it). Batched plans: weights are
   // loaded as the FMAs need them, so no register copy of the tile bounds TR,
@@ -184,11 +187,12 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
     return;
   }
   const int tpp = R / TR;
-  // K split: CTA kb of each grid half takes the same tiles, half kh its columns
-  const bool ksplit = EPI == kMatDown && a.ksplit;
+  // K split: CTA kb of each grid half takes the same tiles, column half kh.
+  // The publishing half (kh = 1) has the LOW block indices so it is
+  // dispatched first: a waiting CTA's partner is then already resident.
   const int kG = ksplit ? (int)gridDim.x / 2 : (int)gridDim.x;
-  const int kh = ksplit && (int)blockIdx.x >= kG ? 1 : 0;
-  const int kb = (int)blockIdx.x - kh * kG;
+  const int kh = ksplit && (int)blockIdx.x < kG ? 1 : 0;
+  const int kb = ksplit ? (int)blockIdx.x - (kh ? 0 : kG) : (int)blockIdx.x;
   long long t0, t1;
   int hv_p = 0, hv_c0 = 0, hv_c1 = 0;  // kHeadV: this CTA's problem and its CTA span
   if (kHeadV) {
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
             w = a.head_w;
           } else {
             const LayerW& L = a.layers[work->first[s_pg[p]] + a.layer_i];
-            w = EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;
+            w = EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o : EPI == kMatGU ? L.gu : L.down;  // kDown
           }
           wb = reinterpret_cast<const unsigned char*>(w);
           cur_p = p;
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
               if (EPI == kMatQKV) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.attn_norm; }
               if (EPI == kMatGU) { src[m] = a.x + (size_t)s * a.dm.d; nw[m] = L.mlp_norm; }
               if (EPI == kMatO) src[m] = a.o + (size_t)s * a.dm.H * a.dm.hd;
-              if (EPI == kMatDown) src[m] = a.h + (size_t)s * a.dm.ffn + (size_t)kh * K;
+              if (kDown) src[m] = a.h + (size_t)s * a.dm.ffn + (size_t)kh * K;
             }
           }
         }
@@ -482,12 +486,19 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
       const bool last_of_problem = (n == ntiles - 1) || (tip + 1 == tpp);
       if (ct == CHT - 1 || last_of_problem) {
         named_bar_sync(1, NC);
-        int* kflag = ksplit ? a.part_flag + (size_t)kb * kSplitChunks + (nchunk++ % kSplitChunks) : nullptr;
+        // K split: publication / consumption counts of this chunk slot
+        int* kpub = ksplit ? a.part_flag + (size_t)kb * kSplitChunks + (nchunk++ % kSplitChunks) : nullptr;
+        int* kcons = ksplit ? kpub + (size_t)gridDim.x * kSplitChunks : nullptr;
         if (ksplit && kh == 0) {  // wait for the second half's row sums of this chunk
           if (tid == 0) {
+            const int want = *kcons + 1;  // only this CTA writes its consumption count
             const uint64_t tw = globaltimer();
-            while (ld_acquire_gpu(kflag) == 0)
-              if (globaltimer() - tw > 2000000000ull) break;  // 2 s: wrong result, never a hang
+            while ((int)((unsigned)ld_acquire_gpu(kpub) - (unsigned)want) < 0)
+              if (globaltimer() - tw > 2000000000ull) {  // 2 s: sticky error, never a hang
+                atomicOr(a.err, kGemvErrSplitTimeout);
+                break;
+              }
+            *kcons = want;  // consumed (a late publication then pairs with this chunk, not the next)
           }
           named_bar_sync(1, NC);
         }
@@ -580,10 +591,7 @@ __global__ void __launch_bounds__(gemv_threads<VPT, M, EPI>(), 1) gemv_kernel(co
         }
         if (ksplit && kh == 1) __threadfence();  // row sums before the flag
         named_bar_sync(1, NC);
-        if (ksplit && tid == 0) {
-          if (kh == 1) st_release_gpu(kflag, 1);
-          else *kflag = 0;  // consumed: ready for the next launch
-        }
+        if (ksplit && kh == 1 && tid == 0) red_release_gpu_add(kpub, 1);  // publish
       }
       if (++tip == tpp) {
         tip = 0;
@@ -701,6 +709,7 @@ cudaError_t launch_vm(const GemvArgs& a, size_t smem, int grid, cudaStream_t st,
   if constexpr ((M == 1) || (M == m_batched(VPT))) {
     if (mat == kMatO) return launch_one<VPT, M, kMatO>(a, smem, grid, st, attrs_only);
     if (mat == kMatDown) return launch_one<VPT, M, kMatDown>(a, smem, grid, st, attrs_only);
+    if (mat == kMatDownS) return launch_one<VPT, M, kMatDownS>(a, smem, grid, st, attrs_only);
     if constexpr (tr_for(VPT, M) >= 2) {  // row-pair epilogues
       if (mat == kMatQKV) return launch_one<VPT, M, kMatQKV>(a, smem, grid, st, attrs_only);
       if (mat == kMatGU) return launch_one<VPT, M, kMatGU>(a, smem, grid, st, attrs_only);
@@ -774,13 +783,13 @@ int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int
   return 0;
 }
 
-cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem) {
+cudaError_t gemv_set_attrs(int vpt, int m, int mat, int ksplit, size_t smem) {
   GemvArgs dummy{};
-  return dispatch(dummy, vpt, m, smem, 0, 0, true, mat);
+  return dispatch(dummy, vpt, m, smem, 0, 0, true, mat == kMatDown && ksplit ? kMatDownS : mat);
 }
 
 cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st) {
-  return dispatch(a, vpt, m, smem, grid, st, false, a.mat);
+  return dispatch(a, vpt, m, smem, grid, st, false, a.mat == kMatDown && a.ksplit ? kMatDownS : a.mat);
 }
 
 }  // namespace ppsd

@@ -48,6 +48,9 @@ struct Dims {
 
 enum : int { kMatQKV = 0, kMatO = 1, kMatGU = 2, kMatDown = 3, kMatHead = 4, kMatHeadV = 5 };
 constexpr int kNumMats = 6;
+// gemv_kernel instantiation tag (not a matrix index): the down projection
+// split over K across the two grid halves (GemvArgs.ksplit = 1)
+constexpr int kMatDownS = 6;
 
 struct GemvArgs {
   Work* work;
@@ -72,14 +75,21 @@ struct GemvArgs {
   float* head_part;  // [grid][kMaxVec][2] (value, index-as-float bits)
   int32_t* head_cnt; // [kMaxVec] arrival tickets
   // K split (wide down projections, ksplit = 1): the two halves of the grid
-  // stream the two column halves [h*K, h*K + K) of rows k_ld long; the
-  // second half publishes its row sums (part_buf + part_flag), the first
-  // adds them in fixed order before the residual add
+  // stream the two column halves [h*K, h*K + K) of rows k_ld long; the CTAs
+  // streaming the second column half (low blockIdx, dispatched first)
+  // publish their row sums (part_buf + a publication count), their partners
+  // add them in fixed order before the residual add
   int32_t ksplit, k_ld;
   float* part_buf;     // [nslot][d]
-  int32_t* part_flag;  // [grid/2][kSplitChunks]
+  // [2][grid][kSplitChunks] monotone sequence numbers per (CTA pair, chunk
+  // slot): [0] publications by the second-half CTA, [1] consumptions by its
+  // partner. A wait is for "publications > consumptions", so a late or
+  // stale publication can never be mistaken for a later one.
+  int32_t* part_flag;
+  int32_t* err;  // sticky device error word (kGemvErrSplitTimeout), checked by the host
 };
-constexpr int kSplitChunks = 64;  // epilogue chunks per CTA pair
+constexpr int kSplitChunks = 64;  // epilogue chunk slots per CTA pair (sequence-numbered, may wrap)
+constexpr int kGemvErrSplitTimeout = 1;
 
 struct AttnArgs {
   const Work* work;
@@ -151,7 +161,7 @@ cudaError_t launch_pdl(Kern fn, dim3 grid, dim3 block, size_t smem, cudaStream_t
 int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, int* sub,
               size_t* smem);
 cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st);
-cudaError_t gemv_set_attrs(int vpt, int m, int mat, size_t smem);
+cudaError_t gemv_set_attrs(int vpt, int m, int mat, int ksplit, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 bool umma_shape_ok(int R, int K);

@@ -191,6 +191,27 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
     }
     __syncthreads();
   }
+  if (!begin && c.tap && c.logits32 && !inbox) {  // logits tap, before sched_finish moves the chains
+    __shared__ int s_tp[2], s_trow[2];
+    if (threadIdx.x == 0) {
+      // exit head: folded, the chain launched last tick (eager shallow stages);
+      // pipelined, the chain at the exit stage. Final head: the chain at
+      // stage S (folded: its row of the deep batch).
+      const int es = c.fold ? (s.launched ? s.work[1] : -1) : s.exit_slot;
+      s_tp[0] = es >= 0 ? s.ch_pos[es] : -1;
+      s_trow[0] = 0;
+      s_tp[1] = s.final_slot >= 0 ? s.ch_pos[s.final_slot] : -1;
+      s_trow[1] = c.fold ? 1 + s_tp[1] - s.fold_base : 1;
+    }
+    __syncthreads();
+    for (int wh = 0; wh < 2; ++wh) {
+      const int p = s_tp[wh];
+      if (p < 1 || p > c.tap_max) continue;
+      const float* src = c.logits32 + (size_t)s_trow[wh] * c.vocab;
+      float* dst = c.tap + ((size_t)p * 2 + wh) * c.vocab;
+      for (int i = threadIdx.x; i < c.vocab; i += blockDim.x) dst[i] = src[i];
+    }
+  }
   if (threadIdx.x == 0) {
     int exit_tok = s_exit_tok, final_tok = s_final_tok;
     if (inbox && c.greedy) {  // replicated scheduler: head results come from their owners' boxes

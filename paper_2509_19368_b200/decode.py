@@ -182,6 +182,21 @@ class Engine:
                    "read_logits")
         return out
 
+    def set_logits_tap(self, tap=None) -> None:
+        """Parity tests: while `tap` (a CUDA float32 tensor [P+1, 2, vocab]) is
+        set, decode() leaves the exit (index 0) and final (index 1) logits row
+        of the committed prefix at every generated position 1..P in it
+        (include/ppsd.h ppsd_set_logits_tap). None clears it."""
+        if tap is None:
+            _lib.check(_lib.lib().ppsd_set_logits_tap(self.h, None, 0), "set_logits_tap")
+            self._tap = None
+            return
+        if tap.dim() != 3 or tap.shape[1] != 2 or tap.shape[2] != self._vocab or not tap.is_contiguous():
+            raise ValueError("tap must be a contiguous [P+1, 2, vocab] tensor")
+        self._tap = tap  # keep alive while the engine holds the pointer
+        _lib.check(_lib.lib().ppsd_set_logits_tap(self.h, C.c_void_p(tap.data_ptr()), tap.shape[0] - 1),
+                   "set_logits_tap")
+
     def probe_gemv(self, which: int, n_groups: int, reps: int = 20):
         ms, nbytes = C.c_double(), C.c_double()
         _lib.check(_lib.lib().ppsd_probe_gemv(self.h, which, n_groups, reps, C.byref(ms), C.byref(nbytes)),
