@@ -48,7 +48,7 @@ EXIT_DEPTH = 8
 DEEP_SCALE = 0.08   # residual scale of layers >= E: measured alpha ~0.73 (paper V7B E=8: 0.67-0.81)
 SEED = 0
 NOMINAL_HBM_GBS = 8000.0   # BASELINE.md §4's denominator (B200 nominal)
-REF_STEP_TOKENS = 32       # tokens per reference-arm step (a bounded sample)
+REF_STEP_TOKENS = 16       # tokens per reference-arm step (a bounded sample: W+K=25 steps ~ 2.5 min)
 EESD_GAMMAS = (5, 10)
 # BASELINE.json configs by GPU count: (model, exit depth)
 DEFAULTS_BY_N = {1: ("7b", 8), 2: ("13b", 20), 4: ("70b", 20), 8: ("70b", 10)}
