@@ -289,6 +289,12 @@ int ppsd_set_logits_tap(ppsd_engine* e, float* dev_tap, int32_t max_pos);
 int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, int32_t reps,
                     double* avg_ms, double* bytes_per_launch);
 
+/* Kernel-time probe of decode attention: one group of n_vec query vectors,
+ * longest context ctx, timed over `reps` launches on the engine stream;
+ * bytes = the K/V rows one launch must read. */
+int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32_t reps, double* avg_ms,
+                    double* bytes_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

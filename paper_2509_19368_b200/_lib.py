@@ -121,6 +121,8 @@ EXPORTS = {
                                    C.c_int32, C.c_void_p]),
     "ppsd_read_logits": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_float)]),
     "ppsd_set_logits_tap": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "ppsd_probe_attn": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]),
     "ppsd_probe_gemv": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }

@@ -197,6 +197,12 @@ class Engine:
         _lib.check(_lib.lib().ppsd_set_logits_tap(self.h, C.c_void_p(tap.data_ptr()), tap.shape[0] - 1),
                    "set_logits_tap")
 
+    def probe_attn(self, n_vec: int, ctx: int, reps: int = 20):
+        ms, nbytes = C.c_double(), C.c_double()
+        _lib.check(_lib.lib().ppsd_probe_attn(self.h, n_vec, ctx, reps, C.byref(ms), C.byref(nbytes)),
+                   "probe_attn")
+        return ms.value, nbytes.value
+
     def probe_gemv(self, which: int, n_groups: int, reps: int = 20):
         ms, nbytes = C.c_double(), C.c_double()
         _lib.check(_lib.lib().ppsd_probe_gemv(self.h, which, n_groups, reps, C.byref(ms), C.byref(nbytes)),
