@@ -45,45 +45,76 @@ namespace cg = cooperative_groups;
 namespace ppsd {
 
 constexpr int kDecRowsChunk = 16;  // query rows scored together (registers)
+constexpr int kDecMaxWorkers = 4;  // 128-thread page workers per CTA (128 registers per thread)
 
 struct DecLayout {  // dynamic shared memory carve-up, identical on host and device
-  size_t ring, part, qs, sc, total;
+  size_t ring, sc, qs, part, se, total;
 };
 
+// W workers per CTA, C CTAs per cluster (pages C*W), qmax query rows
 template <int HD, typename KVT>
-__host__ __device__ inline DecLayout dec_layout(int nb, int ppc, int qmax) {
+__host__ __device__ inline DecLayout dec_layout(int W, int C, int qmax) {
   DecLayout L;
   const size_t page = 2 * (size_t)kPage * HD * sizeof(KVT);  // K block + V block
+  const int rc = qmax < kDecRowsChunk ? qmax : kDecRowsChunk;
   L.ring = 0;
-  L.part = L.ring + (size_t)nb * page;
-  L.qs = L.part + (size_t)ppc * qmax * (HD + 2) * sizeof(float);
-  L.sc = L.qs + (size_t)qmax * HD * sizeof(float);
-  L.total = L.sc + (size_t)kDecRowsChunk * kPage * sizeof(float);
+  L.sc = L.ring + (size_t)W * page;
+  L.qs = L.sc + (size_t)W * rc * kPage * sizeof(float);
+  L.part = L.qs + (size_t)qmax * HD * sizeof(float);
+  L.se = L.part + (size_t)C * W * qmax * (HD + 2) * sizeof(float);
+  L.total = L.se + (size_t)qmax * (kMergePages + 1) * sizeof(float);
   return L;
 }
 
+// Scores of rows r0 .. r0+RC (RC <= RCT) of one worker against its K page
+// (attn_core.cuh arithmetic per (row, token)). Row q's context in the page
+// is n(q) tokens; tokens past the longest (nmax) are not scored.
+template <int HD, typename KVT, int QPK, int RCT, class NF>
+__device__ __forceinline__ void page_scores(const KVT* ks, const float* qs, float* sc, int r0, int RC, int nmax,
+                                            int wwarp, int lane, float scale, NF nrow) {
+  constexpr int EPV = 16 / (int)sizeof(KVT);
+  constexpr int LPT = HD / EPV;
+  constexpr int TPW = 32 / LPT;
+  const int li = lane % LPT, tw = lane / LPT;
+  for (int base = wwarp * TPW; base < nmax; base += 4 * TPW) {
+    const int tt = base + tw;
+    float kf[EPV];
+    if (tt < nmax) unpack16<KVT>(lds128(ks + (size_t)tt * HD + li * EPV), kf);
+    float prt[RCT];
+#pragma unroll
+    for (int q = 0; q < RCT; ++q) {
+      prt[q] = 0.f;
+      if (q < RC && tt < nmax) {
+        const float* qr = qs + (size_t)(r0 + q) * HD + li * EPV;
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) prt[q] = fmaf(kf[e], qr[e], prt[q]);
+      }
+    }
+#pragma unroll
+    for (int off = LPT / 2; off > 0; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < RCT; ++q) prt[q] += __shfl_xor_sync(0xffffffffu, prt[q], off);
+    if (li == 0)
+#pragma unroll
+      for (int q = 0; q < RCT; ++q)
+        if (q < RC && tt < nrow(r0 + q)) sc[q * kPage + tt] = prt[q] * scale;
+  }
+}
+
 template <int HD, typename KVT, int QPK>
-__global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArgs a) {
-  constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte vector
-  constexpr int LPT = HD / EPV;                // lanes per token
-  constexpr int TPW = 32 / LPT;                // tokens per warp pass
-  constexpr int BLK = kPage * HD;              // elements per K (or V) page block
-  static_assert(LPT >= 1 && LPT <= 32 && (32 % LPT) == 0, "head_dim / dtype combination");
+__global__ void __launch_bounds__(kAttnThreads* kDecMaxWorkers) attn_decode_kernel(const AttnArgs a) {
+  constexpr int BLK = kPage * HD;  // elements per K (or V) page block
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bar[4];
-  __shared__ float s_m[kDecRowsChunk], s_l[kDecRowsChunk];
-  __shared__ float s_e[kMergePages];
-  __shared__ float s_L;
+  __shared__ uint64_t bar[kDecMaxWorkers];
+  __shared__ float s_m[kDecMaxWorkers][kDecRowsChunk], s_l[kDecMaxWorkers][kDecRowsChunk];
 
   cg::cluster_group cluster = cg::this_cluster();
-  const int C = a.dec_c, nb = a.dec_nb, ppc = a.dec_ppc, qmax = a.dec_qmax;
-  const DecLayout lay = dec_layout<HD, KVT>(nb, ppc, qmax);
-  KVT* ring = reinterpret_cast<KVT*>(smem + lay.ring);
-  float* part = reinterpret_cast<float*>(smem + lay.part);  // [ppc][qmax][HD + 2]
-  float* qs = reinterpret_cast<float*>(smem + lay.qs);      // [qmax][HD]
-  float* sc = reinterpret_cast<float*>(smem + lay.sc);      // [kDecRowsChunk][kPage]
+  const int C = a.dec_c, W = a.dec_w, qmax = a.dec_qmax;
+  const DecLayout lay = dec_layout<HD, KVT>(W, C, qmax);
+  const int rcmax = qmax < kDecRowsChunk ? qmax : kDecRowsChunk;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int wk = tid >> 7, wt = tid & 127, wwarp = wt >> 5;  // page worker, its thread / warp
   const int cr = (int)cluster.block_rank();
   const int row = (int)blockIdx.x / C;
   const int H = a.dm.H, KVh = a.dm.KV;
@@ -109,87 +140,59 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArg
   const int pos0 = w->pos[g], nv = w->nv[g], slot0 = w->slot[g];
   const int Q = nv * QPK;
   const int nch = (pos0 + nv - 1 + kPage) / kPage;  // pages of the longest context
-  const int my_n = cr < nch ? (nch - 1 - cr) / C + 1 : 0;  // pages this CTA owns
+  const int c = wk * C + cr;                        // this worker's page
+  const bool active = c < nch;
+  const int nmax = active ? min(kPage, pos0 + nv - c * kPage) : 0;  // rows of the page, longest context
+  auto nrow = [&](int q) { return min(kPage, pos0 + q / QPK + 1 - c * kPage); };
   const int gl = w->first[g] + a.layer_i;
   const int lloc = gl == a.hl_global ? a.hl_local : gl - a.first_local;
   const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
+  KVT* ks = reinterpret_cast<KVT*>(smem + lay.ring) + (size_t)wk * 2 * BLK;
+  const KVT* vs = ks + BLK;
+  float* sc = reinterpret_cast<float*>(smem + lay.sc) + (size_t)wk * rcmax * kPage;
+  float* qs = reinterpret_cast<float*>(smem + lay.qs);  // [Q][HD]
+  // partials live in the cluster leader's shared memory: [page][qmax][HD + 2]
+  float* part0 = cluster.map_shared_rank(reinterpret_cast<float*>(smem + lay.part), 0);
 
-  if (tid == 0) {
-    for (int i = 0; i < nb; ++i) mbar_init(&bar[i], 1);
+  if (wt == 0) {
+    mbar_init(&bar[wk], 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  // page j of this CTA (global page cr + j*C), into ring slot j % nb
-  auto issue = [&](int j) {
-    const int c = cr + j * C;
-    const int n = min(kPage, pos0 + nv - c * kPage);  // rows of the page in the longest context
-    const int page = a.page_table[c];
-    const size_t blk = ((size_t)page * KVh + kvh) * BLK;
-    const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
-    KVT* ks = ring + (size_t)(j % nb) * 2 * BLK;
-    mbar_expect_tx(&bar[j % nb], 2 * bytes);
-    bulk_g2s(ks, reinterpret_cast<const KVT*>(kvl) + blk, bytes, &bar[j % nb]);
-    bulk_g2s(ks + BLK, reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes) + blk, bytes, &bar[j % nb]);
+  named_bar_sync(1 + wk, kAttnThreads);
+  auto issue = [&]() {  // worker thread 0: the page's K and V blocks, one mbarrier
+    const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;
+    const uint32_t bytes = (uint32_t)(nmax * HD * sizeof(KVT));
+    mbar_expect_tx(&bar[wk], 2 * bytes);
+    bulk_g2s(ks, reinterpret_cast<const KVT*>(kvl) + blk, bytes, &bar[wk]);
+    bulk_g2s(ks + BLK, reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes) + blk, bytes, &bar[wk]);
   };
-  // a page entirely below the first position this layer's QKV kernel writes is final
-  int issued = 0;
-  if (tid == 0)
-    while (issued < min(my_n, nb) && (cr + issued * C + 1) * kPage <= pos0) issue(issued++);
+  // a page entirely below the first position this layer's QKV kernel writes
+  // is final: fetch it while the previous kernel drains
+  const bool early = active && (c + 1) * kPage <= pos0;
+  if (early && wt == 0) issue();
   pdl_wait();     // q and this layer's new K/V rows are visible from here on
   pdl_trigger();  // the O projection may start streaming its weights
-  if (tid == 0)
-    while (issued < min(my_n, nb)) issue(issued++);
-  for (int i = tid; i < Q * HD; i += kAttnThreads) {
+  if (active && !early && wt == 0) issue();
+  for (int i = tid; i < Q * HD; i += blockDim.x) {
     const int v = i / (QPK * HD), rem = i - v * QPK * HD;
     qs[i] = a.q[(size_t)(slot0 + v) * H * HD + (size_t)kvh * QPK * HD + rem];
   }
   __syncthreads();
 
-  const int li = lane % LPT, tw = lane / LPT;
-  for (int j = 0; j < my_n; ++j) {
-    const int c = cr + j * C;
-    mbar_wait(&bar[j % nb], (j / nb) & 1);
-    const KVT* ks = ring + (size_t)(j % nb) * 2 * BLK;
-    const KVT* vs = ks + BLK;
-    float* pj = part + (size_t)j * qmax * (HD + 2);
+  if (active) {
+    mbar_wait(&bar[wk], 0);
     for (int r0 = 0; r0 < Q; r0 += kDecRowsChunk) {
       const int RC = min(kDecRowsChunk, Q - r0);
-      const int nmax = min(kPage, pos0 + nv - c * kPage);
-      // scores (rows r0 .. r0+RC of this chunk; row r = vector r / QPK)
-      for (int base = warp * TPW; base < nmax; base += 4 * TPW) {
-        const int tt = base + tw;
-        float kf[EPV];
-        if (tt < nmax) unpack16<KVT>(lds128(ks + (size_t)tt * HD + li * EPV), kf);
-        float prt[kDecRowsChunk];
-#pragma unroll
-        for (int q = 0; q < kDecRowsChunk; ++q) {
-          prt[q] = 0.f;
-          if (q < RC && tt < nmax) {
-            const float* qr = qs + (size_t)(r0 + q) * HD + li * EPV;
-#pragma unroll
-            for (int e = 0; e < EPV; ++e) prt[q] = fmaf(kf[e], qr[e], prt[q]);
-          }
-        }
-#pragma unroll
-        for (int off = LPT / 2; off > 0; off >>= 1)
-#pragma unroll
-          for (int q = 0; q < kDecRowsChunk; ++q) prt[q] += __shfl_xor_sync(0xffffffffu, prt[q], off);
-        if (li == 0)
-#pragma unroll
-          for (int q = 0; q < kDecRowsChunk; ++q) {
-            if (q >= RC) break;
-            const int n = min(kPage, pos0 + (r0 + q) / QPK + 1 - c * kPage);
-            if (tt < n) sc[q * kPage + tt] = prt[q] * scale;
-          }
-      }
-      __syncthreads();
-      for (int q = warp; q < RC; q += 4) {  // chunk-local softmax statistics
-        const int n = min(kPage, pos0 + (r0 + q) / QPK + 1 - c * kPage);
+      if (RC == 1) page_scores<HD, KVT, QPK, 1>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
+      else if (RC <= 2) page_scores<HD, KVT, QPK, 2>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
+      else if (RC <= 4) page_scores<HD, KVT, QPK, 4>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
+      else if (RC <= 8) page_scores<HD, KVT, QPK, 8>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
+      else page_scores<HD, KVT, QPK, 16>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
+      named_bar_sync(1 + wk, kAttnThreads);
+      for (int q = wwarp; q < RC; q += 4) {  // chunk-local softmax statistics
+        const int n = nrow(r0 + q);
         float* sr = sc + q * kPage;
-        if (n <= 0) {
-          if (lane == 0) { s_m[q] = -FLT_MAX; s_l[q] = 0.f; }
-          continue;
-        }
+        if (n <= 0) continue;  // the page is past this vector's context
         float mx = -FLT_MAX;
         for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, sr[tt]);
         mx = warp_max(mx);
@@ -200,66 +203,64 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_kernel(const AttnArg
           l += p;
         }
         l = warp_sum(l);
-        if (lane == 0) { s_m[q] = mx; s_l[q] = l; }
+        if (lane == 0) { s_m[wk][q] = mx; s_l[wk][q] = l; }
       }
-      __syncthreads();
-      for (int idx = tid; idx < RC * HD; idx += kAttnThreads) {
-        const int q = idx / HD, d = idx - q * HD;
-        const int n = min(kPage, pos0 + (r0 + q) / QPK + 1 - c * kPage);
-        float acc = 0.f;
-#pragma unroll 8
-        for (int tt = 0; tt < n; ++tt) acc = fmaf(sc[q * kPage + tt], tof(vs[(size_t)tt * HD + d]), acc);
-        pj[(size_t)(r0 + q) * (HD + 2) + d] = acc;
+      named_bar_sync(1 + wk, kAttnThreads);
+      // PV: each thread owns dims d = wt (+128) of every row of the chunk;
+      // the rows' accumulators advance together (ILP), each in token order
+      for (int d = wt; d < HD; d += kAttnThreads) {
+        float acc[kDecRowsChunk];
+#pragma unroll
+        for (int q = 0; q < kDecRowsChunk; ++q) acc[q] = 0.f;
+        for (int tt = 0; tt < nmax; ++tt) {
+          const float vv = tof(vs[(size_t)tt * HD + d]);
+#pragma unroll
+          for (int q = 0; q < kDecRowsChunk; ++q)
+            if (q < RC && tt < nrow(r0 + q)) acc[q] = fmaf(sc[q * kPage + tt], vv, acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kDecRowsChunk; ++q)
+          if (q < RC && nrow(r0 + q) > 0) part0[((size_t)c * qmax + r0 + q) * (HD + 2) + d] = acc[q];
       }
-      if (tid < RC) {
-        pj[(size_t)(r0 + tid) * (HD + 2) + HD] = s_m[tid];
-        pj[(size_t)(r0 + tid) * (HD + 2) + HD + 1] = s_l[tid];
+      if (wt < RC && nrow(r0 + wt) > 0) {
+        part0[((size_t)c * qmax + r0 + wt) * (HD + 2) + HD] = s_m[wk][wt];
+        part0[((size_t)c * qmax + r0 + wt) * (HD + 2) + HD + 1] = s_l[wk][wt];
       }
-      __syncthreads();
+      named_bar_sync(1 + wk, kAttnThreads);
     }
-    // refill this ring slot with the page nb ahead (its reads are done)
-    if (tid == 0 && j + nb < my_n) issue(j + nb);
   }
 
-  cluster.sync();  // every page partial of the row is in some CTA's shared memory
+  cluster.sync();  // every page partial of the row is in the leader's shared memory
+  if (cr != 0) return;
 
-  // ---- merge rows cr, cr + C, ... in page order over DSMEM
-  for (int q = cr; q < Q; q += C) {
+  // ---- leader: merge each row over its pages in page order
+  const float* part = reinterpret_cast<const float*>(smem + lay.part);
+  float* se = reinterpret_cast<float*>(smem + lay.se);  // [Q][kMergePages] page weights, then [Q] sums
+  const int nwarps = blockDim.x >> 5, warp = tid >> 5;
+  for (int q = warp; q < Q; q += nwarps) {
+    const int nq = (pos0 + q / QPK + kPage) / kPage;
+    float mv = -FLT_MAX;
+    for (int cc = lane; cc < nq; cc += 32) mv = fmaxf(mv, part[((size_t)cc * qmax + q) * (HD + 2) + HD]);
+    mv = warp_max(mv);
+    float Ls = 0.f;
+    for (int cc = lane; cc < nq; cc += 32) {
+      const float* pp = part + ((size_t)cc * qmax + q) * (HD + 2);
+      const float e = expf(pp[HD] - mv);
+      se[q * kMergePages + cc] = e;  // page weight
+      Ls = fmaf(pp[HD + 1], e, Ls);
+    }
+    Ls = warp_sum(Ls);
+    if (lane == 0) se[qmax * kMergePages + q] = Ls;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < Q * HD; idx += blockDim.x) {
+    const int q = idx / HD, d = idx - q * HD;
     const int v = q / QPK, i = q - v * QPK;
-    const int nq = (pos0 + v + kPage) / kPage;  // pages of this vector's context
-    auto pptr = [&](int cc) {                    // partial row of page cc (peer smem)
-      float* base = cluster.map_shared_rank(part, cc % C);
-      return base + ((size_t)(cc / C) * qmax + q) * (HD + 2);
-    };
-    if (warp == 0) {
-      float mv = -FLT_MAX;
-      for (int cc = lane; cc < nq; cc += 32) mv = fmaxf(mv, pptr(cc)[HD]);
-      mv = warp_max(mv);
-      float Ls = 0.f;
-      for (int cc = lane; cc < nq; cc += 32) {
-        const float* pp = pptr(cc);
-        const float e = expf(pp[HD] - mv);
-        s_e[cc] = e;  // page weight
-        Ls = fmaf(pp[HD + 1], e, Ls);
-      }
-      Ls = warp_sum(Ls);
-      if (lane == 0) s_L = Ls;
-    }
-    __syncthreads();
-    for (int d = tid; d < HD; d += kAttnThreads) {
-      float pv[kMergePages];
-#pragma unroll
-      for (int cc = 0; cc < kMergePages; ++cc)
-        if (cc < nq) pv[cc] = pptr(cc)[d];
-      float O = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < kMergePages; ++cc)
-        if (cc < nq) O = fmaf(pv[cc], s_e[cc], O);
-      a.o[(size_t)(slot0 + v) * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / s_L;
-    }
-    __syncthreads();
+    const int nq = (pos0 + v + kPage) / kPage;
+    float O = 0.f;
+    for (int cc = 0; cc < nq; ++cc) O = fmaf(part[((size_t)cc * qmax + q) * (HD + 2) + d], se[q * kMergePages + cc], O);
+    a.o[(size_t)(slot0 + v) * H * HD + ((size_t)kvh * QPK + i) * HD + d] = O / se[qmax * kMergePages + q];
   }
-  cluster.sync();  // peers may still read this CTA's partials
 }
 
 namespace {
@@ -273,7 +274,7 @@ cudaError_t dec_launch_k(const AttnArgs& a, int rows, cudaStream_t st, bool attr
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(rows * a.dec_c);
-  cfg.blockDim = dim3(kAttnThreads);
+  cfg.blockDim = dim3(kAttnThreads * a.dec_w);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
@@ -316,7 +317,7 @@ size_t dec_smem(const AttnArgs& a) {
   auto f = [&](auto hdc, auto kvt) {
     constexpr int HDc = decltype(hdc)::value;
     using KVT = decltype(kvt);
-    return dec_layout<HDc, KVT>(a.dec_nb, a.dec_ppc, a.dec_qmax).total;
+    return dec_layout<HDc, KVT>(a.dec_w, a.dec_c, a.dec_qmax).total;
   };
   using I16 = std::integral_constant<int, 16>;
   using I32 = std::integral_constant<int, 32>;
@@ -333,25 +334,23 @@ size_t dec_smem(const AttnArgs& a) {
 }
 }  // namespace
 
-// Plan a decode-attention launch for rows = gmax * KV rows of up to nvmax
-// query vectors each: cluster size C (largest power of two <= 8 keeping
-// rows * C within two CTAs per SM and C <= pages), pages per CTA, ring depth.
-// Returns false when the plan does not fit shared memory (the caller then
-// launches the split-K kernel, attn_core.cuh: same arithmetic).
+// Plan a decode-attention launch for gmax * KV rows of up to nvmax query
+// vectors each: one cluster of C CTAs per row, W 128-thread page workers per
+// CTA, C * W >= the engine's pages. C is the largest power of two <= 8 with
+// rows * C <= 2 CTAs per SM. Returns false when the plan does not fit (the
+// caller then launches the split-K kernel, attn_core.cuh: same arithmetic).
 bool attn_decode_plan(AttnArgs* a, int gmax, int nvmax, int num_sms) {
   const int rows = gmax * a->dm.KV;
   const int qpk = a->dm.H / a->dm.KV;
   if (nvmax < 1 || a->max_pages > kMergePages || a->max_pages < 1) return false;
   int C = 8;
   while (C > 1 && (rows * C > 2 * num_sms || C > a->max_pages)) C >>= 1;
+  const int W = (a->max_pages + C - 1) / C;
+  if (W > kDecMaxWorkers) return false;
   a->dec_c = C;
-  a->dec_ppc = (a->max_pages + C - 1) / C;
+  a->dec_w = W;
   a->dec_qmax = nvmax * qpk;
-  for (int nb = std::min(a->dec_ppc, 3); nb >= 1; --nb) {
-    a->dec_nb = nb;
-    if (dec_smem(*a) <= 220 * 1024) return true;
-  }
-  return false;
+  return dec_smem(*a) <= 220 * 1024;
 }
 
 // the dynamic shared-memory ceiling every plan stays under (attn_decode_plan)

@@ -109,8 +109,8 @@ struct AttnArgs {
   int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
   int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
   // decode kernel plan (attn_decode.cu, attn_decode_plan): cluster size,
-  // ring slots, pages per CTA, query rows per row (nv * H/KV) at most
-  int32_t dec_c, dec_nb, dec_ppc, dec_qmax;
+  // 128-thread page workers per CTA, query rows per row (nv * H/KV) at most
+  int32_t dec_c, dec_w, dec_qmax;
 };
 
 // tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
