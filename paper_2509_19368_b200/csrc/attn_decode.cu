@@ -66,15 +66,19 @@ __host__ __device__ inline DecLayout dec_layout(int W, int C, int qmax) {
   return L;
 }
 
-// Scores of rows r0 .. r0+RC (RC <= RCT) of one worker against its K page
-// (attn_core.cuh arithmetic per (row, token)). Row q's context in the page
-// is n(q) tokens; tokens past the longest (nmax) are not scored.
-template <int HD, typename KVT, int QPK, int RCT, class NF>
-__device__ __forceinline__ void page_scores(const KVT* ks, const float* qs, float* sc, int r0, int RC, int nmax,
-                                            int wwarp, int lane, float scale, NF nrow) {
+// One worker (128 threads, named barrier `wbar`) runs rows r0 .. r0+RC
+// (RC <= RCT) of its page: scores, chunk-local softmax, PV, and pushes the
+// partials (o[HD], m, l) of the rows whose context reaches the page into the
+// cluster leader's shared memory `pdst` ([page][qmax][HD + 2]). Row q's
+// context in the page is nq[q] tokens (attn_core.cuh arithmetic per row).
+template <int HD, typename KVT, int RCT>
+__device__ __forceinline__ void page_rows(const KVT* ks, const KVT* vs, const float* qs, float* sc, float* s_m,
+                                          float* s_l, float* pdst, int r0, int RC, int nmax, const int (&nq)[RCT],
+                                          const int* s_nq, int wt, int lane, int wbar, float scale) {
   constexpr int EPV = 16 / (int)sizeof(KVT);
   constexpr int LPT = HD / EPV;
   constexpr int TPW = 32 / LPT;
+  const int wwarp = wt >> 5;
   const int li = lane % LPT, tw = lane / LPT;
   for (int base = wwarp * TPW; base < nmax; base += 4 * TPW) {
     const int tt = base + tw;
@@ -97,8 +101,59 @@ __device__ __forceinline__ void page_scores(const KVT* ks, const float* qs, floa
     if (li == 0)
 #pragma unroll
       for (int q = 0; q < RCT; ++q)
-        if (q < RC && tt < nrow(r0 + q)) sc[q * kPage + tt] = prt[q] * scale;
+        if (tt < nq[q]) sc[q * kPage + tt] = prt[q] * scale;
   }
+  named_bar_sync(wbar, kAttnThreads);
+  for (int q = wwarp; q < RC; q += 4) {  // chunk-local softmax statistics
+    const int n = s_nq[q];
+    float* sr = sc + q * kPage;
+    if (n <= 0) continue;  // the page is past this vector's context
+    float mx = -FLT_MAX;
+    for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, sr[tt]);
+    mx = warp_max(mx);
+    float l = 0.f;
+    for (int tt = lane; tt < n; tt += 32) {
+      const float p = expf(sr[tt] - mx);
+      sr[tt] = p;
+      l += p;
+    }
+    l = warp_sum(l);
+    if (lane == 0) { s_m[q] = mx; s_l[q] = l; }
+  }
+  named_bar_sync(wbar, kAttnThreads);
+  // PV: thread wt owns dim d of every row; the rows' accumulators advance
+  // together (ILP), each over its tokens in order
+  for (int d = wt; d < HD; d += kAttnThreads) {
+    float acc[RCT];
+#pragma unroll
+    for (int q = 0; q < RCT; ++q) acc[q] = 0.f;
+#pragma unroll 4
+    for (int tt = 0; tt < nmax; ++tt) {
+      const float vv = tof(vs[(size_t)tt * HD + d]);
+#pragma unroll
+      for (int q = 0; q < RCT; ++q)
+        if (tt < nq[q]) acc[q] = fmaf(sc[q * kPage + tt], vv, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RCT; ++q)
+      if (nq[q] > 0) pdst[(size_t)(r0 + q) * (HD + 2) + d] = acc[q];
+  }
+  if (wt < RC && s_nq[wt] > 0) {
+    pdst[(size_t)(r0 + wt) * (HD + 2) + HD] = s_m[wt];
+    pdst[(size_t)(r0 + wt) * (HD + 2) + HD + 1] = s_l[wt];
+  }
+  named_bar_sync(wbar, kAttnThreads);
+}
+
+template <int HD, typename KVT, int RCT, class NF>
+__device__ __forceinline__ void page_chunk(const KVT* ks, const KVT* vs, const float* qs, float* sc, float* s_m,
+                                           float* s_l, int* s_nq, float* pdst, int r0, int RC, int nmax, NF nrow,
+                                           int wt, int lane, int wbar, float scale) {
+  int nq[RCT];
+#pragma unroll
+  for (int q = 0; q < RCT; ++q) nq[q] = q < RC ? nrow(r0 + q) : 0;
+  if (wt < RC) s_nq[wt] = nrow(r0 + wt);  // read after the worker barrier below
+  page_rows<HD, KVT, RCT>(ks, vs, qs, sc, s_m, s_l, pdst, r0, RC, nmax, nq, s_nq, wt, lane, wbar, scale);
 }
 
 template <int HD, typename KVT, int QPK>
@@ -107,6 +162,7 @@ __global__ void __launch_bounds__(kAttnThreads* kDecMaxWorkers) attn_decode_kern
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bar[kDecMaxWorkers];
   __shared__ float s_m[kDecMaxWorkers][kDecRowsChunk], s_l[kDecMaxWorkers][kDecRowsChunk];
+  __shared__ int s_nq[kDecMaxWorkers][kDecRowsChunk];
 
   cg::cluster_group cluster = cg::this_cluster();
   const int C = a.dec_c, W = a.dec_w, qmax = a.dec_qmax;
@@ -114,7 +170,7 @@ __global__ void __launch_bounds__(kAttnThreads* kDecMaxWorkers) attn_decode_kern
   const int rcmax = qmax < kDecRowsChunk ? qmax : kDecRowsChunk;
 
   const int tid = threadIdx.x, lane = tid & 31;
-  const int wk = tid >> 7, wt = tid & 127, wwarp = wt >> 5;  // page worker, its thread / warp
+  const int wk = tid >> 7, wt = tid & 127;  // page worker and its thread
   const int cr = (int)cluster.block_rank();
   const int row = (int)blockIdx.x / C;
   const int H = a.dm.H, KVh = a.dm.KV;
@@ -158,6 +214,9 @@ __global__ void __launch_bounds__(kAttnThreads* kDecMaxWorkers) attn_decode_kern
     mbar_init(&bar[wk], 1);
     fence_mbar_init();
   }
+  // DSMEM may be touched only once every CTA of the cluster runs: arrive now,
+  // wait before the first push into the leader's shared memory
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   named_bar_sync(1 + wk, kAttnThreads);
   auto issue = [&]() {  // worker thread 0: the page's K and V blocks, one mbarrier
     const size_t blk = ((size_t)a.page_table[c] * KVh + kvh) * BLK;
@@ -178,55 +237,20 @@ __global__ void __launch_bounds__(kAttnThreads* kDecMaxWorkers) attn_decode_kern
     qs[i] = a.q[(size_t)(slot0 + v) * H * HD + (size_t)kvh * QPK * HD + rem];
   }
   __syncthreads();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 
   if (active) {
     mbar_wait(&bar[wk], 0);
+    float* pdst = part0 + (size_t)c * qmax * (HD + 2);
     for (int r0 = 0; r0 < Q; r0 += kDecRowsChunk) {
       const int RC = min(kDecRowsChunk, Q - r0);
-      if (RC == 1) page_scores<HD, KVT, QPK, 1>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
-      else if (RC <= 2) page_scores<HD, KVT, QPK, 2>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
-      else if (RC <= 4) page_scores<HD, KVT, QPK, 4>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
-      else if (RC <= 8) page_scores<HD, KVT, QPK, 8>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
-      else page_scores<HD, KVT, QPK, 16>(ks, qs, sc, r0, RC, nmax, wwarp, lane, scale, nrow);
-      named_bar_sync(1 + wk, kAttnThreads);
-      for (int q = wwarp; q < RC; q += 4) {  // chunk-local softmax statistics
-        const int n = nrow(r0 + q);
-        float* sr = sc + q * kPage;
-        if (n <= 0) continue;  // the page is past this vector's context
-        float mx = -FLT_MAX;
-        for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, sr[tt]);
-        mx = warp_max(mx);
-        float l = 0.f;
-        for (int tt = lane; tt < n; tt += 32) {
-          const float p = expf(sr[tt] - mx);
-          sr[tt] = p;
-          l += p;
-        }
-        l = warp_sum(l);
-        if (lane == 0) { s_m[wk][q] = mx; s_l[wk][q] = l; }
-      }
-      named_bar_sync(1 + wk, kAttnThreads);
-      // PV: each thread owns dims d = wt (+128) of every row of the chunk;
-      // the rows' accumulators advance together (ILP), each in token order
-      for (int d = wt; d < HD; d += kAttnThreads) {
-        float acc[kDecRowsChunk];
-#pragma unroll
-        for (int q = 0; q < kDecRowsChunk; ++q) acc[q] = 0.f;
-        for (int tt = 0; tt < nmax; ++tt) {
-          const float vv = tof(vs[(size_t)tt * HD + d]);
-#pragma unroll
-          for (int q = 0; q < kDecRowsChunk; ++q)
-            if (q < RC && tt < nrow(r0 + q)) acc[q] = fmaf(sc[q * kPage + tt], vv, acc[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < kDecRowsChunk; ++q)
-          if (q < RC && nrow(r0 + q) > 0) part0[((size_t)c * qmax + r0 + q) * (HD + 2) + d] = acc[q];
-      }
-      if (wt < RC && nrow(r0 + wt) > 0) {
-        part0[((size_t)c * qmax + r0 + wt) * (HD + 2) + HD] = s_m[wk][wt];
-        part0[((size_t)c * qmax + r0 + wt) * (HD + 2) + HD + 1] = s_l[wk][wt];
-      }
-      named_bar_sync(1 + wk, kAttnThreads);
+      float* sm = s_m[wk];
+      float* sl = s_l[wk];
+      if (RC == 1) page_chunk<HD, KVT, 1>(ks, vs, qs, sc, sm, sl, s_nq[wk], pdst, r0, RC, nmax, nrow, wt, lane, 1 + wk, scale);
+      else if (RC <= 2) page_chunk<HD, KVT, 2>(ks, vs, qs, sc, sm, sl, s_nq[wk], pdst, r0, RC, nmax, nrow, wt, lane, 1 + wk, scale);
+      else if (RC <= 4) page_chunk<HD, KVT, 4>(ks, vs, qs, sc, sm, sl, s_nq[wk], pdst, r0, RC, nmax, nrow, wt, lane, 1 + wk, scale);
+      else if (RC <= 8) page_chunk<HD, KVT, 8>(ks, vs, qs, sc, sm, sl, s_nq[wk], pdst, r0, RC, nmax, nrow, wt, lane, 1 + wk, scale);
+      else page_chunk<HD, KVT, 16>(ks, vs, qs, sc, sm, sl, s_nq[wk], pdst, r0, RC, nmax, nrow, wt, lane, 1 + wk, scale);
     }
   }
 
