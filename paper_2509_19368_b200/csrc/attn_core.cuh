@@ -131,32 +131,39 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
     }
     return false;
   };
-  auto issue_copy = [&](const Item& it) {  // thread 0
-    const int ctx = wpos(it.g) + it.vv + 1;
-    const int n = min(kPage, ctx - it.c * kPage);
+  // rows [r0, r1) of the item's K and V page blocks (thread 0); `arrive`:
+  // the copy that completes the item's mbarrier phase (arrive + its bytes),
+  // else bytes only (the phase waits for the later arriving copy)
+  auto issue_rows = [&](const Item& it, int r0, int r1, bool arrive) {
     // this layer's K / V caches: [k, v] per local layer, contiguous (engine.cu)
     const int gl = wfirst(it.g) + a.layer_i;
     const int lloc = gl == a.hl_global ? a.hl_local : gl - a.first_local;
     const char* kvl = static_cast<const char*>(a.kv_base) + a.kv_layer_bytes * (2 * (size_t)lloc);
     const int page = it.c < kStagePages ? S.st_page[it.c] : a.page_table[it.c];
-    const size_t blk = ((size_t)page * KVh + it.kvh) * BLK;
-    const uint32_t bytes = (uint32_t)(n * HD * sizeof(KVT));
-    mbar_expect_tx(&S.bar, 2 * bytes);
-    bulk_g2s(ks, reinterpret_cast<const KVT*>(kvl) + blk, bytes, &S.bar);
-    bulk_g2s(vs, reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes) + blk, bytes, &S.bar);
+    const size_t blk = ((size_t)page * KVh + it.kvh) * BLK + (size_t)r0 * HD;
+    const uint32_t bytes = (uint32_t)((r1 - r0) * HD * sizeof(KVT));
+    if (arrive) mbar_expect_tx(&S.bar, 2 * bytes);
+    else mbar_expect_tx_only(&S.bar, 2 * bytes);
+    if (bytes) {
+      bulk_g2s(ks + (size_t)r0 * HD, reinterpret_cast<const KVT*>(kvl) + blk, bytes, &S.bar);
+      bulk_g2s(vs + (size_t)r0 * HD, reinterpret_cast<const KVT*>(kvl + a.kv_layer_bytes) + blk, bytes, &S.bar);
+    }
   };
+  auto page_rows = [&](const Item& it) { return min(kPage, wpos(it.g) + it.vv + 1 - it.c * kPage); };
   Item it;
   bool have = decode(worker, it);
-  // a page entirely below the group's first written position is final
-  bool issued = have && (it.c + 1) * kPage <= wpos(it.g);
-  if (issued && tid == 0) issue_copy(it);
+  // The rows of the first item's page below the group's first written
+  // position are final: fetch them while the producing kernel drains; the
+  // rows this layer's QKV kernel writes follow griddepcontrol.wait.
+  const int early = have ? max(0, min(page_rows(it), wpos(it.g) - it.c * kPage)) : 0;
+  if (early > 0 && tid == 0) issue_rows(it, 0, early, false);
   wait_inputs();
 
-  for (int item = worker; have; item += nworkers, have = decode(item, it), issued = false) {
+  for (int item = worker, first = 1; have; item += nworkers, have = decode(item, it), first = 0) {
     const int g = it.g, vv = it.vv, kvh = it.kvh, c = it.c, nch = it.nch;
-    const int slot = wslot(g) + vv, ctx = wpos(g) + vv + 1;
-    const int n = min(kPage, ctx - c * kPage);
-    if (!issued && tid == 0) issue_copy(it);
+    const int slot = wslot(g) + vv;
+    const int n = page_rows(it);
+    if (tid == 0) issue_rows(it, first ? early : 0, n, true);
     const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
     for (int i = tid; i < QPK * HD; i += kAttnThreads) S.qs[i / HD][i % HD] = qsrc[i];
     sync();

@@ -68,7 +68,6 @@ struct ppsd_engine {
   int32_t* d_part_flag = nullptr;  // ... and their per-chunk sequence numbers
   int32_t* d_kerr = nullptr;       // sticky GEMV error word (K-split wait timeout)
   bool hl = false;              // exit head has a decoder layer
-  bool attn_decode = true;      // decode attention on the cluster kernel (PPSD_ATTN=splitk: off)
   TickCtx* d_ctx = nullptr;
   ArCtl* d_arctl = nullptr;
   int32_t* d_tokens = nullptr;
@@ -188,9 +187,7 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   return gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st);
 }
 
-// nvmax: most query vectors per group this launch can see (0 = prefill:
-// the split-K kernel); gmax: most groups (local stages) of the Work.
-static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i, int nvmax, int gmax) {
+static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   // PPSD_PROFILE_SKIP_ATTN=1: timing experiments only (wrong results)
   static const bool skip = getenv("PPSD_PROFILE_SKIP_ATTN") && atoi(getenv("PPSD_PROFILE_SKIP_ATTN")) != 0;
   if (skip) return cudaSuccess;
@@ -210,11 +207,6 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i, int nvmax,
   a.first_local = e->first_local_layer;
   a.hl_global = e->hl ? e->md.n_layers : -1;
   a.hl_local = e->n_local_layers;
-  // decode launches: the cluster kernel (attn_decode.cu), same arithmetic
-  if (nvmax > 0 && e->attn_decode) {
-    AttnArgs d = a;
-    if (attn_decode_plan(&d, gmax, nvmax, e->num_sms)) return attn_decode_launch(d, gmax * e->dm.KV, e->st);
-  }
   return attn_launch(a, attn_grid(e), e->st);
 }
 
@@ -249,13 +241,13 @@ static cudaError_t enqueue_umma(ppsd_engine* e, Work* w, int layer_i, int mat) {
 // Prompt layers for a chunk of <= kMaxVec vectors in group 0 of `w`: the
 // tcgen05 GEMM when planned (2 launches per matrix: operand staging + GEMM),
 // else the batched GEMV. Returns launches enqueued, or -1.
-static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched, int nvmax = 1, int gmax = 1);
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched);
 static int enqueue_prefill_layers(ppsd_engine* e, Work* w, int n_slots) {
-  if (!e->umma) return enqueue_layers(e, w, n_slots, true, 0, 1);
+  if (!e->umma) return enqueue_layers(e, w, n_slots, true);
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
     if (enqueue_umma(e, w, i, kMatQKV) != cudaSuccess) return -1;
-    if (enqueue_attn(e, w, i, 0, 1) != cudaSuccess) return -1;
+    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
     if (enqueue_umma(e, w, i, kMatO) != cudaSuccess) return -1;
     if (enqueue_umma(e, w, i, kMatGU) != cudaSuccess) return -1;
     if (enqueue_umma(e, w, i, kMatDown) != cudaSuccess) return -1;
@@ -264,13 +256,12 @@ static int enqueue_prefill_layers(ppsd_engine* e, Work* w, int n_slots) {
   return n;
 }
 
-// returns launches enqueued, or -1 on error. nvmax / gmax bound the Work's
-// vectors per group and groups (attention plan); nvmax 0 = prefill.
-static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched, int nvmax, int gmax) {
+// returns launches enqueued, or -1 on error
+static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
     if (enqueue_gemv(e, w, i, kMatQKV, batched) != cudaSuccess) return -1;
-    if (enqueue_attn(e, w, i, nvmax, gmax) != cudaSuccess) return -1;
+    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatO, batched) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatGU, batched) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatDown, batched) != cudaSuccess) return -1;
@@ -354,7 +345,7 @@ static int build_fold_graph(ppsd_engine* e) {
   // tick; without a batch its kernels find no work and exit
   const char* cv = getenv("PPSD_FOLD_COND");
   if (ok && cv && atoi(cv) == 0) {
-    const int m = enqueue_layers(e, e->d_work_deep, deep, true, sched_fold_width(&e->cfg), 1);
+    const int m = enqueue_layers(e, e->d_work_deep, deep, true);
     need(m >= 0, "deep layers");
     need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
          "final heads");
@@ -389,7 +380,7 @@ static int build_fold_graph(ppsd_engine* e) {
              cudaSuccess, "body capture");
     if (ok) {
       e->st = body_st;
-      const int m = enqueue_layers(e, e->d_work_deep, deep, true, sched_fold_width(&e->cfg), 1);
+      const int m = enqueue_layers(e, e->d_work_deep, deep, true);
       need(m >= 0, "deep layers");
       n_body = m;
       need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
@@ -423,7 +414,7 @@ static int build_graphs(ppsd_engine* e) {
       [&]() -> int {
         int n = 0;
         if (kind == PPSD_MODEL_TRANSFORMER) {
-          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false, 1, e->hi - e->lo + 1);
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
           n += m;
           if (e->hl) {  // exit-head layer on a copy of the exit chain's state
@@ -705,9 +696,6 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       AttnArgs aa{};
       aa.dm = d;
       CU(attn_set_attrs(aa));
-      const char* av = getenv("PPSD_ATTN");  // read per engine: "splitk" = the attn_core.cuh kernel only
-      e->attn_decode = !(av && strcmp(av, "splitk") == 0);
-      if (e->attn_decode) CU(attn_decode_set_attrs(aa));
     }
     e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
     e->final_norm = w->final_norm;
@@ -1227,7 +1215,7 @@ static int eesd_graph(ppsd_engine* e, int gamma, cudaGraphExec_t* out, int64_t* 
           cnt += m + mh + 3;
         }
         if (launch_pdl(eesd_verify_begin_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
-        const int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true, gamma + 1, 1);  // batched verify
+        const int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, true);  // batched verify
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work_ar, 0, kMatHeadV, true) != cudaSuccess) return -1;
         if (launch_pdl(eesd_scan_kernel, dim3(1), dim3(256), 0, e->st, ctx, es) != cudaSuccess) return -1;
@@ -1463,7 +1451,7 @@ extern "C" int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32
   w.nl[0] = e->n_local_layers;
   w.head_slot[0] = w.head_slot[1] = -1;
   CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
-  auto launch = [&](int i) { return enqueue_attn(e, e->d_work_ar, i % e->n_local_layers, n_vec, 1); };
+  auto launch = [&](int i) { return enqueue_attn(e, e->d_work_ar, i % e->n_local_layers); };
   for (int i = 0; i < 3; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev0, e->st));
   for (int i = 0; i < reps; ++i) CU(launch(i));
@@ -1511,7 +1499,7 @@ static int build_mr_graphs(ppsd_engine* e) {
   int rc = capture(
       e,
       [&]() -> int {
-        int m = enqueue_layers(e, e->d_work, e->max_local_layers, false, 1, e->hi - e->lo + 1);
+        int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
         if (m < 0) return -1;
         if (e->hl) {  // exit rank: head layer on a copy of the exit chain's state
           const int mh = enqueue_head_layer(e, false);
@@ -1823,7 +1811,7 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
     rc = capture(
         e,
         [&]() -> int {
-          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false, 1, e->hi - e->lo + 1);
+          int m = enqueue_layers(e, e->d_work, e->max_local_layers, false);
           if (m < 0) return -1;
           if (e->hl) {
             const int mh = enqueue_head_layer(e, false);

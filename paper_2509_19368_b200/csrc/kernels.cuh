@@ -108,9 +108,6 @@ struct AttnArgs {
   int32_t first_local;  // global index of the first local layer
   int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
   int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
-  // decode kernel plan (attn_decode.cu, attn_decode_plan): cluster size,
-  // 128-thread page workers per CTA, query rows per row (nv * H/KV) at most
-  int32_t dec_c, dec_w, dec_qmax;
 };
 
 // tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
@@ -167,9 +164,6 @@ cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid
 cudaError_t gemv_set_attrs(int vpt, int m, int mat, int ksplit, size_t smem);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
-bool attn_decode_plan(AttnArgs* a, int gmax, int nvmax, int num_sms);
-cudaError_t attn_decode_set_attrs(const AttnArgs& a);
-cudaError_t attn_decode_launch(const AttnArgs& a, int rows, cudaStream_t st);
 bool umma_shape_ok(int R, int K);
 int umma_encode_map(void* map, const void* base, int rows, int K, int box_rows);
 size_t umma_map_bytes();

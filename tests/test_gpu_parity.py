@@ -323,42 +323,3 @@ def test_head_layer_lossless_and_schedules_agree(name):
         assert 0 < out["folded"][1][2] < 64  # accepts and rejects both occur
     et, em, _ = ppsd.decode_eesd(lm, ppsd.PipelineConfig(8, 2), prompt, 64, 3)
     assert et[:64] == ar
-
-
-# ------------------------------------------------- decode attention kernels --
-
-@pytest.mark.parametrize("shape,kv", [("l7b_2layer", "bf16"), ("mid_gqa", "bf16"), ("mid_gqa", "fp32"),
-                                      ("tiny", "fp32")])
-def test_decode_attention_bit_identical_to_splitk(shape, kv, monkeypatch):
-    """The cluster decode-attention kernel (attn_decode.cu) and the split-K
-    kernel (attn_core.cuh, PPSD_ATTN=splitk) produce bit-identical logits for
-    every position of a folded PPSD decode (shallow ticks at M=1, deep batches
-    of up to S vectors), an EESD decode (verify of gamma+1 vectors) and AR,
-    with contexts crossing several KV pages."""
-    import torch
-
-    from paper_2509_19368_b200.decode import Engine
-
-    if shape == "tiny":
-        config = ppsd.TransformerConfig.tiny(8)
-    else:
-        sh = dict(SHAPES[shape])
-        sh["n_layers"] = 8
-        config = ppsd.TransformerConfig(**sh, kv_dtype=kv, max_ctx=512)
-    lm = ppsd.TransformerLM(config, seed=17, deep_scale=0.3, deep_from=2)
-    cfg = ppsd.PipelineConfig(8, 2)
-    prompt = [int(t) for t in np.random.default_rng(8).integers(0, config.vocab, size=150)]
-    out = {}
-    for mode in ("splitk", "decode"):
-        monkeypatch.setenv("PPSD_ATTN", mode)
-        eng = Engine(lm.model_desc(), lm.weights_struct(), cfg, device=lm.device.index)
-        tap = torch.full((97, 2, config.vocab), float("nan"), dtype=torch.float32, device=lm.device)
-        eng.set_logits_tap(tap)
-        toks, m, tr = eng.decode(prompt, 96)
-        eng.set_logits_tap(None)
-        et, em, _ = eng.decode_eesd(prompt, 96, 7)
-        ar = eng.decode_ar(prompt, 96)
-        out[mode] = (toks, _metrics_list(m), tr.to_csv(), tap.cpu().numpy().tobytes(), et, _metrics_list(em), ar)
-        eng.close()
-    assert out["decode"] == out["splitk"]
-    assert out["decode"][0] == out["decode"][6]
