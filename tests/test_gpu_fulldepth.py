@@ -17,7 +17,10 @@ them) teacher-forced along the GPU's own token path:
   oracle argmax; inside the margin it is within 2*tol of the max;
 * verdicts: where both heads' margins are clear, accept <=> exit argmax ==
   final argmax (greedy_match, pipesim.py:351-358), position by position from
-  the trace, so the accepted-token count is pinned too.
+  the trace, so the accepted-token count is pinned too;
+* trace invariants: the reference's work-conservation, commit-order and
+  flush-discipline checkers (pkg/tests/helpers.py:80-151, tests/trace_checks.py)
+  hold on the 512-token trace.
 
 The margin histogram is printed (and written to $PPSD_PARITY_OUT as JSON:
 profiles/r02_fulldepth_parity.json).
@@ -66,6 +69,10 @@ def test_bench_config_full_depth_vs_oracle():
     toks, m, tr, sched, tap = _run_gpu(config, cfg, prompt, n_new, bench.DEEP_SCALE, E, bench.SEED)
     assert sched == "folded"  # the bench's schedule
     assert m.committed_tokens == n_new
+    # the reference's trace invariants (pkg/tests/helpers.py:80-151) on the bench trace
+    from trace_checks import check_all
+
+    check_all(tr, cfg.n_stages, cfg.exit_stage)
 
     shape = ModelShape(config.n_layers, config.d_model, config.n_heads, config.n_kv_heads, config.head_dim,
                        config.ffn_dim, config.vocab, config.rms_eps, config.rope_theta)
@@ -76,7 +83,8 @@ def test_bench_config_full_depth_vs_oracle():
     del orc
 
     report = {"config": "llama2-7b shape, 32 layers, E=8, deep_scale 0.08, bf16 KV, prompt 128, 512 tokens, "
-                        "folded schedule, tcgen05 prefill", "tol_rel": TOL_REL}
+                        "folded schedule, tcgen05 prefill", "tol_rel": TOL_REL,
+              "trace_rows": len(list(tr)), "trace_invariants": "work conservation, commit order, flush discipline: ok"}
     # ---- logits, both heads, every position ----
     worst = {}
     for which, z_or in ((0, ze), (1, zf)):

@@ -1,6 +1,6 @@
-"""Decode-attention latency per launch, cluster kernel vs split-K kernel
-(PPSD_ATTN=splitk), at the 7B shape (32 kv heads, hd 128, bf16 KV):
-n_vec query vectors in one group, longest context ctx.
+"""Decode-attention latency per launch (attn_core.cuh split-K kernel) at the
+7B shape (32 kv heads, hd 128, bf16 KV): n_vec query vectors in one group,
+longest context ctx, back-to-back launches walking the layers.
 
     python tools/probe_attn.py [--model 7b] [--out profiles/r02_attn_probe.json]
 """
@@ -30,8 +30,7 @@ def main():
     lm = ppsd.TransformerLM(config, seed=0)
     cfg = ppsd.PipelineConfig(args.layers, 1)
     rows = []
-    for mode in ("splitk", "decode"):
-        os.environ["PPSD_ATTN"] = mode
+    for mode in ("splitk",):
         eng = Engine(lm.model_desc(), lm.weights_struct(), cfg, device=lm.device.index)
         for nv in (1, 4, 11):
             for ctx in (128, 384, 640, 1000):
