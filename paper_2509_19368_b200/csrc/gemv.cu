@@ -108,15 +108,16 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[N], int lane) {
 // every plan uses 8.
 constexpr int nw_for(int /*vpt*/) { return 8; }
 
-// Register boost for the batched plans of wide-K matrices (VPT >= 5, and
-// the K-split down projection from VPT 3 on): their M=4 input slices need
-// ~230 registers per thread, but 9 warps cap every thread at 168 (allocation
-// granularity is 4 warps). Those instantiations run a 4-warp producer
-// warpgroup that hands its registers to the consumers (setmaxnreg).
-// Measured: the boost made the K = 4096 batched plans slower, so only wide-K
-// plans and the split down projection (13B K/2 = 6912: no spills) use it.
+// Register boost for the batched plans of wide-K matrices (VPT >= 3: K >
+// 4096): their M=4 input slices need ~170-230 registers per thread, but 9
+// warps cap every thread at 168 (allocation granularity is 4 warps). Those
+// instantiations run a 4-warp producer warpgroup that hands its registers
+// to the consumers (setmaxnreg). Measured: the boost made the K = 4096
+// (VPT 2) batched plans slower, so they keep 9 warps; without it the 13B
+// (K = 5120) and 70B (K = 8192) 4-vector plans spilled 100-480 bytes, the
+// 70B split down projection's 2-vector plans (K/2 = 14336) 260-400.
 template <int VPT, int M, int EPI = -1>
-constexpr bool reg_boost() { return (VPT >= 5 || (VPT >= 3 && EPI == kMatDownS)) && M >= 4; }
+constexpr bool reg_boost() { return (VPT >= 3 && M >= 4) || (VPT >= 7 && M >= 2); }
 template <int VPT, int M, int EPI = -1>
 constexpr int gemv_threads() { return (nw_for(VPT) + (reg_boost<VPT, M, EPI>() ? 4 : 1)) * 32; }
 
