@@ -262,12 +262,31 @@ int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int
 /* Device weight initialiser: the counter-hash init of oracle/transformer.py,
  * written straight into the engine's physical layout.
  * layout: 0 plain [rows][cols]; 1 = fused qkv (q,k pair-interleaved);
- * 2 = fused gate/up (row-interleaved). For layouts 1/2 tid0..tid2 are the
+ * 2 = fused gate/up (row-interleaved), optionally | PPSD_LAYOUT_TC_TILED:
+ * the tensor-core GEMV's tiled matrix layout (the buffer holds
+ * ppsd_weight_elems(1, rows, cols) bf16). For layouts 1/2 tid0..tid2 are the
  * logical tensors' ids and a0..a2 their scales. */
+#define PPSD_LAYOUT_TC_TILED 16
+/* bf16 elements of a [rows][cols] matrix in the plain (tiled = 0) or the
+ * TC-tiled (tiled = 1: K padded to a multiple of 64) layout */
+int ppsd_weight_elems(int32_t tiled, int64_t rows, int64_t cols, int64_t* elems);
 int ppsd_init_weight(void* dst_bf16, int32_t layout, int64_t rows, int64_t cols,
                      uint64_t seed, const uint64_t* tids, const float* scales,
                      int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
                      void* cuda_stream);
+
+/* GEMV unit check (parity tests): y_v = W x_v through the shipped kernel for
+ * the O (which = 1) or down (which = 3) projection of global layer `layer`;
+ * nv vectors (<= 5 decode-tick plan, <= 16 batched plan); in [nv][K], out
+ * [nv][R], host fp32. */
+int ppsd_debug_matvec(ppsd_engine* e, int32_t which, int32_t layer, int32_t nv, int32_t batched,
+                      const float* in, float* out);
+
+/* Tensor-core GEMV pipeline timeline (debugging; needs a build with
+ * -DPPSD_TC_TRACE, else zeros): on >= 0 enables (1) / disables (0) recording,
+ * out (or NULL) receives [8][128] CTA-0 events then [160][4] per-CTA marks,
+ * %globaltimer ns. */
+int ppsd_debug_tc_trace(int32_t on, uint64_t* out);
 
 /* fp32 logits of the last head evaluation: which 0 = exit head, 1 = final
  * head (length vocab) — debugging / tolerance tests. */

@@ -42,16 +42,34 @@ static int fail(int code, const std::string& msg) {
                                   std::to_string(__LINE__));                                  \
   } while (0)
 
+// layers whose matrices of one kind sit at a fixed stride (one allocation)
+struct WStride {
+  const void* base = nullptr;
+  long long stride = 0;
+  int n = 0;  // layers [0, n) follow base + l * stride
+};
+
 struct GemvPlan {
   int vpt = 0, tr = 0, m = 1, ns = 0, sub = 1, R = 0, K = 0;
   int ksplit = 0, K_full = 0;  // K split across the two grid halves (K = K_full / 2)
   size_t smem = 0;
+  TcPlan tc;                   // tensor-core GEMV plan (e->tc)
 };
+
+// PPSD_GEMV=cc: the CUDA-core GEMV over row-major weights (A/B experiments);
+// default: the tensor-core GEMV over TC-tiled weights
+static bool gemv_tc_env() {
+  const char* v = getenv("PPSD_GEMV");
+  return !(v && v[0] == 'c');
+}
 
 struct ppsd_engine {
   ppsd_model_desc md{};
   ppsd_pipeline_desc pd{};
   int device = 0, num_sms = 148;
+  bool tc = true;  // tensor-core GEMV (weights TC-tiled)
+  WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
+  bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
   cudaStream_t st = nullptr;
   SchedCfg cfg{};
   int S = 0, lo = 1, hi = 1, max_local_layers = 0, first_local_layer = 0, n_local_layers = 0;
@@ -144,17 +162,30 @@ struct ppsd_engine {
 extern "C" const char* ppsd_last_error(void) { return g_err.c_str(); }
 
 extern "C" const char* ppsd_build_info(void) {
-  return "libppsd sm_100a: tma-bulk gemv ring, split-K paged attention, device tick machine";
+  return "libppsd sm_100a: tcgen05 weight-streaming GEMV (TMEM accumulators, bulk-copy ring, cluster split-K), "
+         "split-K paged attention, device tick machine";
 }
 
 static int attn_grid(const ppsd_engine* e) { return 8 * e->num_sms; }
+
+// first failed launch inside a graph capture (the capture itself only
+// reports "invalidated")
+static thread_local cudaError_t g_launch_err = cudaSuccess;
+static cudaError_t note_launch(cudaError_t e) {
+  if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;
+  return e;
+}
 
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
 
 static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, bool batched = false,
                                 float* logits = nullptr) {
-  const GemvPlan& p = batched ? e->gpb[mat] : e->gp[mat];
+  // tensor-core GEMV: groups of <= 5 vectors (the folded deep batch at
+  // E >= N/5) run the decode-tick plan, whose smaller operand stages leave
+  // room for a deeper weight ring; the arithmetic is the same in every plan
+  const bool use_b = batched && !(e->tc && e->small_batch);
+  const GemvPlan& p = use_b ? e->gpb[mat] : e->gp[mat];
   GemvArgs a{};
   a.work = w;
   a.layer_i = layer_i;
@@ -184,7 +215,32 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   a.part_buf = e->d_part;
   a.part_flag = e->d_part_flag;
   a.err = e->d_kerr;
-  return gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st);
+  if (e->tc) {
+    const TcPlan& t = p.tc;
+    if (mat == kMatHead || mat == kMatHeadV) {
+      a.wp[0] = e->lm_head;
+    } else {
+      const WStride& ws = e->wstride[mat];
+      a.wbase = ws.base;
+      a.wstride = ws.stride;
+      a.wn = ws.n;
+      if (e->h_layers.size() <= (size_t)kTcMaxWp)
+        for (size_t l = 0; l < e->h_layers.size(); ++l) {
+          const LayerW& L = e->h_layers[l];
+          a.wp[l] = mat == kMatQKV ? (const void*)L.qkv : mat == kMatO ? (const void*)L.o
+                  : mat == kMatGU ? (const void*)L.gu : (const void*)L.down;
+        }
+    }
+    a.nstage = t.ns;
+    a.js = t.js;
+    a.nj = t.nj;
+    a.nb = t.nb;
+    a.tg = t.tg;
+    a.nblk = t.nblk;
+    a.bar_off = t.bar_off;
+    return note_launch(tc_launch(a, t.cs, t.smem, t.grid, e->st));
+  }
+  return note_launch(gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st));
 }
 
 static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
@@ -285,13 +341,14 @@ static int enqueue_head_layer(ppsd_engine* e, bool prefill) {
 template <class F>
 static int capture(ppsd_engine* e, F body, cudaGraphExec_t* out, int64_t* nlaunch) {
   cudaGraph_t g = nullptr;
+  g_launch_err = cudaSuccess;
   CU(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
   int n = body();
   cudaError_t ce = cudaStreamEndCapture(e->st, &g);
   if (n < 0) {
     if (g) cudaGraphDestroy(g);
-    return fail(PPSD_ECUDA, std::string("kernel launch failed during capture: ") +
-                                cudaGetErrorString(cudaGetLastError()));
+    const cudaError_t le = g_launch_err != cudaSuccess ? g_launch_err : cudaGetLastError();
+    return fail(PPSD_ECUDA, std::string("kernel launch failed during capture: ") + cudaGetErrorString(le));
   }
   CU(ce);
   CU(cudaGraphInstantiate(out, g, 0));
@@ -380,12 +437,14 @@ static int build_fold_graph(ppsd_engine* e) {
              cudaSuccess, "body capture");
     if (ok) {
       e->st = body_st;
+      e->small_batch = sched_fold_width(&e->cfg) <= 5;
       const int m = enqueue_layers(e, e->d_work_deep, deep, true);
       need(m >= 0, "deep layers");
       n_body = m;
       need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
            "final heads");
       n_body += 1;
+      e->small_batch = false;
       e->st = main_st;
       cudaGraph_t bg = body;
       need(cudaStreamEndCapture(body_st, &bg) == cudaSuccess, "body end capture");
@@ -667,12 +726,13 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     // PPSD_DOWN_SPLIT (read per engine, recorded in the plan): 0 disables
     // the K split of the down projection (DESIGN.md environment knobs)
     const char* dsv = getenv("PPSD_DOWN_SPLIT");
-    const bool split_on = !(dsv && dsv[0] == '0') && e->lo == 1 && e->hi == e->S && ppsd::g_pdl;
+    e->tc = gemv_tc_env();
+    const bool split_on = !e->tc && !(dsv && dsv[0] == '0') && e->lo == 1 && e->hi == e->S && ppsd::g_pdl;
     const int shapes[kNumMats][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d},
                                      {d.d, d.ffn}, {d.V, d.d}, {d.V, d.d}};
     for (int m = 0; m < kNumMats; ++m) {
       for (int b = 0; b < 2; ++b) {
-        if ((m == kMatHead && b) || (m == kMatHeadV && !b)) continue;
+        if ((m == kMatHead && b) || (m == kMatHeadV && !b && !e->tc)) continue;
         GemvPlan& p = b ? e->gpb[m] : e->gp[m];
         p.R = shapes[m][0];
         p.K = p.K_full = shapes[m][1];
@@ -685,6 +745,21 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         if (m == kMatDown && split_on && p.K > 8192 && (p.K / 2) % 8 == 0 && e->num_sms % 2 == 0) {
           p.ksplit = 1;
           p.K = p.K / 2;
+        }
+        if (e->tc) {
+          // one weight pass for every vector of a group: one 16-column B
+          // block (<= 5 vectors x 3 parts) for the decode tick and the PPSD
+          // head, 3 (<= 16 vectors) batched
+          const int nblk = b ? 3 : 1;
+          if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc) != 0)
+            return fail(PPSD_EUNSUPPORTED, "no tensor-core GEMV plan for matrix " + std::to_string(m) + " [" +
+                                               std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
+          CU(tc_set_attrs(m, p.tc.cs, p.tc.smem));
+          if (getenv("PPSD_TC_VERBOSE"))
+            fprintf(stderr, "tc plan mat %d b %d: R %d K %d JS %d NJ %d CS %d grid %d TG %d nb %d NS %d smem %zu\n", m, b,
+                    p.R, p.K, p.tc.js, p.tc.nj, p.tc.cs, p.tc.grid, p.tc.tg, p.tc.nb, p.tc.ns, p.tc.smem);
+          p.m = b ? kMaxVec : (m == kMatHead ? 2 : 1);
+          continue;
         }
         if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.sub, &p.smem) != 0)
           return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
@@ -758,6 +833,23 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     }
     CU(dalloc(&e->d_layers, sizeof(LayerW) * e->h_layers.size()));
     CU(cudaMemcpy(e->d_layers, e->h_layers.data(), sizeof(LayerW) * e->h_layers.size(), cudaMemcpyHostToDevice));
+    // weights of one matrix kind at a fixed stride across the local layers
+    // (one allocation per kind, models.py): the GEMV producer computes the
+    // address instead of loading it
+    for (int m = kMatQKV; m <= kMatDown; ++m) {
+      auto ptr = [&](int l) -> long long {
+        const LayerW& L = e->h_layers[l];
+        return (long long)(uintptr_t)(m == kMatQKV ? (const void*)L.qkv : m == kMatO ? (const void*)L.o
+                                      : m == kMatGU ? (const void*)L.gu : (const void*)L.down);
+      };
+      const int l0 = e->first_local_layer, nl = e->n_local_layers;
+      e->wstride[m] = WStride{};
+      if (nl < 2) continue;
+      const long long st = ptr(l0 + 1) - ptr(l0);
+      bool ok = st > 0;
+      for (int l = l0 + 2; ok && l < l0 + nl; ++l) ok = ptr(l) - ptr(l - 1) == st;
+      if (ok) e->wstride[m] = WStride{(const void*)(uintptr_t)(ptr(l0) - (long long)l0 * st), st, l0 + nl};
+    }
     const int qd = d.H * d.hd;
     // rows: chains / prefill chunk [0, nbuf); exit-head layer copies [nbuf, 2*nbuf)
     const size_t nb = (size_t)e->nbuf * (e->hl ? 2 : 1);
@@ -776,7 +868,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_head_cnt, sizeof(int32_t) * kMaxVec));
     c.logits32 = e->d_logits;
     c.x = e->d_x;
-    int rc = setup_umma(e, shapes);
+    int rc = e->tc ? PPSD_OK : setup_umma(e, shapes);  // umma.cu reads row-major weights
     if (rc) return rc;
     // prompt tokens per prefill chunk: one tcgen05 weight pass (umma_n()), or
     // the batched-GEMV chunk
@@ -793,7 +885,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     // without spilling (K = d_model <= 4096: 7B-class layers). Measured on the
     // 13B shape (d 5120, ffn 13824) the spilling batched plans made folded
     // slower than pipelined (194 vs 218 tok/s), on 7B faster (391 vs 317).
-    e->fold_auto = e->fold_ok && e->gpb[kMatQKV].vpt <= 2;
+    e->fold_auto = e->fold_ok && (e->tc || e->gpb[kMatQKV].vpt <= 2);
     if (pd->schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
       return fail(PPSD_EUNSUPPORTED, "folded schedule needs all stages on this device and at most " +
                                          std::to_string(kMaxVec) + " chains in flight");
@@ -1360,10 +1452,29 @@ extern "C" int ppsd_simulate_eesd(ppsd_engine* e, int32_t gamma, double alpha, u
 // ---------------------------------------------------------------------------
 // weight init
 
+extern "C" int ppsd_weight_elems(int32_t tiled, int64_t rows, int64_t cols, int64_t* elems) {
+  if (rows <= 0 || cols <= 0 || !elems) return fail(PPSD_EINVAL, "bad weight shape");
+  if (!tiled) {
+    *elems = rows * cols;
+    return PPSD_OK;
+  }
+  if (rows % 8 || cols % 8 || rows > INT32_MAX || cols > INT32_MAX)
+    return fail(PPSD_EUNSUPPORTED, "TC-tiled weights need rows and cols multiples of 8");
+  int js, kp;
+  tc_layout((int)rows, (int)cols, &js, &kp);
+  *elems = rows * kp;
+  return PPSD_OK;
+}
+
 extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t cols, uint64_t seed,
                                 const uint64_t* tids, const float* scales, int32_t n_heads, int32_t n_kv_heads,
                                 int32_t head_dim, void* cuda_stream) {
   if (!dst || !tids || !scales || rows <= 0 || cols <= 0) return fail(PPSD_EINVAL, "bad init arguments");
+  const bool tiled = (layout & PPSD_LAYOUT_TC_TILED) != 0;
+  layout &= ~PPSD_LAYOUT_TC_TILED;
+  if (layout < 0 || layout > 2) return fail(PPSD_EINVAL, "bad weight layout");
+  int64_t elems = 0;
+  if (int rc = ppsd_weight_elems(tiled, rows, cols, &elems)) return rc;
   const uint64_t salt = 0x5EEDB200C0FFEE01ull;  // oracle/transformer.py INIT_SALT
   uint64_t b[3] = {0, 0, 0};
   float a[3] = {0, 0, 0};
@@ -1373,12 +1484,12 @@ extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t
     a[i] = scales[i];
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  const long long n = rows * cols;
+  const long long n = elems;
   long long blocks = (n + 255) / 256;
   if (blocks > 148LL * 64) blocks = 148LL * 64;
-  init_weight_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(dst), layout, rows, cols,
-                                                     b[0], b[1], b[2], a[0], a[1], a[2], n_heads, n_kv_heads,
-                                                     head_dim);
+  init_weight_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(dst), layout, tiled ? 1 : 0,
+                                                     rows, cols, b[0], b[1], b[2], a[0], a[1], a[2], n_heads,
+                                                     n_kv_heads, head_dim);
   CU(cudaGetLastError());
   return PPSD_OK;
 }
@@ -1417,11 +1528,13 @@ extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, 
   w.head_slot[1] = ng > 1 ? 1 : -1;
   CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
   const bool head = which >= kMatHead;
+  e->small_batch = batched && nv <= 5;  // as the folded deep batch runs it
   auto launch = [&](int i) { return enqueue_gemv(e, e->d_work_ar, head ? 0 : i % nl, which, batched); };
   for (int i = 0; i < 3; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev0, e->st));
   for (int i = 0; i < reps; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev1, e->st));
+  e->small_batch = false;
   CU(cudaEventSynchronize(e->ev1));
   if (int rc = check_kerr(e)) return rc;
   float ms = 0;
@@ -1429,6 +1542,54 @@ extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, 
   const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
   *avg_ms = ms / reps;
   *bytes_per_launch = (double)p.R * (p.ksplit ? p.K_full : p.K) * 2.0 * (head ? 1 : ng);
+  return PPSD_OK;
+}
+
+// GEMV unit check (parity tests): y_v = W x_v for one O or down projection of
+// global layer `layer` through the shipped kernel (residual epilogue into a
+// zeroed hidden state), nv vectors in one group, decode-tick (batched = 0,
+// nv <= 5) or batched plan. in: host [nv][K] fp32, out: host [nv][R] fp32.
+extern "C" int ppsd_debug_matvec(ppsd_engine* e, int32_t which, int32_t layer, int32_t nv, int32_t batched,
+                                 const float* in, float* out) {
+  if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "matvec needs a transformer engine");
+  if ((which != kMatO && which != kMatDown) || !in || !out) return fail(PPSD_EINVAL, "matvec: O or down only");
+  if (nv < 1 || nv > (batched ? (int)kMaxVec : 5) || nv > e->nbuf) return fail(PPSD_EINVAL, "matvec: bad nv");
+  if (layer < e->first_local_layer || layer >= e->first_local_layer + e->n_local_layers)
+    return fail(PPSD_EINVAL, "matvec: layer not local");
+  CU(cudaSetDevice(e->device));
+  const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
+  const int K = p.K_full, R = p.R;
+  Work w{};
+  w.G = 1;
+  w.slot[0] = 0;
+  w.pos[0] = 0;
+  w.nv[0] = nv;
+  w.first[0] = layer;
+  w.nl[0] = 1;
+  w.head_slot[0] = w.head_slot[1] = -1;
+  CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
+  float* dst_in = which == kMatO ? e->d_o : e->d_h;
+  const size_t ld_in = which == kMatO ? (size_t)e->dm.H * e->dm.hd : (size_t)e->dm.ffn;
+  for (int v = 0; v < nv; ++v)
+    CU(cudaMemcpyAsync(dst_in + v * ld_in, in + (size_t)v * K, sizeof(float) * K, cudaMemcpyHostToDevice, e->st));
+  CU(cudaMemsetAsync(e->d_x, 0, sizeof(float) * (size_t)nv * e->dm.d, e->st));
+  CU(enqueue_gemv(e, e->d_work_ar, 0, which, batched != 0));
+  for (int v = 0; v < nv; ++v)
+    CU(cudaMemcpyAsync(out + (size_t)v * R, e->d_x + (size_t)v * e->dm.d, sizeof(float) * R, cudaMemcpyDeviceToHost,
+                       e->st));
+  CU(cudaStreamSynchronize(e->st));
+  return check_kerr(e);
+}
+
+namespace ppsd {
+int tc_trace_enable(int on);
+int tc_trace_read(unsigned long long* out);  // [8][128] + [160][4]
+}
+// tensor-core GEMV pipeline timeline of CTA 0 (debugging): on = 1 records the
+// next launches, out = [8][128] %globaltimer ns of the last one
+extern "C" int ppsd_debug_tc_trace(int32_t on, uint64_t* out) {
+  if (on >= 0 && tc_trace_enable(on)) return fail(PPSD_ECUDA, "trace enable");
+  if (out && tc_trace_read(reinterpret_cast<unsigned long long*>(out))) return fail(PPSD_ECUDA, "trace read");
   return PPSD_OK;
 }
 

@@ -116,7 +116,7 @@ __global__ void eesd_draft_end_kernel(const TickCtx* ctxp, EesdState* es);
 __global__ void eesd_verify_begin_kernel(const TickCtx* ctxp, EesdState* es);
 __global__ void eesd_scan_kernel(const TickCtx* ctxp, EesdState* es);
 __global__ void eesd_toy_round_kernel(const TickCtx* ctxp, EesdState* es);
-__global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long rows, long long cols,
+__global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, int tiled, long long rows, long long cols,
                                    uint64_t b0, uint64_t b1, uint64_t b2, float a0, float a1, float a2,
                                    int H, int KV, int hd);
 

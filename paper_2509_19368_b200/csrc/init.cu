@@ -12,13 +12,22 @@ __device__ __forceinline__ __nv_bfloat16 hash_weight(uint64_t base, long long id
   return __float2bfloat16_rn(__fmul_rn(t, a));
 }
 
-__global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long rows, long long cols,
+// tiled = 1: the TC-tiled layout of the tensor-core GEMV (kernels.cuh:
+// tc_offset), K padded with zeros to a multiple of 64
+__global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, int tiled, long long rows, long long cols,
                                    uint64_t b0, uint64_t b1, uint64_t b2, float a0, float a1, float a2,
                                    int H, int KV, int hd) {
-  const long long n = rows * cols;
+  int js = 1, kp = (int)cols;
+  if (tiled) tc_layout((int)rows, (int)cols, &js, &kp);
+  const long long n = rows * kp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const long long pr = i / cols, col = i - pr * cols;
+    const long long pr = i / kp, col = i - pr * kp;
+    const long long di = tiled ? tc_offset((int)rows, (int)cols, pr, col) : i;
+    if (col >= cols) {  // K padding (tiled only)
+      dst[di] = __float2bfloat16_rn(0.f);
+      continue;
+    }
     uint64_t base = b0;
     float a = a0;
     long long lr = pr;  // logical row in the logical tensor
@@ -40,7 +49,7 @@ __global__ void init_weight_kernel(__nv_bfloat16* dst, int layout, long long row
       lr = pr >> 1;
       if (pr & 1) { base = b1; a = a1; }
     }
-    dst[i] = hash_weight(base, lr * cols + col, a);
+    dst[di] = hash_weight(base, lr * cols + col, a);
   }
 }
 

@@ -52,6 +52,8 @@ constexpr int kNumMats = 6;
 // split over K across the two grid halves (GemvArgs.ksplit = 1)
 constexpr int kMatDownS = 6;
 
+constexpr int kTcMaxWp = 128;  // layers (incl. the exit-head layer) whose weight pointers ride in the launch
+
 struct GemvArgs {
   Work* work;
   int32_t layer_i;        // layer offset inside each stage
@@ -87,6 +89,25 @@ struct GemvArgs {
   // stale publication can never be mistaken for a later one.
   int32_t* part_flag;
   int32_t* err;  // sticky device error word (kGemvErrSplitTimeout), checked by the host
+  // tensor-core GEMV (tcgemv.cu): TC-tiled weight layout and ring plan
+  int32_t js, nj;       // 64-wide K slabs per J-block, J-blocks
+  int32_t nb, tg;       // J-blocks per ring stage, max 8-row groups per tile
+  int32_t nblk;         // 16-column B blocks reserved per stage (<= 3: 16 vectors x 3 parts)
+  int32_t bar_off;      // smem offset of the mbarriers
+  // this matrix's weights per global layer index (launch parameters: the
+  // producer issues its first copy without a dependent load of LayerW)
+  const void* wp[kTcMaxWp];
+  // ... or, when every layer's matrix sits at a fixed stride from layer 0's
+  // (one allocation per matrix kind), base + layer * stride for layers < wn
+  const void* wbase;
+  long long wstride;
+  int32_t wn;
+};
+
+// tensor-core GEMV plan (tcgemv.cu: tc_pick)
+struct TcPlan {
+  int R = 0, K = 0, js = 1, nj = 0, nb = 1, tg = 1, nblk = 1, ns = 0, bar_off = 0, cs = 1, grid = 0;
+  size_t smem = 0;
 };
 constexpr int kSplitChunks = 64;  // epilogue chunk slots per CTA pair (sequence-numbered, may wrap)
 constexpr int kGemvErrSplitTimeout = 1;
@@ -162,6 +183,31 @@ int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int
               size_t* smem);
 cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st);
 cudaError_t gemv_set_attrs(int vpt, int m, int mat, int ksplit, size_t smem);
+// TC-tiled weight layout (tcgemv.cu header comment): K padded to KP
+// (multiple of 64) and cut into J-blocks of JS 64-wide slabs, rows into
+// 8-row groups; element (r, k) sits in the 1 KB SWIZZLE_128B atom
+// [k / (64 JS)][r / 8][(k / 64) % JS], row r % 8, 16-byte chunk
+// ((k % 64) / 8) ^ (r % 8). JS = 4 where K allows (one CTA's J-block copy
+// is tg * 4 KB); a property of the matrix shape only.
+__host__ __device__ inline void tc_layout(int R, int K, int* js, int* kp) {
+  (void)R;
+  const int KP = (K + 63) / 64 * 64, NSL = KP / 64;
+  *js = NSL % 4 == 0 ? 4 : NSL % 2 == 0 ? 2 : 1;
+  *kp = KP;
+}
+// element offset of (r, k) in a TC-tiled [R][K] matrix
+__host__ __device__ inline long long tc_offset(int R, int K, long long r, long long k) {
+  int JS, KP;
+  tc_layout(R, K, &JS, &KP);
+  const long long G = R / 8;
+  const long long slab = k / 64, j = slab / JS, s = slab % JS, g = r / 8, rr = r % 8, c = (k % 64) / 8, e = k % 8;
+  return ((((j * G + g) * JS + s) * 8 + rr) * 64) + ((c ^ rr) * 8) + e;
+}
+
+// tensor-core GEMV (tcgemv.cu); weights in the TC-tiled layout
+int tc_pick(int K, int R, int nblk, int grid, TcPlan* p);
+cudaError_t tc_set_attrs(int mat, int cs, size_t smem);
+cudaError_t tc_launch(const GemvArgs& a, int cs, size_t smem, int grid, cudaStream_t st);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 bool umma_shape_ok(int R, int K);

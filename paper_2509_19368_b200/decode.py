@@ -59,6 +59,7 @@ class Engine:
         self.h = h
         self.max_ctx = model_desc.max_ctx
         self._vocab = model_desc.vocab
+        self._d_model = model_desc.d_model
         self.last = None
         self._fin = weakref.finalize(self, L.ppsd_engine_destroy, h)
 
@@ -180,6 +181,18 @@ class Engine:
         out = np.zeros(V, dtype=np.float32)
         _lib.check(_lib.lib().ppsd_read_logits(self.h, which, out.ctypes.data_as(C.POINTER(C.c_float))),
                    "read_logits")
+        return out
+
+    def debug_matvec(self, which: int, layer: int, x: np.ndarray, batched: bool) -> np.ndarray:
+        """GEMV unit check: y = W x for the O (which=1) or down (which=3)
+        projection of `layer`, x [nv][K] fp32 -> [nv][R] fp32, through the
+        shipped kernel (parity tests)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        nv = x.shape[0]
+        out = np.zeros((nv, self._d_model), dtype=np.float32)
+        _lib.check(_lib.lib().ppsd_debug_matvec(self.h, which, layer, nv, int(batched),
+                                                x.ctypes.data_as(C.POINTER(C.c_float)),
+                                                out.ctypes.data_as(C.POINTER(C.c_float))), "debug_matvec")
         return out
 
     def set_logits_tap(self, tap=None) -> None:

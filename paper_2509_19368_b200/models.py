@@ -14,12 +14,16 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
 
 from . import _lib
 
+LAYOUT_TC_TILED = 16  # include/ppsd.h PPSD_LAYOUT_TC_TILED
+# PPSD_GEMV=cc: row-major weights for the CUDA-core GEMV (A/B experiments only)
+TC_TILED = not os.environ.get("PPSD_GEMV", "tc").startswith("c")
 INIT_SALT = 0x5EED_B200_C0FF_EE01  # keep in sync with csrc/engine.cu ppsd_init_weight
 TID_EMBED, TID_LM_HEAD = 0xE0, 0xE1
 TID_WQ, TID_WK, TID_WV, TID_WO, TID_WGATE, TID_WUP, TID_WDOWN = 1, 2, 3, 4, 5, 6, 7
@@ -190,18 +194,38 @@ class TransformerLM:
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
 
-            def init(rows, cols, layout, tids, scales):
-                t = torch.empty(rows, cols, dtype=bf, device=dev)
+            pools = {}
+
+            def init(rows, cols, layout, tids, scales, tiled=True, pool=None):
+                # GEMV matrices live in the tensor-core GEMV's TC-tiled layout
+                # (include/ppsd.h PPSD_LAYOUT_TC_TILED); the embedding is gathered by
+                # rows and stays plain. pool: the layers' matrices of one kind are
+                # slices of one allocation, so they sit at a fixed stride (the GEMV
+                # computes their address instead of loading it)
+                tiled = tiled and TC_TILED
+                n = C.c_int64(0)
+                _lib.check(L.ppsd_weight_elems(int(tiled), rows, cols, C.byref(n)), "weight_elems")
+                if pool is not None:
+                    buf, step, used = pools.get(pool, (None, 0, 0))
+                    if buf is None:
+                        step = (n.value + 127) // 128 * 128  # 256-byte aligned slices
+                        buf = torch.empty(step * (hi - lo), dtype=bf, device=dev)
+                    t = buf[used * step:used * step + n.value]
+                    pools[pool] = (buf, step, used + 1)
+                else:
+                    t = torch.empty(n.value, dtype=bf, device=dev)
                 tid_arr = (C.c_uint64 * 3)(*(list(tids) + [0] * (3 - len(tids))))
                 sc_arr = (C.c_float * 3)(*(list(scales) + [0.0] * (3 - len(scales))))
-                _lib.check(L.ppsd_init_weight(C.c_void_p(t.data_ptr()), layout, rows, cols,
+                lay = layout | (LAYOUT_TC_TILED if tiled else 0)
+                _lib.check(L.ppsd_init_weight(C.c_void_p(t.data_ptr()), lay, rows, cols,
                                               seed & ((1 << 64) - 1), tid_arr, sc_arr, c.n_heads,
                                               c.n_kv_heads, c.head_dim, C.c_void_p(stream)),
                            "init")
                 return t
 
             s_d = init_scale(c.d_model)
-            self.embed = init(c.vocab, c.d_model, 0, [TID_EMBED], [float(np.float32(math.sqrt(3.0)))]) \
+            self.embed = init(c.vocab, c.d_model, 0, [TID_EMBED], [float(np.float32(math.sqrt(3.0)))],
+                              tiled=False) \
                 if need_embed else None
             self.lm_head = init(c.vocab, c.d_model, 0, [TID_LM_HEAD], [s_d]) if need_head else None
             ones = lambda: torch.ones(c.d_model, dtype=torch.float32, device=dev)  # noqa: E731
@@ -213,12 +237,14 @@ class TransformerLM:
                 ds = self.deep_scale if layer >= self.deep_from else 1.0
                 self.w_qkv[layer] = init(qd + 2 * kvd, c.d_model, 1,
                                          [layer_tid(layer, TID_WQ), layer_tid(layer, TID_WK),
-                                          layer_tid(layer, TID_WV)], [s_d, s_d, s_d])
-                self.w_o[layer] = init(c.d_model, qd, 0, [layer_tid(layer, TID_WO)], [init_scale(qd, ds)])
+                                          layer_tid(layer, TID_WV)], [s_d, s_d, s_d], pool="qkv")
+                self.w_o[layer] = init(c.d_model, qd, 0, [layer_tid(layer, TID_WO)], [init_scale(qd, ds)],
+                                       pool="o")
                 self.w_gu[layer] = init(2 * c.ffn_dim, c.d_model, 2,
-                                        [layer_tid(layer, TID_WGATE), layer_tid(layer, TID_WUP)], [s_d, s_d])
+                                        [layer_tid(layer, TID_WGATE), layer_tid(layer, TID_WUP)], [s_d, s_d],
+                                        pool="gu")
                 self.w_down[layer] = init(c.d_model, c.ffn_dim, 0, [layer_tid(layer, TID_WDOWN)],
-                                          [init_scale(c.ffn_dim, ds)])
+                                          [init_scale(c.ffn_dim, ds)], pool="down")
                 self.attn_norm[layer], self.mlp_norm[layer] = ones(), ones()
             self.exit_layer_w = None
             if exit_head == "layer":  # the exit head's decoder layer: layer index N in the init ids
