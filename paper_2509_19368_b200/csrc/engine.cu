@@ -49,6 +49,15 @@ struct WStride {
   int n = 0;  // layers [0, n) follow base + l * stride
 };
 
+// persistent layer pass (tcpass.cu): ring / shared-memory plan for one B width
+struct PassPlan {
+  bool ok = false;
+  int nblk = 1, ns = 0, slot_bytes = 0, b_stage = 0, attn_off = 0, attn_kv_bytes = 0, scr_off = 0, bar_off = 0,
+      workers = 1;
+  int nb[4] = {1, 1, 1, 1};
+  size_t smem = 0;
+};
+
 struct GemvPlan {
   int vpt = 0, tr = 0, m = 1, ns = 0, sub = 1, R = 0, K = 0;
   int ksplit = 0, K_full = 0;  // K split across the two grid halves (K = K_full / 2)
@@ -70,6 +79,11 @@ struct ppsd_engine {
   bool tc = true;  // tensor-core GEMV (weights TC-tiled)
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
   bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
+  // persistent layer pass: [0] groups of <= 5 vectors, [1] <= 16
+  bool pass = false;
+  int pass_cs = 1;
+  PassPlan pp[2];
+  unsigned long long* d_pass_bar = nullptr;  // [0] arrivals, [1] base of the next pass, [2] done count
   cudaStream_t st = nullptr;
   SchedCfg cfg{};
   int S = 0, lo = 1, hi = 1, max_local_layers = 0, first_local_layer = 0, n_local_layers = 0;
@@ -179,6 +193,8 @@ static cudaError_t note_launch(cudaError_t e) {
 // ---------------------------------------------------------------------------
 // enqueue helpers (also used while capturing graphs)
 
+static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, const GemvPlan& p, float* logits);
+
 static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, bool batched = false,
                                 float* logits = nullptr) {
   // tensor-core GEMV: groups of <= 5 vectors (the folded deep batch at
@@ -186,6 +202,15 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   // room for a deeper weight ring; the arithmetic is the same in every plan
   const bool use_b = batched && !(e->tc && e->small_batch);
   const GemvPlan& p = use_b ? e->gpb[mat] : e->gp[mat];
+  GemvArgs a = make_gemv_args(e, w, layer_i, mat, p, logits);
+  if (e->tc) {
+    const TcPlan& t = p.tc;
+    return note_launch(tc_launch(a, t.cs, t.smem, t.grid, e->st));
+  }
+  return note_launch(gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st));
+}
+
+static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, const GemvPlan& p, float* logits) {
   GemvArgs a{};
   a.work = w;
   a.layer_i = layer_i;
@@ -238,15 +263,11 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
     a.tg = t.tg;
     a.nblk = t.nblk;
     a.bar_off = t.bar_off;
-    return note_launch(tc_launch(a, t.cs, t.smem, t.grid, e->st));
   }
-  return note_launch(gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st));
+  return a;
 }
 
-static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
-  // PPSD_PROFILE_SKIP_ATTN=1: timing experiments only (wrong results)
-  static const bool skip = getenv("PPSD_PROFILE_SKIP_ATTN") && atoi(getenv("PPSD_PROFILE_SKIP_ATTN")) != 0;
-  if (skip) return cudaSuccess;
+static AttnArgs make_attn_args(ppsd_engine* e, Work* w, int layer_i) {
   AttnArgs a{};
   a.work = w;
   a.layer_i = layer_i;
@@ -263,7 +284,14 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   a.first_local = e->first_local_layer;
   a.hl_global = e->hl ? e->md.n_layers : -1;
   a.hl_local = e->n_local_layers;
-  return attn_launch(a, attn_grid(e), e->st);
+  return a;
+}
+
+static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
+  // PPSD_PROFILE_SKIP_ATTN=1: timing experiments only (wrong results)
+  static const bool skip = getenv("PPSD_PROFILE_SKIP_ATTN") && atoi(getenv("PPSD_PROFILE_SKIP_ATTN")) != 0;
+  if (skip) return cudaSuccess;
+  return attn_launch(make_attn_args(e, w, layer_i), attn_grid(e), e->st);
 }
 
 static cudaError_t enqueue_umma(ppsd_engine* e, Work* w, int layer_i, int mat) {
@@ -312,8 +340,57 @@ static int enqueue_prefill_layers(ppsd_engine* e, Work* w, int n_slots) {
   return n;
 }
 
+static int setup_pass(ppsd_engine* e);
+
+// One persistent launch for n_slots layer slots (tcpass.cu); -1 on error.
+static int enqueue_pass(ppsd_engine* e, Work* w, int n_slots, bool batched) {
+  const bool big = batched && !e->small_batch;
+  const PassPlan& pl = e->pp[big ? 1 : 0];
+  TcPassArgs a{};
+  const GemvPlan& pq = big ? e->gpb[kMatQKV] : e->gp[kMatQKV];
+  a.g = make_gemv_args(e, w, 0, kMatQKV, pq, nullptr);
+  a.at = make_attn_args(e, w, 0);
+  for (int m = 0; m < 4; ++m) {
+    const TcPlan& t = (big ? e->gpb[m] : e->gp[m]).tc;
+    TcPassMat& M = a.mat[m];
+    M.R = t.R;
+    M.K = t.K;
+    M.js = t.js;
+    M.nj = t.nj;
+    M.tg = t.tg;
+    M.cs = t.cs;
+    M.nb = pl.nb[m];
+    M.wbase = e->wstride[m].base;
+    M.wstride = e->wstride[m].stride;
+    M.wn = e->wstride[m].n;
+  }
+  a.n_slots = n_slots;
+  a.desc_early = 0;
+  a.ns = pl.ns;
+  a.slot_bytes = pl.slot_bytes;
+  a.b_stage = pl.b_stage;
+  a.nblk = pl.nblk;
+  a.attn_off = pl.attn_off;
+  a.attn_kv_bytes = pl.attn_kv_bytes;
+  a.scr_off = pl.scr_off;
+  a.bar_off = pl.bar_off;
+  a.attn_workers = pl.workers;
+  // L2 prefetch distance per CTA (PPSD_PASS_PREFETCH=<KB>, default 384): the
+  // grid's prefetched weights (~57 MB) stay well inside the 126 MB L2
+  static const unsigned long long pf = getenv("PPSD_PASS_PREFETCH") ? (unsigned long long)atoll(getenv("PPSD_PASS_PREFETCH")) * 1024
+                                                                    : 384ull * 1024;
+  a.prefetch_bytes = pf;
+  a.bar_cnt = e->d_pass_bar;
+  a.bar_seq = e->d_pass_bar + 1;
+  a.done_cnt = reinterpret_cast<uint32_t*>(e->d_pass_bar + 2);
+  const cudaError_t ce = note_launch(tc_pass_launch(a, e->pass_cs, e->dm.hd, e->dm.H / e->dm.KV, e->dm.kv_bf16,
+                                                    pl.smem, e->num_sms / e->pass_cs * e->pass_cs, e->st));
+  return ce == cudaSuccess ? 1 : -1;
+}
+
 // returns launches enqueued, or -1 on error
 static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
+  if (e->pass && n_slots > 0) return enqueue_pass(e, w, n_slots, batched);
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
     if (enqueue_gemv(e, w, i, kMatQKV, batched) != cudaSuccess) return -1;
@@ -886,6 +963,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     // 13B shape (d 5120, ffn 13824) the spilling batched plans made folded
     // slower than pipelined (194 vs 218 tok/s), on 7B faster (391 vs 317).
     e->fold_auto = e->fold_ok && (e->tc || e->gpb[kMatQKV].vpt <= 2);
+    if (int rc = setup_pass(e)) return rc;
     if (pd->schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
       return fail(PPSD_EUNSUPPORTED, "folded schedule needs all stages on this device and at most " +
                                          std::to_string(kMaxVec) + " chains in flight");
@@ -926,6 +1004,82 @@ extern "C" int ppsd_engine_destroy(ppsd_engine* e) {
   return PPSD_OK;
 }
 
+// Persistent layer pass (tcpass.cu): on when the engine owns its device (all
+// stages local, PDL on: the grid barriers need every CTA resident; several
+// engines sharing a GPU run the per-kernel sequence, same arithmetic), the
+// head geometry has a pass instantiation and PPSD_PASS != 0.
+static int setup_pass(ppsd_engine* e) {
+  e->pass = false;
+  // measured slower than the per-kernel sequence on the 7B shape (DESIGN.md
+  // §8): opt-in experiment (PPSD_PASS=1)
+  const char* ev = getenv("PPSD_PASS");
+  if (!(ev && ev[0] == '1') || !e->tc || e->lo != 1 || e->hi != e->S || !ppsd::g_pdl) return PPSD_OK;
+  const int qpk = e->dm.H / e->dm.KV;
+  if (!tc_pass_supported(e->dm.hd, qpk)) return PPSD_OK;
+  int cs = 1;
+  for (int m = 0; m < 4; ++m) cs = std::max(cs, std::max(e->gp[m].tc.cs, e->gpb[m].tc.cs));
+  if (cs > 2) return PPSD_OK;
+  const size_t kv_el = e->dm.kv_bf16 ? 2 : 4;
+  const size_t kvb = 2 * (size_t)kPage * e->dm.hd * kv_el;          // one worker's K + V page blocks
+  const size_t scr = (tc_pass_scratch_bytes(e->dm.hd, qpk, e->dm.kv_bf16) + 127) / 128 * 128;
+  const size_t cap = 221 * 1024;
+  for (int v = 0; v < 2; ++v) {
+    PassPlan& pl = e->pp[v];
+    pl = PassPlan{};
+    pl.nblk = v ? 3 : 1;
+    size_t slot = 0, over = 0;
+    for (int m = 0; m < 4; ++m) {
+      const TcPlan& t = (v ? e->gpb[m] : e->gp[m]).tc;
+      slot = std::max(slot, (size_t)t.tg * t.js * 1024);
+      over = std::max(over, (size_t)(16 - t.tg) * t.js * 1024);
+    }
+    size_t bst = 0;
+    for (int m = 0; m < 4; ++m) {
+      const TcPlan& t = (v ? e->gpb[m] : e->gp[m]).tc;
+      const size_t jb = (size_t)t.tg * t.js * 1024;
+      int nb = (int)(slot / jb);
+      const int njr = (t.nj + t.cs - 1) / t.cs;
+      nb = std::max(1, std::min(nb, njr));
+      pl.nb[m] = nb;
+      bst = std::max(bst, (size_t)nb * pl.nblk * t.js * 2048);
+    }
+    const size_t recv = cs > 1 ? (size_t)kMaxVec * 128 * 4 : 0;
+    const int cands[][2] = {{4, 2}, {3, 2}, {4, 1}, {3, 1}, {2, 2}, {2, 1}};
+    for (const auto& c : cands) {
+      const int ns = c[0], wk = c[1];
+      const size_t ring = (size_t)ns * slot;
+      const size_t uni = std::max((size_t)ns * bst, (size_t)wk * kvb);
+      const size_t pad = over > uni ? over - uni : 0;
+      const size_t scr_off = (ring + uni + pad + 127) / 128 * 128;
+      const size_t bar_off = scr_off + (size_t)wk * scr;
+      const size_t total = bar_off + 256 + recv + 1024;
+      if (total > cap) continue;
+      pl.ok = true;
+      pl.ns = ns;
+      pl.workers = wk;
+      pl.slot_bytes = (int)slot;
+      pl.b_stage = (int)bst;
+      pl.attn_off = (int)ring;
+      pl.attn_kv_bytes = (int)kvb;
+      pl.scr_off = (int)scr_off;
+      pl.bar_off = (int)bar_off;
+      pl.smem = total;
+      break;
+    }
+    if (!pl.ok) return PPSD_OK;
+    CU(tc_pass_set_attrs(cs, e->dm.hd, qpk, e->dm.kv_bf16, cap));  // one kernel serves both plans
+    if (getenv("PPSD_TC_VERBOSE"))
+      fprintf(stderr, "tc pass plan %d: CS %d NS %d workers %d slot %d b_stage %d smem %zu\n", v, cs, pl.ns,
+              pl.workers, pl.slot_bytes, pl.b_stage, pl.smem);
+  }
+  CU(cudaSetDevice(e->device));
+  CU(dalloc(&e->d_pass_bar, 3 * sizeof(unsigned long long)));
+  CU(cudaMemset(e->d_pass_bar, 0, 3 * sizeof(unsigned long long)));
+  e->pass_cs = cs;
+  e->pass = true;
+  return PPSD_OK;
+}
+
 // ---------------------------------------------------------------------------
 // decode
 
@@ -933,12 +1087,13 @@ extern "C" int ppsd_engine_destroy(ppsd_engine* e) {
 // down projection gave up waiting for its partner's row sums is reported
 // as PPSD_ESTATE, never returned as tokens. Called after the stream drained.
 static int check_kerr(ppsd_engine* e) {
-  if (!e->gp[kMatDown].ksplit) return PPSD_OK;  // the only writer
+  if (!e->gp[kMatDown].ksplit && !e->pass) return PPSD_OK;  // the only writers
   int32_t v = 0;
   CU(cudaMemcpy(&v, e->d_kerr, sizeof(v), cudaMemcpyDeviceToHost));
   if (v == 0) return PPSD_OK;
   CU(cudaMemset(e->d_kerr, 0, sizeof(v)));
-  return fail(PPSD_ESTATE, "K-split down projection: partner row sums timed out (results discarded)");
+  return fail(PPSD_ESTATE, v & kGemvErrPassTimeout ? "layer pass: a grid barrier timed out (results discarded)"
+                                                  : "K-split down projection: partner row sums timed out (results discarded)");
 }
 
 static int check_prompt(const ppsd_engine* e, const int32_t* prompt, int n_prompt) {
@@ -1584,12 +1739,18 @@ extern "C" int ppsd_debug_matvec(ppsd_engine* e, int32_t which, int32_t layer, i
 namespace ppsd {
 int tc_trace_enable(int on);
 int tc_trace_read(unsigned long long* out);  // [8][128] + [160][4]
+int tc_pass_trace_enable(int on);
+int tc_pass_trace_read(unsigned long long* out);  // [8][128]
 }
 // tensor-core GEMV pipeline timeline of CTA 0 (debugging): on = 1 records the
 // next launches, out = [8][128] %globaltimer ns of the last one
 extern "C" int ppsd_debug_tc_trace(int32_t on, uint64_t* out) {
-  if (on >= 0 && tc_trace_enable(on)) return fail(PPSD_ECUDA, "trace enable");
-  if (out && tc_trace_read(reinterpret_cast<unsigned long long*>(out))) return fail(PPSD_ECUDA, "trace read");
+  // on / out & 2 (bit 1 of on >= 2): the layer pass's trace instead of the GEMV's
+  const bool pass = on >= 2 || (on < 0 && out && (on & 2));
+  if (on >= 0 && (pass ? tc_pass_trace_enable(on & 1) : tc_trace_enable(on))) return fail(PPSD_ECUDA, "trace enable");
+  if (out && (on == -2 ? tc_pass_trace_read(reinterpret_cast<unsigned long long*>(out))
+                       : tc_trace_read(reinterpret_cast<unsigned long long*>(out))))
+    return fail(PPSD_ECUDA, "trace read");
   return PPSD_OK;
 }
 

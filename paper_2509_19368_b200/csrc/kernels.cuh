@@ -111,6 +111,7 @@ struct TcPlan {
 };
 constexpr int kSplitChunks = 64;  // epilogue chunk slots per CTA pair (sequence-numbered, may wrap)
 constexpr int kGemvErrSplitTimeout = 1;
+constexpr int kGemvErrPassTimeout = 2;  // a layer-pass grid barrier waited > 5 s
 
 struct AttnArgs {
   const Work* work;
@@ -129,6 +130,27 @@ struct AttnArgs {
   int32_t first_local;  // global index of the first local layer
   int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
   int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
+};
+
+// one matrix of the persistent layer pass (tcpass.cu); the arithmetic plan
+// (js, nj, cs) is the standalone GEMV's, tg / nb follow the pass's ring
+struct TcPassMat {
+  int32_t R, K, js, nj, tg, nb, cs, wn;
+  const void* wbase;  // layers at a fixed stride (else LayerW)
+  long long wstride;
+};
+struct TcPassArgs {
+  GemvArgs g;          // shared fields: work, layers, dims, activations, RoPE, page table, err
+  AttnArgs at;         // attention of the pass (layer_i set per slot)
+  TcPassMat mat[4];    // kMatQKV, kMatO, kMatGU, kMatDown
+  int32_t n_slots;     // layer slots (layer_i = 0 .. n_slots-1 of every active group)
+  int32_t desc_early;  // 1: the work descriptor was written >= 2 kernels ago
+  int32_t ns, slot_bytes, b_stage, nblk;  // weight ring slots, operand stage bytes, B blocks
+  int32_t attn_off, attn_kv_bytes, scr_off, bar_off, attn_workers;
+  unsigned long long prefetch_bytes;  // L2 prefetch distance of the weight producer (bytes ahead)
+  unsigned long long* bar_cnt;  // grid-barrier arrivals (monotone)
+  unsigned long long* bar_seq;  // arrivals at the end of the previous pass
+  uint32_t* done_cnt;           // CTAs finished (the last publishes bar_seq)
 };
 
 // tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
@@ -208,6 +230,11 @@ __host__ __device__ inline long long tc_offset(int R, int K, long long r, long l
 int tc_pick(int K, int R, int nblk, int grid, TcPlan* p);
 cudaError_t tc_set_attrs(int mat, int cs, size_t smem);
 cudaError_t tc_launch(const GemvArgs& a, int cs, size_t smem, int grid, cudaStream_t st);
+bool tc_pass_supported(int hd, int qpk);
+size_t tc_pass_scratch_bytes(int hd, int qpk, int kv_bf16);
+cudaError_t tc_pass_set_attrs(int cs, int hd, int qpk, int kv_bf16, size_t smem);
+cudaError_t tc_pass_launch(const TcPassArgs& a, int cs, int hd, int qpk, int kv_bf16, size_t smem, int grid,
+                           cudaStream_t st);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 bool umma_shape_ok(int R, int K);
