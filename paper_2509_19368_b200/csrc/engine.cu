@@ -79,6 +79,7 @@ struct ppsd_engine {
   bool tc = true;  // tensor-core GEMV (weights TC-tiled)
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
   bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
+  int hint_first = -1;       // capturing single-problem launches whose first layer is known (speculative start)
   // persistent layer pass: [0] groups of <= 5 vectors, [1] <= 16
   bool pass = false;
   int pass_cs = 1;
@@ -240,8 +241,14 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
   a.part_buf = e->d_part;
   a.part_flag = e->d_part_flag;
   a.err = e->d_kerr;
+  a.hint_li = -1;
   if (e->tc) {
     const TcPlan& t = p.tc;
+    // speculative start: measured slower on the 7B bench (427 vs 437 tok/s,
+    // DESIGN.md §8), opt-in PPSD_TC_HINT=1
+    static const bool hints = getenv("PPSD_TC_HINT") && getenv("PPSD_TC_HINT")[0] == '1';
+    if (hints && (mat == kMatHead || mat == kMatHeadV)) a.hint_li = 0;  // one problem at most, the LM head
+    else if (hints && e->hint_first >= 0) a.hint_li = e->hint_first + layer_i;
     if (mat == kMatHead || mat == kMatHeadV) {
       a.wp[0] = e->lm_head;
     } else {
@@ -461,7 +468,9 @@ static int build_fold_graph(ppsd_engine* e) {
            cudaSuccess, "sched");
   n_outer = 1;
   if (ok) {
+    e->hint_first = e->lo == 1 ? 0 : -1;  // sched.cu: the launched chain's layers [0, shallow)
     const int m = enqueue_layers(e, e->d_work, shallow, false);
+    e->hint_first = -1;
     need(m >= 0, "shallow layers");
     n_outer += m;
   }
@@ -479,7 +488,9 @@ static int build_fold_graph(ppsd_engine* e) {
   // tick; without a batch its kernels find no work and exit
   const char* cv = getenv("PPSD_FOLD_COND");
   if (ok && cv && atoi(cv) == 0) {
+    e->hint_first = shallow;
     const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+    e->hint_first = -1;
     need(m >= 0, "deep layers");
     need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
          "final heads");
@@ -515,7 +526,9 @@ static int build_fold_graph(ppsd_engine* e) {
     if (ok) {
       e->st = body_st;
       e->small_batch = sched_fold_width(&e->cfg) <= 5;
+      e->hint_first = shallow;  // sched.cu: the batch's layers [shallow, N)
       const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+      e->hint_first = -1;
       need(m >= 0, "deep layers");
       n_body = m;
       need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
@@ -579,7 +592,9 @@ static int build_graphs(ppsd_engine* e) {
         if (launch_pdl(ar_begin_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
             cudaSuccess)
           return -1;
+        e->hint_first = e->first_local_layer;  // ar_begin_kernel: first = the first local layer
         int m = enqueue_layers(e, e->d_work_ar, e->n_local_layers, false);
+        e->hint_first = -1;
         if (m < 0) return -1;
         if (enqueue_gemv(e, e->d_work_ar, 0, kMatHead) != cudaSuccess) return -1;
         if (launch_pdl(ar_end_kernel, dim3(1), dim3(256), 0, e->st, (const TickCtx*)e->d_ctx, e->d_arctl, 1) !=
@@ -1087,13 +1102,14 @@ static int setup_pass(ppsd_engine* e) {
 // down projection gave up waiting for its partner's row sums is reported
 // as PPSD_ESTATE, never returned as tokens. Called after the stream drained.
 static int check_kerr(ppsd_engine* e) {
-  if (!e->gp[kMatDown].ksplit && !e->pass) return PPSD_OK;  // the only writers
+  if (!e->gp[kMatDown].ksplit && !e->pass && !e->tc) return PPSD_OK;  // the only writers
   int32_t v = 0;
   CU(cudaMemcpy(&v, e->d_kerr, sizeof(v), cudaMemcpyDeviceToHost));
   if (v == 0) return PPSD_OK;
   CU(cudaMemset(e->d_kerr, 0, sizeof(v)));
-  return fail(PPSD_ESTATE, v & kGemvErrPassTimeout ? "layer pass: a grid barrier timed out (results discarded)"
-                                                  : "K-split down projection: partner row sums timed out (results discarded)");
+  return fail(PPSD_ESTATE, v & kGemvErrHint ? "GEMV speculative start: hint did not match the work (results discarded)"
+                          : v & kGemvErrPassTimeout ? "layer pass: a grid barrier timed out (results discarded)"
+                          : "K-split down projection: partner row sums timed out (results discarded)");
 }
 
 static int check_prompt(const ppsd_engine* e, const int32_t* prompt, int n_prompt) {

@@ -102,6 +102,9 @@ struct GemvArgs {
   const void* wbase;
   long long wstride;
   int32_t wn;
+  // >= 0: the launch has at most one problem, layer hint_li (any value for
+  // the heads): the producer starts streaming before reading the descriptor
+  int32_t hint_li;
 };
 
 // tensor-core GEMV plan (tcgemv.cu: tc_pick)
@@ -112,6 +115,7 @@ struct TcPlan {
 constexpr int kSplitChunks = 64;  // epilogue chunk slots per CTA pair (sequence-numbered, may wrap)
 constexpr int kGemvErrSplitTimeout = 1;
 constexpr int kGemvErrPassTimeout = 2;  // a layer-pass grid barrier waited > 5 s
+constexpr int kGemvErrHint = 4;         // a speculative-start hint did not match the work descriptor
 
 struct AttnArgs {
   const Work* work;

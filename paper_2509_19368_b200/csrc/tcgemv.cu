@@ -104,6 +104,53 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
     tc_trace(6, 0);
     tc_cta_mark(0);
   }
+  // Speculative start (a.hint_li >= 0: the caller guarantees the launch has
+  // at most one problem, layer hint_li / the LM head): the producer issues
+  // the first ring stages before reading the work descriptor (and, for the
+  // first kernel of a tick, before the scheduler kernel has finished).
+  __shared__ int s_spec;  // stages issued speculatively
+  int spec_n = 0;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 2);      // producer (expect_tx) + the builder warp of the stage
+      mbar_init(&empty[i], 1);     // MMA commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);  // epilogue warps
+    }
+    if (CS > 1) {
+      mbar_init(recv_full, 4 * (CS - 1));  // every epilogue warp of the other ranks
+      mbar_init(recv_empty, 4);            // the leader's epilogue warps
+    }
+    fence_mbar_init();
+    const unsigned char* wsp = nullptr;
+    if (a.hint_li >= 0) {
+      if (kHead) wsp = reinterpret_cast<const unsigned char*>(a.head_w);
+      else if (a.wstride && a.hint_li < a.wn)
+        wsp = reinterpret_cast<const unsigned char*>(a.wbase) + (size_t)a.hint_li * a.wstride;
+    }
+    if (wsp) {  // the first tile of this CTA's share of one problem
+      const int sc = CS > 1 ? (int)cluster_rank() : 0;
+      const int snc = (int)gridDim.x / CS, sb = (int)blockIdx.x / CS;
+      const int su0 = (int)((long long)G * sb / snc), su1 = (int)((long long)G * (sb + 1) / snc);
+      const int sjlo = NJ * sc / CS, sjhi = NJ * (sc + 1) / CS;
+      TcTiles tl;
+      tl.init(su0, su1, G, TG);
+      int tp, g0, tg;
+      if (su0 < su1 && tl.next(tp, g0, tg)) {
+        const uint64_t pol = policy_evict_first();
+        const uint32_t tb = (uint32_t)tg * JSB;
+        for (int j = sjlo; j < sjhi && spec_n < NS; j += NB, ++spec_n) {
+          const int nbj = min(NB, sjhi - j);
+          mbar_expect_tx(&full[spec_n], (uint32_t)nbj * tb);
+          for (int jj = 0; jj < nbj; ++jj)
+            bulk_g2s(smem + (size_t)spec_n * w_stage + (size_t)jj * tb, wsp + ((size_t)(j + jj) * G + g0) * JSB, tb,
+                     &full[spec_n], pol);
+        }
+      }
+    }
+  }
   if (!a.desc_early) pdl_wait();
   if (tid == 0) {
     int np = 0;
@@ -119,22 +166,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           s_nv[np++] = work->nv[g];
         }
     }
+    if (spec_n > 0 && np == 1 && !kHead && s_li[0] != a.hint_li) {
+      // a wrong hint is a caller bug: flag it (the decode reports PPSD_ESTATE)
+      // and run nothing; the speculative copies are drained below
+      atomicOr(a.err, kGemvErrHint);
+      np = 0;
+    }
+    if (np > 1 && spec_n > 0) {
+      atomicOr(a.err, kGemvErrHint);
+      np = 0;
+    }
     s_np = np;
+    s_spec = np == 1 ? spec_n : 0;
+    if (np == 0 && spec_n > 0) {  // nothing to do: let the copies land before exit
+      for (int i = 0; i < spec_n; ++i) {
+        mbar_arrive(&full[i]);
+        mbar_wait(&full[i], 0);
+      }
+    }
     tc_trace(7, 0);
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&full[i], 2);      // producer (expect_tx) + the builder warp of the stage
-      mbar_init(&empty[i], 1);     // MMA commit
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);  // epilogue warps
-    }
-    if (CS > 1) {
-      mbar_init(recv_full, 4 * (CS - 1));  // every epilogue warp of the other ranks
-      mbar_init(recv_empty, 4);            // the leader's epilogue warps
-    }
-    fence_mbar_init();
-    tc_trace(7, 1);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_taddr)),
@@ -198,6 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           for (int j = jlo; j < jhi; j += NB, ++n) {
             const int nbj = min(NB, jhi - j);
             const int st = n % NS;
+            if (n < s_spec) continue;  // issued before the work descriptor was read
             if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
             if (g_tc_exp & 1) {
               mbar_arrive(&full[st]);
@@ -728,7 +779,7 @@ int tc_pick(int K, int R, int nblk, int num_sms, TcPlan* p) {
   const int G = R / 8, NJ = KP / 64 / JS;
   int best_cs = 1;
   double best = 1e30;
-  for (int cs : {1, 2}) {  // clusters of 4 fit only ~33 at once on 148 SMs (the pass needs all SMs)
+  for (int cs : {1, 2, 4}) {
     if (cs > NJ) break;
     int ncl = num_sms / cs;
     if (cs > 1) {
@@ -746,7 +797,7 @@ int tc_pick(int K, int R, int nblk, int num_sms, TcPlan* p) {
   int CS = best_cs;
   if (const char* v = getenv("PPSD_TC_CS")) {  // experiments: force the split-K cluster size
     const int f = atoi(v);
-    if ((f == 1 || f == 2 || f == 4) && f <= NJ) CS = f;
+    if ((f == 1 || f == 2 || f == 4) && f <= NJ && CS > 1) CS = f;  // matrices that split at all
   }
   int ncl = num_sms / CS;
   if (CS > 1) {
