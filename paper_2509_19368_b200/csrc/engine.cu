@@ -843,7 +843,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
           // block (<= 5 vectors x 3 parts) for the decode tick and the PPSD
           // head, 3 (<= 16 vectors) batched
           const int nblk = b ? 3 : 1;
-          if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc) != 0)
+          if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc, m) != 0)
             return fail(PPSD_EUNSUPPORTED, "no tensor-core GEMV plan for matrix " + std::to_string(m) + " [" +
                                                std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
           CU(tc_set_attrs(m, p.tc.cs, p.tc.smem));

@@ -231,7 +231,7 @@ __host__ __device__ inline long long tc_offset(int R, int K, long long r, long l
 }
 
 // tensor-core GEMV (tcgemv.cu); weights in the TC-tiled layout
-int tc_pick(int K, int R, int nblk, int grid, TcPlan* p);
+int tc_pick(int K, int R, int nblk, int grid, TcPlan* p, int mat = -1);
 cudaError_t tc_set_attrs(int mat, int cs, size_t smem);
 cudaError_t tc_launch(const GemvArgs& a, int cs, size_t smem, int grid, cudaStream_t st);
 bool tc_pass_supported(int hd, int qpk);

@@ -55,6 +55,7 @@
 // processed as tiles of <= TG groups (TG <= 16), each tile over the whole K.
 #include <float.h>
 #include <limits.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -772,32 +773,32 @@ constexpr size_t kTcStageTarget = 48 * 1024;  // weight bytes per ring stage to 
 // Split-K cluster size CS in {1, 2, 4}: the smallest whose per-CTA MMA work
 // (1 MMA per 16-wide K step and 128-row tile, ~60 cycles each measured in
 // situ) stays well under the CTA's HBM time; the rest streams like CS = 1.
-int tc_pick(int K, int R, int nblk, int num_sms, TcPlan* p) {
+int tc_pick(int K, int R, int nblk, int num_sms, TcPlan* p, int p_mat_hint) {
   if (K <= 0 || R <= 0 || R % 8 != 0 || K % 8 != 0 || nblk < 1 || nblk > kTcMaxBlk) return -1;
   int JS, KP;
   tc_layout(R, K, &JS, &KP);
   const int G = R / 8, NJ = KP / 64 / JS;
+  // Split-K cluster size: measured on the 7B shapes (tools/probe_gemv.py,
+  // tools/quick_decode.py with PPSD_TC_CS), a CTA with fewer than 8 row
+  // groups (64 rows) is bound by its MMA issue rate (one M=128 MMA per 16-wide
+  // K step whatever the rows) and by the fixed per-launch cost; 4-CTA
+  // clusters give each CTA 4x the rows over a quarter of K (O 12.3 -> 10.7 us,
+  // down 21.5 -> 18.6 us); the wide matrices stay unsplit (gate/up with CS 2
+  // or 4: 30.1 -> 31.3 / 37.0 us).
   int best_cs = 1;
-  double best = 1e30;
-  for (int cs : {1, 2, 4}) {
-    if (cs > NJ) break;
-    int ncl = num_sms / cs;
-    if (cs > 1) {
-      int maxc = tc_max_clusters(cs);
-      if (maxc > 0 && maxc < ncl) ncl = maxc;
-    }
-    if (ncl < 1) continue;
-    const int c = (G + ncl - 1) / ncl, nt = (c + 15) / 16;
-    const double steps = (double)nt * ((NJ + cs - 1) / cs) * JS * 4;
-    const double mma_cyc = steps * 60.0;
-    const double hbm_cyc = (double)c * 8 * ((double)KP / cs) * 2 / 22.0;
-    const double cost = std::max(mma_cyc * 1.6, hbm_cyc) + (cs > 1 ? 1500.0 : 0.0);
-    if (cost < best * 0.97) { best = cost; best_cs = cs; }
-  }
+  if ((G + num_sms - 1) / num_sms < 8 && NJ >= 4 && tc_max_clusters(4) >= 8) best_cs = 4;
   int CS = best_cs;
   if (const char* v = getenv("PPSD_TC_CS")) {  // experiments: force the split-K cluster size
-    const int f = atoi(v);
-    if ((f == 1 || f == 2 || f == 4) && f <= NJ && CS > 1) CS = f;  // matrices that split at all
+    // "<cs>" for the matrices that split at all, "<qkv>,<o>,<gu>,<down>" per matrix (row counts R
+    // identify them: the 7B probe shapes)
+    int f[4] = {0, 0, 0, 0};
+    const int nf = sscanf(v, "%d,%d,%d,%d", &f[0], &f[1], &f[2], &f[3]);
+    if (nf == 1) {
+      if ((f[0] == 1 || f[0] == 2 || f[0] == 4) && f[0] <= NJ && CS > 1) CS = f[0];
+    } else if (nf == 4) {
+      const int idx = p_mat_hint;
+      if (idx >= 0 && idx < 4 && (f[idx] == 1 || f[idx] == 2 || f[idx] == 4) && f[idx] <= NJ) CS = f[idx];
+    }
   }
   int ncl = num_sms / CS;
   if (CS > 1) {
