@@ -270,6 +270,30 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
     a.tg = t.tg;
     a.nblk = t.nblk;
     a.bar_off = t.bar_off;
+    // L2 prefetch of the next GEMV of the layer: QKV -> O the whole O slice
+    // (attention leaves HBM idle in between), O -> GU, GU -> down, down -> next
+    // QKV the first 96 KB per CTA (the next launch's first stages; measured
+    // 443.3 -> 446.9 tok/s, 192 KB: 444.1). PPSD_TC_NEXT=<KB> overrides.
+    static const int nx_kb = getenv("PPSD_TC_NEXT") ? atoi(getenv("PPSD_TC_NEXT")) : 96;
+    if (mat <= kMatDown && (mat == kMatQKV || nx_kb > 0)) {
+      const int nm = (mat + 1) % 4;
+      const GemvPlan& np_ = &p == &e->gpb[mat] ? e->gpb[nm] : e->gp[nm];
+      const WStride& ws = e->wstride[nm];
+      if (ws.stride) {
+        TcNext& X = a.nx;
+        X.wbase = ws.base;
+        X.wstride = ws.stride;
+        X.wn = ws.n;
+        X.dli = mat == kMatDown ? 1 : 0;
+        X.R = np_.tc.R;
+        X.js = np_.tc.js;
+        X.nj = np_.tc.nj;
+        X.tg = np_.tc.tg;
+        X.cs = np_.tc.cs;
+        const long long slice = (long long)np_.tc.R * np_.tc.K * 2 / std::max(1, np_.tc.grid) + (1 << 16);
+        X.bytes = mat == kMatQKV ? (int)std::min<long long>(slice, 1 << 30) : nx_kb * 1024;
+      }
+    }
   }
   return a;
 }

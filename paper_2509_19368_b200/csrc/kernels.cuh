@@ -52,7 +52,17 @@ constexpr int kNumMats = 6;
 // split over K across the two grid halves (GemvArgs.ksplit = 1)
 constexpr int kMatDownS = 6;
 
-constexpr int kTcMaxWp = 128;  // layers (incl. the exit-head layer) whose weight pointers ride in the launch
+constexpr int kTcMaxWp = 128;
+
+// the next GEMV of the decoder layer, for the producer's L2 prefetch
+struct TcNext {
+  const void* wbase;     // layer 0's matrix; nullptr: no prefetch
+  long long wstride;     // bytes between layers
+  int32_t wn;            // layers [0, wn) at the stride
+  int32_t dli;           // layer offset from this launch's (0: same layer, 1: next layer)
+  int32_t R, js, nj, tg, cs;
+  int32_t bytes;         // per CTA
+};  // layers (incl. the exit-head layer) whose weight pointers ride in the launch
 
 struct GemvArgs {
   Work* work;
@@ -105,6 +115,10 @@ struct GemvArgs {
   // >= 0: the launch has at most one problem, layer hint_li (any value for
   // the heads): the producer starts streaming before reading the descriptor
   int32_t hint_li;
+  // L2 prefetch of the NEXT GEMV's weights (this CTA's slice of its first
+  // nx_bytes), issued after this launch's last copy: it lands while the
+  // launch drains, the next launch starts and (QKV -> O) attention runs
+  TcNext nx;
 };
 
 // tensor-core GEMV plan (tcgemv.cu: tc_pick)

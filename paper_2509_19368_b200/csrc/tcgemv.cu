@@ -274,6 +274,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           pdl_wait();
           pdl_trigger();
         }
+        // the next GEMV's weights into L2: this CTA's slice of the next
+        // matrix (same tile split as that launch), first nx.bytes of it
+        if (a.nx.wbase && np == 1 && !kHead) {
+          const TcNext& X = a.nx;
+          const int li = s_li[0] + X.dli;
+          if (li < X.wn) {
+            const unsigned char* xw = reinterpret_cast<const unsigned char*>(X.wbase) + (size_t)li * X.wstride;
+            const int xG = X.R >> 3, xncl = (int)gridDim.x / X.cs;
+            if ((int)blockIdx.x < xncl * X.cs) {
+              const int xb = (int)blockIdx.x / X.cs, xr = (int)blockIdx.x % X.cs;
+              const int xu0 = (int)((long long)xG * xb / xncl), xu1 = (int)((long long)xG * (xb + 1) / xncl);
+              const int xjlo = X.nj * xr / X.cs, xjhi = X.nj * (xr + 1) / X.cs;
+              const uint32_t xJSB = (uint32_t)X.js << 10;
+              TcTiles xt;
+              xt.init(xu0, xu1, xG, X.tg);
+              int xp, xg0, xtg, left = X.bytes;
+              while (left > 0 && xt.next(xp, xg0, xtg)) {
+                const uint32_t xtb = (uint32_t)xtg * xJSB;
+                for (int j = xjlo; j < xjhi && left > 0; ++j, left -= (int)xtb)
+                  prefetch_l2(xw + ((size_t)j * xG + xg0) * xJSB, xtb);
+              }
+            }
+          }
+        }
       } else {
         pdl_wait();
         pdl_trigger();

@@ -87,9 +87,6 @@ __device__ __forceinline__ void pass_share(const TcPassMat& M, int np, PassShare
   s.jhi = M.nj * (s.crank + 1) / M.cs;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 
 // The producer's walk over the weight stages of a pass: (layer slot i,
 // matrix m, tile, J-blocks [j, j + nbj)) in the order every role uses.
