@@ -361,8 +361,8 @@ def run_ours(args):
                 "note": "public decode_ppsd call incl. prefill of the 128-token prompt"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": (f"gemv_kernel<gate/up + SwiGLU>, one vector, {gu_bytes / 1e6:.0f} MB per launch"
-                                if folded else f"gemv_kernel<gate/up>, {cfg.n_stages} stages per launch"),
+                     "kernel": (f"tcgemv_kernel<gate/up + SwiGLU> (tcgen05), one vector, {gu_bytes / 1e6:.0f} MB per launch"
+                                if folded else f"tcgemv_kernel<gate/up>, {cfg.n_stages} stages per launch"),
                      "algorithmic_bytes": gu_bytes, "peak_kind": peak_kind, "avg_ms": round(gu_ms, 4)},
         "kernels": kern,
         "step_roofline": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / hbm, 4),

@@ -1,6 +1,6 @@
 // attn.cu — standalone split-K decode attention kernel: one 128-thread
-// worker (attn_core.cuh) per CTA. The O-projection GEMV runs the same worker
-// code fused (gemv.cu) where the grid may synchronise (engine.cu).
+// worker (attn_core.cuh) per CTA. The persistent layer pass (tcpass.cu) runs
+// the same worker code between its QKV and O phases.
 #include "attn_core.cuh"
 
 namespace ppsd {

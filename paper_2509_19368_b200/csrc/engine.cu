@@ -59,18 +59,9 @@ struct PassPlan {
 };
 
 struct GemvPlan {
-  int vpt = 0, tr = 0, m = 1, ns = 0, sub = 1, R = 0, K = 0;
-  int ksplit = 0, K_full = 0;  // K split across the two grid halves (K = K_full / 2)
-  size_t smem = 0;
-  TcPlan tc;                   // tensor-core GEMV plan (e->tc)
+  int m = 1, R = 0, K = 0;  // vectors per weight pass, matrix shape
+  TcPlan tc;                // tensor-core GEMV plan (tcgemv.cu)
 };
-
-// PPSD_GEMV=cc: the CUDA-core GEMV over row-major weights (A/B experiments);
-// default: the tensor-core GEMV over TC-tiled weights
-static bool gemv_tc_env() {
-  const char* v = getenv("PPSD_GEMV");
-  return !(v && v[0] == 'c');
-}
 
 struct ppsd_engine {
   ppsd_model_desc md{};
@@ -97,8 +88,6 @@ struct ppsd_engine {
   Work* d_work_head = nullptr;  // exit-head layer (md.exit_head_layer)
   Work* d_work_p2 = nullptr;       // prefill: layers after the exit (exit-head layer)
   Work* d_work_head_pf = nullptr;  // prefill's exit-head layer
-  float* d_part = nullptr;         // K-split down projection: second half's row sums
-  int32_t* d_part_flag = nullptr;  // ... and their per-chunk sequence numbers
   int32_t* d_kerr = nullptr;       // sticky GEMV error word (K-split wait timeout)
   bool hl = false;              // exit head has a decoder layer
   TickCtx* d_ctx = nullptr;
@@ -119,14 +108,6 @@ struct ppsd_engine {
   GemvPlan gp[kNumMats];   // decode tick: one vector per weight pass (head: exit + final)
   GemvPlan gpb[kNumMats];  // batched prefill / EESD verify: up to 4 vectors per pass
   int nbuf = 0;            // activation slots (>= nslot, >= kMaxVec)
-  // tcgen05 prefill (umma.cu): weight tensor maps [n_layers][4], activation
-  // operand per input width (d, H*hd, ffn) with its map, split-tile scratch
-  bool umma = false;
-  void* d_wmaps = nullptr;
-  void* d_xmaps = nullptr;
-  __nv_bfloat16* d_xs[3] = {nullptr, nullptr, nullptr};
-  float* d_umws = nullptr;
-  int32_t* d_umcnt = nullptr;
   uint64_t verify_seed = 0;  // sampling mode: derive_seed(rng.seed, "verify")
   double *d_pdist = nullptr, *d_qbuf = nullptr, *d_wbuf = nullptr, *d_logits64 = nullptr;
   const __nv_bfloat16* lm_head = nullptr;
@@ -201,14 +182,11 @@ static cudaError_t enqueue_gemv(ppsd_engine* e, Work* w, int layer_i, int mat, b
   // tensor-core GEMV: groups of <= 5 vectors (the folded deep batch at
   // E >= N/5) run the decode-tick plan, whose smaller operand stages leave
   // room for a deeper weight ring; the arithmetic is the same in every plan
-  const bool use_b = batched && !(e->tc && e->small_batch);
+  const bool use_b = batched && !e->small_batch;
   const GemvPlan& p = use_b ? e->gpb[mat] : e->gp[mat];
   GemvArgs a = make_gemv_args(e, w, layer_i, mat, p, logits);
-  if (e->tc) {
-    const TcPlan& t = p.tc;
-    return note_launch(tc_launch(a, t.cs, t.smem, t.grid, e->st));
-  }
-  return note_launch(gemv_launch(a, p.vpt, p.m, p.smem, e->num_sms, e->st));
+  const TcPlan& t = p.tc;
+  return note_launch(tc_launch(a, t.cs, t.smem, t.grid, e->st));
 }
 
 static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, const GemvPlan& p, float* logits) {
@@ -223,8 +201,6 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
   a.head_norm1 = e->final_norm;
   a.R = p.R;
   a.K = p.K;
-  a.nstage = p.ns;
-  a.sub = p.sub;
   a.dm = e->dm;
   a.x = e->d_x;
   a.q = e->d_q;
@@ -236,13 +212,9 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
   a.page_table = e->d_page_table;
   a.head_part = e->d_head_part;
   a.head_cnt = e->d_head_cnt;
-  a.ksplit = p.ksplit;
-  a.k_ld = p.K_full;
-  a.part_buf = e->d_part;
-  a.part_flag = e->d_part_flag;
   a.err = e->d_kerr;
   a.hint_li = -1;
-  if (e->tc) {
+  {
     const TcPlan& t = p.tc;
     // speculative start: measured slower on the 7B bench (427 vs 437 tok/s,
     // DESIGN.md §8), opt-in PPSD_TC_HINT=1
@@ -325,50 +297,12 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
   return attn_launch(make_attn_args(e, w, layer_i), attn_grid(e), e->st);
 }
 
-static cudaError_t enqueue_umma(ppsd_engine* e, Work* w, int layer_i, int mat) {
-  const int Rq = (e->dm.H + 2 * e->dm.KV) * e->dm.hd;
-  const int R[4] = {Rq, e->dm.d, 2 * e->dm.ffn, e->dm.d};
-  const int K[4] = {e->dm.d, e->dm.H * e->dm.hd, e->dm.d, e->dm.ffn};
-  const int xi = mat == kMatO ? 1 : mat == kMatDown ? 2 : 0;
-  UmmaArgs a{};
-  a.work = w;
-  a.layer_i = layer_i;
-  a.mat = mat;
-  a.R = R[mat];
-  a.K = K[mat];
-  a.layers = e->d_layers;
-  a.wmaps = e->d_wmaps;
-  a.xmap = static_cast<const unsigned char*>(e->d_xmaps) + xi * umma_map_bytes();
-  a.xs = e->d_xs[xi];
-  a.dm = e->dm;
-  a.x = e->d_x;
-  a.q = e->d_q;
-  a.o = e->d_o;
-  a.h = e->d_h;
-  a.rope_cos = e->rope_cos;
-  a.rope_sin = e->rope_sin;
-  a.page_table = e->d_page_table;
-  a.ws = e->d_umws;
-  a.cnt = e->d_umcnt;
-  return umma_launch(a, e->num_sms, e->st);
-}
-
 // Prompt layers for a chunk of <= kMaxVec vectors in group 0 of `w`: the
-// tcgen05 GEMM when planned (2 launches per matrix: operand staging + GEMM),
-// else the batched GEMV. Returns launches enqueued, or -1.
+// batched tensor-core GEMV plans (every vector of the chunk in one weight
+// pass). Returns launches enqueued, or -1.
 static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched);
 static int enqueue_prefill_layers(ppsd_engine* e, Work* w, int n_slots) {
-  if (!e->umma) return enqueue_layers(e, w, n_slots, true);
-  int n = 0;
-  for (int i = 0; i < n_slots; ++i) {
-    if (enqueue_umma(e, w, i, kMatQKV) != cudaSuccess) return -1;
-    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
-    if (enqueue_umma(e, w, i, kMatO) != cudaSuccess) return -1;
-    if (enqueue_umma(e, w, i, kMatGU) != cudaSuccess) return -1;
-    if (enqueue_umma(e, w, i, kMatDown) != cudaSuccess) return -1;
-    n += 9;
-  }
-  return n;
+  return enqueue_layers(e, w, n_slots, true);
 }
 
 static int setup_pass(ppsd_engine* e);
@@ -676,12 +610,11 @@ static void free_engine(ppsd_engine* e) {
                   (void*)e->d_xerr})
     if (b) cudaFree(b);
   if (e->d_eesd) cudaFree(e->d_eesd);
-  for (void* b : {e->d_wmaps, e->d_xmaps, (void*)e->d_xs[0], (void*)e->d_xs[1], (void*)e->d_xs[2],
-                  (void*)e->d_umws, (void*)e->d_umcnt})
+  for (void* b : {(void*)e->d_pass_bar})
     if (b) cudaFree(b);
   for (void* b : e->retired) cudaFree(b);
   void* bufs[] = {e->d_sched, e->d_work, e->d_work_ar, e->d_work_deep, e->d_work_head, e->d_work_p2,
-                  e->d_work_head_pf, e->d_part, e->d_part_flag, e->d_kerr, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
+                  e->d_work_head_pf, e->d_kerr, e->d_ctx, e->d_arctl, e->d_tokens, e->d_pdig,
                   e->d_chain_dig, e->d_trace, e->d_layers, e->d_x, e->d_q, e->d_o, e->d_h, e->d_logits,
                   e->d_attn_part, e->d_head_part, e->d_attn_cnt, e->d_head_cnt, e->d_page_table, e->d_kv,
                   e->d_pdist, e->d_qbuf, e->d_wbuf, e->d_logits64};
@@ -701,44 +634,6 @@ static cudaError_t dalloc(T** p, size_t bytes) {
   cudaError_t r = cudaMalloc(reinterpret_cast<void**>(p), bytes);
   if (r == cudaSuccess) r = cudaMemset(*p, 0, bytes);
   return r;
-}
-
-// tcgen05 prefill plan: tensor maps over every local layer's matrices. Off
-// (batched GEMV prefill) when a matrix does not tile by 128 x 128 or with
-// PPSD_UMMA=0.
-static int setup_umma(ppsd_engine* e, const int (*shapes)[2]) {
-  const char* env = getenv("PPSD_UMMA");
-  if (env && atoi(env) == 0) return PPSD_OK;
-  for (int m = kMatQKV; m <= kMatDown; ++m)
-    if (!umma_shape_ok(shapes[m][0], shapes[m][1])) return PPSD_OK;
-  const int L = (int)e->h_layers.size();  // + the exit-head layer
-  const size_t mb = umma_map_bytes();
-  std::vector<unsigned char> maps((size_t)L * 4 * mb, 0);
-  for (int l = 0; l < L; ++l) {
-    const LayerW& W = e->h_layers[l];
-    if (!W.qkv) continue;
-    const void* ptr[4] = {W.qkv, W.o, W.gu, W.down};
-    for (int m = 0; m < 4; ++m)
-      if (umma_encode_map(&maps[((size_t)l * 4 + m) * mb], ptr[m], shapes[m][0], shapes[m][1], umma_tile_rows()))
-        return PPSD_OK;  // no driver tensor-map entry point: stay on the GEMV prefill
-  }
-  const int widths[3] = {e->dm.d, e->dm.H * e->dm.hd, e->dm.ffn};
-  std::vector<unsigned char> xm(3 * mb, 0);
-  for (int i = 0; i < 3; ++i) {
-    CU(dalloc(&e->d_xs[i], sizeof(__nv_bfloat16) * 2 * umma_n() * (size_t)widths[i]));
-    if (umma_encode_map(&xm[i * mb], e->d_xs[i], 2 * umma_n(), widths[i], umma_n())) return PPSD_OK;
-  }
-  CU(cudaMalloc(&e->d_wmaps, maps.size()));
-  CU(cudaMemcpy(e->d_wmaps, maps.data(), maps.size(), cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&e->d_xmaps, xm.size()));
-  CU(cudaMemcpy(e->d_xmaps, xm.data(), xm.size(), cudaMemcpyHostToDevice));
-  int tiles = 0;
-  for (int m = kMatQKV; m <= kMatDown; ++m) tiles = std::max(tiles, shapes[m][0] / umma_tile_rows());
-  CU(dalloc(&e->d_umws, sizeof(float) * (size_t)e->num_sms * 2 * umma_tile_rows() * umma_n()));
-  CU(dalloc(&e->d_umcnt, sizeof(int32_t) * tiles));
-  CU(umma_set_attrs());
-  e->umma = true;
-  return PPSD_OK;
 }
 
 static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const ppsd_pipeline_desc* pd,
@@ -774,7 +669,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   const int max_ctx = md->max_ctx > 0 ? md->max_ctx : 4096;
   e->md.max_ctx = max_ctx;
   const int nslot = e->cfg.nslot;
-  e->nbuf = std::max(nslot, std::max((int)kMaxVec, umma_n()));  // + a tcgen05 prefill chunk
+  e->nbuf = std::max(nslot, (int)kMaxVec);  // + a prefill chunk / EESD verify group
 
   CU(dalloc(&e->d_sched, sizeof(Sched)));
   CU(dalloc(&e->d_work, sizeof(Work)));
@@ -805,7 +700,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
   c.n_layers = md->n_layers;
   c.vocab = md->vocab;
   c.model_stages = e->cfg.S;
-  c.prefill_chunk = kMaxVec;  // transformer engines: set after setup_umma
+  c.prefill_chunk = kMaxVec;
 
   if (md->kind == PPSD_MODEL_TOYLM) {
     if (md->vocab < 2) return fail(PPSD_EINVAL, "vocab must be >= 2");
@@ -839,48 +734,26 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         (need_head && !w->lm_head))
       return fail(PPSD_EINVAL, "missing transformer weights");
     const int Rq = (d.H + 2 * d.KV) * d.hd;
-    // PPSD_DOWN_SPLIT (read per engine, recorded in the plan): 0 disables
-    // the K split of the down projection (DESIGN.md environment knobs)
-    const char* dsv = getenv("PPSD_DOWN_SPLIT");
-    e->tc = gemv_tc_env();
-    const bool split_on = !e->tc && !(dsv && dsv[0] == '0') && e->lo == 1 && e->hi == e->S && ppsd::g_pdl;
     const int shapes[kNumMats][2] = {{Rq, d.d}, {d.d, d.H * d.hd}, {2 * d.ffn, d.d},
                                      {d.d, d.ffn}, {d.V, d.d}, {d.V, d.d}};
     for (int m = 0; m < kNumMats; ++m) {
       for (int b = 0; b < 2; ++b) {
-        if ((m == kMatHead && b) || (m == kMatHeadV && !b && !e->tc)) continue;
+        if (m == kMatHead && b) continue;
         GemvPlan& p = b ? e->gpb[m] : e->gp[m];
         p.R = shapes[m][0];
-        p.K = p.K_full = shapes[m][1];
-        // Wide down projections (K > 8192): each grid half streams one column
-        // half (half the input slice per thread), in every plan, so M = 1 and
-        // batched results agree. The two halves exchange row sums through
-        // spin-waits, so the split runs only where the engine's grid owns the
-        // device: not for stage-subset engines (several may share one GPU)
-        // and not without PDL (PPSD_PDL=0 is the shared-device mode).
-        if (m == kMatDown && split_on && p.K > 8192 && (p.K / 2) % 8 == 0 && e->num_sms % 2 == 0) {
-          p.ksplit = 1;
-          p.K = p.K / 2;
-        }
-        if (e->tc) {
-          // one weight pass for every vector of a group: one 16-column B
-          // block (<= 5 vectors x 3 parts) for the decode tick and the PPSD
-          // head, 3 (<= 16 vectors) batched
-          const int nblk = b ? 3 : 1;
-          if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc, m) != 0)
-            return fail(PPSD_EUNSUPPORTED, "no tensor-core GEMV plan for matrix " + std::to_string(m) + " [" +
-                                               std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
-          CU(tc_set_attrs(m, p.tc.cs, p.tc.smem));
-          if (getenv("PPSD_TC_VERBOSE"))
-            fprintf(stderr, "tc plan mat %d b %d: R %d K %d JS %d NJ %d CS %d grid %d TG %d nb %d NS %d smem %zu\n", m, b,
-                    p.R, p.K, p.tc.js, p.tc.nj, p.tc.cs, p.tc.grid, p.tc.tg, p.tc.nb, p.tc.ns, p.tc.smem);
-          p.m = b ? kMaxVec : (m == kMatHead ? 2 : 1);
-          continue;
-        }
-        if (gemv_pick(p.K, p.R, m, b, &p.vpt, &p.tr, &p.m, &p.ns, &p.sub, &p.smem) != 0)
-          return fail(PPSD_EUNSUPPORTED, "no GEMV tiling for matrix " + std::to_string(m) + " [" +
+        p.K = shapes[m][1];
+        // one weight pass for every vector of a group: one 16-column B block
+        // (<= 5 vectors x 3 parts) for the decode tick, the folded deep batch
+        // and the PPSD head; 3 (<= 16 vectors) for prefill chunks and EESD
+        const int nblk = b ? 3 : 1;
+        if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc, m) != 0)
+          return fail(PPSD_EUNSUPPORTED, "no tensor-core GEMV plan for matrix " + std::to_string(m) + " [" +
                                              std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
-        CU(gemv_set_attrs(p.vpt, p.m, m, p.ksplit, p.smem));
+        CU(tc_set_attrs(m, p.tc.cs, p.tc.smem));
+        if (getenv("PPSD_TC_VERBOSE"))
+          fprintf(stderr, "tc plan mat %d b %d: R %d K %d JS %d NJ %d CS %d grid %d TG %d nb %d NS %d smem %zu\n", m, b,
+                  p.R, p.K, p.tc.js, p.tc.nj, p.tc.cs, p.tc.grid, p.tc.tg, p.tc.nb, p.tc.ns, p.tc.smem);
+        p.m = b ? kMaxVec : (m == kMatHead ? 2 : 1);
       }
     }
     {
@@ -973,10 +846,6 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_h, sizeof(float) * nb * d.ffn));
-    if (e->gp[kMatDown].ksplit) {
-      CU(dalloc(&e->d_part, sizeof(float) * nb * d.d));
-      CU(dalloc(&e->d_part_flag, sizeof(int32_t) * 2 * (size_t)e->num_sms * kSplitChunks));
-    }
     CU(dalloc(&e->d_logits, sizeof(float) * (kMaxVec + 1) * (size_t)d.V));  // folded: exit + batch rows
     CU(dalloc(&e->d_attn_part, sizeof(float) * nb * d.H * e->max_pages * (d.hd + 2)));
     CU(dalloc(&e->d_attn_cnt, sizeof(int32_t) * nb * d.KV));
@@ -984,12 +853,9 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     CU(dalloc(&e->d_head_cnt, sizeof(int32_t) * kMaxVec));
     c.logits32 = e->d_logits;
     c.x = e->d_x;
-    int rc = e->tc ? PPSD_OK : setup_umma(e, shapes);  // umma.cu reads row-major weights
-    if (rc) return rc;
-    // prompt tokens per prefill chunk: one tcgen05 weight pass (umma_n()), or
-    // the batched-GEMV chunk
+    // prompt tokens per prefill chunk: one batched weight pass
     {
-      const int cmax = e->umma ? umma_n() : (int)kMaxVec;
+      const int cmax = (int)kMaxVec;
       c.prefill_chunk = cmax;
       if (const char* v = getenv("PPSD_PREFILL_CHUNK")) c.prefill_chunk = std::min(std::max(atoi(v), 1), cmax);
     }
@@ -997,11 +863,9 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
     e->schedule = pd->schedule;
     e->fold_ok = e->lo == 1 && e->hi == e->S && sched_fold_width(&e->cfg) <= kMaxVec &&
                  pd->schedule != PPSD_SCHEDULE_PIPELINED;
-    // AUTO folds where the batched GEMVs keep their input slices in registers
-    // without spilling (K = d_model <= 4096: 7B-class layers). Measured on the
-    // 13B shape (d 5120, ffn 13824) the spilling batched plans made folded
-    // slower than pipelined (194 vs 218 tok/s), on 7B faster (391 vs 317).
-    e->fold_auto = e->fold_ok && (e->tc || e->gpb[kMatQKV].vpt <= 2);
+    // AUTO folds wherever it can: the tensor-core GEMV streams a weight once
+    // for every vector of the deep batch at the cost of one vector
+    e->fold_auto = e->fold_ok;
     if (int rc = setup_pass(e)) return rc;
     if (pd->schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
       return fail(PPSD_EUNSUPPORTED, "folded schedule needs all stages on this device and at most " +
@@ -1052,7 +916,7 @@ static int setup_pass(ppsd_engine* e) {
   // measured slower than the per-kernel sequence on the 7B shape (DESIGN.md
   // §8): opt-in experiment (PPSD_PASS=1)
   const char* ev = getenv("PPSD_PASS");
-  if (!(ev && ev[0] == '1') || !e->tc || e->lo != 1 || e->hi != e->S || !ppsd::g_pdl) return PPSD_OK;
+  if (!(ev && ev[0] == '1') || e->lo != 1 || e->hi != e->S || !ppsd::g_pdl) return PPSD_OK;
   const int qpk = e->dm.H / e->dm.KV;
   if (!tc_pass_supported(e->dm.hd, qpk)) return PPSD_OK;
   int cs = 1;
@@ -1122,18 +986,17 @@ static int setup_pass(ppsd_engine* e) {
 // ---------------------------------------------------------------------------
 // decode
 
-// Sticky GEMV error word (K-split wait timeout, gemv.cu): a decode whose
-// down projection gave up waiting for its partner's row sums is reported
-// as PPSD_ESTATE, never returned as tokens. Called after the stream drained.
+// Sticky GEMV error word (tcgemv.cu / tcpass.cu: a speculative-start hint
+// that did not match the work descriptor, a layer-pass grid barrier that
+// timed out): such a decode is reported as PPSD_ESTATE, never returned as
+// tokens. Called after the stream drained.
 static int check_kerr(ppsd_engine* e) {
-  if (!e->gp[kMatDown].ksplit && !e->pass && !e->tc) return PPSD_OK;  // the only writers
   int32_t v = 0;
   CU(cudaMemcpy(&v, e->d_kerr, sizeof(v), cudaMemcpyDeviceToHost));
   if (v == 0) return PPSD_OK;
   CU(cudaMemset(e->d_kerr, 0, sizeof(v)));
   return fail(PPSD_ESTATE, v & kGemvErrHint ? "GEMV speculative start: hint did not match the work (results discarded)"
-                          : v & kGemvErrPassTimeout ? "layer pass: a grid barrier timed out (results discarded)"
-                          : "K-split down projection: partner row sums timed out (results discarded)");
+                          : "layer pass: a grid barrier timed out (results discarded)");
 }
 
 static int check_prompt(const ppsd_engine* e, const int32_t* prompt, int n_prompt) {
@@ -1736,7 +1599,7 @@ extern "C" int ppsd_probe_gemv(ppsd_engine* e, int32_t which, int32_t n_groups, 
   CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
   const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
   *avg_ms = ms / reps;
-  *bytes_per_launch = (double)p.R * (p.ksplit ? p.K_full : p.K) * 2.0 * (head ? 1 : ng);
+  *bytes_per_launch = (double)p.R * p.K * 2.0 * (head ? 1 : ng);
   return PPSD_OK;
 }
 
@@ -1753,7 +1616,7 @@ extern "C" int ppsd_debug_matvec(ppsd_engine* e, int32_t which, int32_t layer, i
     return fail(PPSD_EINVAL, "matvec: layer not local");
   CU(cudaSetDevice(e->device));
   const GemvPlan& p = batched ? e->gpb[which] : e->gp[which];
-  const int K = p.K_full, R = p.R;
+  const int K = p.K, R = p.R;
   Work w{};
   w.G = 1;
   w.slot[0] = 0;

@@ -52,7 +52,7 @@ constexpr int kNumMats = 6;
 // split over K across the two grid halves (GemvArgs.ksplit = 1)
 constexpr int kMatDownS = 6;
 
-constexpr int kTcMaxWp = 128;
+constexpr int kTcMaxWp = 128;  // layers (incl. the exit-head layer) whose weight pointers ride in the launch
 
 // the next GEMV of the decoder layer, for the producer's L2 prefetch
 struct TcNext {
@@ -62,7 +62,7 @@ struct TcNext {
   int32_t dli;           // layer offset from this launch's (0: same layer, 1: next layer)
   int32_t R, js, nj, tg, cs;
   int32_t bytes;         // per CTA
-};  // layers (incl. the exit-head layer) whose weight pointers ride in the launch
+};
 
 struct GemvArgs {
   Work* work;
@@ -73,8 +73,7 @@ struct GemvArgs {
   const __nv_bfloat16* head_w;
   const float* head_norm0;  // exit norm
   const float* head_norm1;  // final norm
-  int32_t R, K, nstage;
-  int32_t sub;            // tiles (TR rows each) per bulk-copy stage
+  int32_t R, K, nstage;   // matrix [R][K], weight-ring stages
   Dims dm;
   float* x;   // [nslot][d]   residual stream (fp32)
   float* q;   // [nslot][H*hd]
@@ -86,19 +85,7 @@ struct GemvArgs {
   const int32_t* page_table;
   float* head_part;  // [grid][kMaxVec][2] (value, index-as-float bits)
   int32_t* head_cnt; // [kMaxVec] arrival tickets
-  // K split (wide down projections, ksplit = 1): the two halves of the grid
-  // stream the two column halves [h*K, h*K + K) of rows k_ld long; the CTAs
-  // streaming the second column half (low blockIdx, dispatched first)
-  // publish their row sums (part_buf + a publication count), their partners
-  // add them in fixed order before the residual add
-  int32_t ksplit, k_ld;
-  float* part_buf;     // [nslot][d]
-  // [2][grid][kSplitChunks] monotone sequence numbers per (CTA pair, chunk
-  // slot): [0] publications by the second-half CTA, [1] consumptions by its
-  // partner. A wait is for "publications > consumptions", so a late or
-  // stale publication can never be mistaken for a later one.
-  int32_t* part_flag;
-  int32_t* err;  // sticky device error word (kGemvErrSplitTimeout), checked by the host
+  int32_t* err;  // sticky device error word (kGemvErr*), checked by the host
   // tensor-core GEMV (tcgemv.cu): TC-tiled weight layout and ring plan
   int32_t js, nj;       // 64-wide K slabs per J-block, J-blocks
   int32_t nb, tg;       // J-blocks per ring stage, max 8-row groups per tile
@@ -126,8 +113,6 @@ struct TcPlan {
   int R = 0, K = 0, js = 1, nj = 0, nb = 1, tg = 1, nblk = 1, ns = 0, bar_off = 0, cs = 1, grid = 0;
   size_t smem = 0;
 };
-constexpr int kSplitChunks = 64;  // epilogue chunk slots per CTA pair (sequence-numbered, may wrap)
-constexpr int kGemvErrSplitTimeout = 1;
 constexpr int kGemvErrPassTimeout = 2;  // a layer-pass grid barrier waited > 5 s
 constexpr int kGemvErrHint = 4;         // a speculative-start hint did not match the work descriptor
 
@@ -171,28 +156,6 @@ struct TcPassArgs {
   uint32_t* done_cnt;           // CTAs finished (the last publishes bar_seq)
 };
 
-// tcgen05 prefill GEMM (umma.cu): one matrix of one layer for the chunk of
-// up to 16 vectors in group 0 of `work`.
-struct UmmaArgs {
-  const Work* work;
-  int32_t layer_i;
-  int32_t mat;           // kMatQKV / kMatO / kMatGU / kMatDown
-  int32_t R, K;
-  const LayerW* layers;
-  const void* wmaps;     // CUtensorMap [n_layers][4] over the weight matrices
-  const void* xmap;      // CUtensorMap over xs
-  __nv_bfloat16* xs;     // [32][K] activation operand: rows 0-15 hi, 16-31 lo
-  Dims dm;
-  float* x;
-  float* q;
-  float* o;
-  float* h;
-  const float* rope_cos;
-  const float* rope_sin;
-  const int32_t* page_table;
-  float* ws;             // [grid][2][128][16] split-tile partials
-  int32_t* cnt;          // [R / 128] arrival tickets
-};
 
 // Programmatic dependent launch (PDL): every kernel of a decode step is
 // launched with programmatic stream serialization so it can be scheduled
@@ -215,14 +178,7 @@ cudaError_t launch_pdl(Kern fn, dim3 grid, dim3 block, size_t smem, cudaStream_t
   return cudaLaunchKernelEx(&cfg, fn, args...);
 }
 
-// launchers (gemv.cu / attn.cu)
-// A GEMV plan: `m` = vectors per weight pass (1 for the decode tick; up to 4
-// for batched prefill / EESD verify, where a group of nv vectors takes
-// ceil(nv/m) passes).
-int gemv_pick(int K, int R, int mat, int batched, int* vpt, int* tr, int* m, int* nstage, int* sub,
-              size_t* smem);
-cudaError_t gemv_launch(const GemvArgs& a, int vpt, int m, size_t smem, int grid, cudaStream_t st);
-cudaError_t gemv_set_attrs(int vpt, int m, int mat, int ksplit, size_t smem);
+// launchers (tcgemv.cu / tcpass.cu / attn.cu)
 // TC-tiled weight layout (tcgemv.cu header comment): K padded to KP
 // (multiple of 64) and cut into J-blocks of JS 64-wide slabs, rows into
 // 8-row groups; element (r, k) sits in the 1 KB SWIZZLE_128B atom
@@ -255,12 +211,5 @@ cudaError_t tc_pass_launch(const TcPassArgs& a, int cs, int hd, int qpk, int kv_
                            cudaStream_t st);
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
-bool umma_shape_ok(int R, int K);
-int umma_encode_map(void* map, const void* base, int rows, int K, int box_rows);
-size_t umma_map_bytes();
-int umma_tile_rows();
-int umma_n();
-cudaError_t umma_set_attrs();
-cudaError_t umma_launch(const UmmaArgs& a, int grid, cudaStream_t st);
 
 }  // namespace ppsd

@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -22,8 +21,6 @@ import numpy as np
 from . import _lib
 
 LAYOUT_TC_TILED = 16  # include/ppsd.h PPSD_LAYOUT_TC_TILED
-# PPSD_GEMV=cc: row-major weights for the CUDA-core GEMV (A/B experiments only)
-TC_TILED = not os.environ.get("PPSD_GEMV", "tc").startswith("c")
 INIT_SALT = 0x5EED_B200_C0FF_EE01  # keep in sync with csrc/engine.cu ppsd_init_weight
 TID_EMBED, TID_LM_HEAD = 0xE0, 0xE1
 TID_WQ, TID_WK, TID_WV, TID_WO, TID_WGATE, TID_WUP, TID_WDOWN = 1, 2, 3, 4, 5, 6, 7
@@ -202,7 +199,6 @@ class TransformerLM:
                 # rows and stays plain. pool: the layers' matrices of one kind are
                 # slices of one allocation, so they sit at a fixed stride (the GEMV
                 # computes their address instead of loading it)
-                tiled = tiled and TC_TILED
                 n = C.c_int64(0)
                 _lib.check(L.ppsd_weight_elems(int(tiled), rows, cols, C.byref(n)), "weight_elems")
                 if pool is not None:
