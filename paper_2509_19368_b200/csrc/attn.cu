@@ -24,12 +24,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
 }
 
 namespace {
+int g_attn_occ = 0;  // attn_set_attrs: resident CTAs per SM of the configured instantiation
+
 template <int HD, typename KVT, int QPK>
 cudaError_t launch_k(const AttnArgs& a, int grid, cudaStream_t st, bool attrs) {
   const size_t smem = 2 * (size_t)kPage * HD * sizeof(KVT);
-  if (attrs)
-    return cudaFuncSetAttribute(attn_kernel<HD, KVT, QPK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+  if (attrs) {
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<HD, KVT, QPK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_attn_occ, attn_kernel<HD, KVT, QPK>, kAttnThreads, smem);
+    return e;
+  }
   return launch_pdl(attn_kernel<HD, KVT, QPK>, dim3(grid), dim3(kAttnThreads), smem, st, a);
 }
 template <int HD, typename KVT>
@@ -63,6 +69,10 @@ bool attn_supported(int hd, int qpk) {
 }
 
 cudaError_t attn_set_attrs(const AttnArgs& a) { return dispatch(a, 0, 0, true); }
+
+// CTAs per SM that are resident at once (after attn_set_attrs): the grid is
+// sized to one wave, a second wave of item-less CTAs costs ~2 us
+int attn_ctas_per_sm() { return g_attn_occ; }
 
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) { return dispatch(a, grid, st, false); }
 

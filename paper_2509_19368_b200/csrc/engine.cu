@@ -67,7 +67,7 @@ struct ppsd_engine {
   ppsd_model_desc md{};
   ppsd_pipeline_desc pd{};
   int device = 0, num_sms = 148;
-  bool tc = true;  // tensor-core GEMV (weights TC-tiled)
+  int attn_per_sm = 8;  // attention CTAs per SM: one resident wave
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
   bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
   int hint_first = -1;       // capturing single-problem launches whose first layer is known (speculative start)
@@ -162,7 +162,7 @@ extern "C" const char* ppsd_build_info(void) {
          "split-K paged attention, device tick machine";
 }
 
-static int attn_grid(const ppsd_engine* e) { return 8 * e->num_sms; }
+static int attn_grid(const ppsd_engine* e) { return e->attn_per_sm * e->num_sms; }
 
 // first failed launch inside a graph capture (the capture itself only
 // reports "invalidated")
@@ -760,6 +760,7 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       AttnArgs aa{};
       aa.dm = d;
       CU(attn_set_attrs(aa));
+      e->attn_per_sm = std::max(1, std::min(8, attn_ctas_per_sm()));
     }
     e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
     e->final_norm = w->final_norm;
