@@ -14,6 +14,7 @@ constexpr int kTcThreads = 320;
 constexpr int kTcAccCols = 64;                   // one accumulator (N <= 48 columns used)
 constexpr int kTcTmemCols = 2 * kTcAccCols;      // double-buffered: 128
 constexpr int kTcMaxProb = 32;
+constexpr int kTcVecPerBlk = 5;  // vectors whose three parts fit one 16-column B block
 
 // kind::f16 instruction descriptor: bf16 x bf16 -> fp32, A and B K-major,
 // M = 128 (bits 24-28: M >> 4); N (bits 17-22: N >> 3) per launch

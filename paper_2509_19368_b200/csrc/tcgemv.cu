@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
       // the vectors' K slice (x, times the RMSNorm weight for QKV / gate-up /
       // heads; the 1/rms scale is applied in the epilogue) split exactly into
       // hi / mid / lo bf16 at rows 3v, 3v+1, 3v+2 of the swizzled operand
-      const int bw = warp - 2;
+      const int bw = warp - 2, bt = tid - 64;
       const int nbw = NS < 4 ? NS : 4;
       pdl_wait();
       pdl_trigger();
@@ -405,22 +405,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           }
           __syncwarp();
         }
+        // > 8 vectors (prefill chunks, EESD verify): the four warps build
+        // every stage together (one round of loads per stage); else stage n
+        // belongs to builder warp n % nbw (stages in flight hide the load
+        // latency); nbw <= NS keeps every warp within one ring lap (an
+        // mbarrier parity wait cannot tell phases two laps apart)
+        const bool coop = nvp > 8;
+        const int tstride = coop ? 128 : 32, tlane = coop ? bt : lane;
         for (int j = jlo; j < jhi; j += NB, ++n) {
-          // stage n belongs to builder warp n % nbw; nbw <= NS keeps every
-          // warp within one ring lap (an mbarrier parity wait cannot tell
-          // phases two laps apart)
-          if (n % nbw != bw) continue;
+          if (!coop && n % nbw != bw) continue;
           const int nbj = min(NB, jhi - j);
           const int st = n % NS;
           if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
           const uint32_t ba = ring_b + (uint32_t)st * b_stage;
           const int per_v = nbj * JS * 8;  // 16-byte K chunks of one vector in this stage
           const int items = nvp * per_v;
-          for (int i0 = 0; i0 < ((g_tc_exp & 2) ? 0 : items); i0 += 4 * 32) {
+          for (int i0 = 0; i0 < ((g_tc_exp & 2) ? 0 : items); i0 += 4 * tstride) {
             float xv[4][8];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {  // all loads of up to 4 items first
-              const int it = i0 + u * 32 + lane;
+              const int it = i0 + u * tstride + tlane;
               const int v = it / per_v, rem = it - v * per_v;
               const int k0 = (j * JS * 64) + rem * 8;  // rem = (jj * JS + s) * 8 + c
               const float* sp = it < items ? srcv[v] : nullptr;
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int it = i0 + u * 32 + lane;
+              const int it = i0 + u * tstride + tlane;
               if (it >= items) break;
               const int v = it / per_v, rem = it - v * per_v;
               const int js_ = rem >> 3, c = rem & 7;  // (jj * JS + s), chunk
@@ -469,10 +473,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
             }
           }
           fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tc_trace(3, n);
-            mbar_arrive(&full[st]);
+          if (coop) {
+            named_bar_sync(2, 128);
+            if (bt == 0) mbar_arrive(&full[st]);
+          } else {
+            __syncwarp();
+            if (lane == 0) {
+              tc_trace(3, n);
+              mbar_arrive(&full[st]);
+            }
           }
         }
       }
