@@ -5,9 +5,10 @@ The multi-rank engines of a world-W pipeline run as W engines on cuda:0
 layers + heads + box pack) is timed with CUDA events on its own stream, and
 so is the replicated scheduler step. On W GPUs the ranks run concurrently, so
 a tick costs max over ranks (compute + scheduler) plus one box exchange.
-Exchange latency is NOT measured here (one GPU); it is an input (--xfer-us,
-default 8 us: an NVLink peer store of the box plus a system-scope flag round
-trip). Output is a projection, not a bench number:
+The exchange is an input (--xfer-us, default 13.3 us: the device-side cost of
+the peer-store exchange per tick measured on one GPU by tools/p2p_overhead.py;
+the NVLink latency between two GPUs comes on top). Output is a projection, not
+a bench number:
 
     python tools/project_multigpu.py --model 13b --exit 20 --world 2
     python tools/project_multigpu.py --model 70b --exit 10 --world 4 --tokens 128
@@ -32,7 +33,7 @@ def main():
     ap.add_argument("--deep-scale", type=float, default=0.1)
     ap.add_argument("--tokens", type=int, default=256)
     ap.add_argument("--prompt", type=int, default=128)
-    ap.add_argument("--xfer-us", type=float, default=8.0)
+    ap.add_argument("--xfer-us", type=float, default=13.3)  # tools/p2p_overhead.py: loopback peer-store exchange, 7B
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
