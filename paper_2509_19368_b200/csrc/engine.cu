@@ -11,6 +11,7 @@
 #include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <map>
@@ -161,6 +162,21 @@ extern "C" const char* ppsd_build_info(void) {
   return "libppsd sm_100a: tcgen05 weight-streaming GEMV (TMEM accumulators, bulk-copy ring, cluster split-K), "
          "split-K paged attention, device tick machine";
 }
+
+// NVTX ranges (header-only nvtx3: free unless a profiler is attached):
+// ppsd.prefill / ppsd.decode / ppsd.ticks (one per launched batch of tick
+// graphs, named with the tick range) / ppsd.ar / ppsd.eesd / ppsd.p2p
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, long long a, long long b) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), "%s %lld..%lld", what, a, b);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 static int attn_grid(const ppsd_engine* e) { return e->attn_per_sm * e->num_sms; }
 
@@ -1029,6 +1045,7 @@ static int prefill(ppsd_engine* e, int n_prompt, double* ms, int64_t* launches) 
   CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
   CU(cudaEventRecord(e->ev0, e->st));
   const int chunks = (n_prompt - 1 + e->h_ctx.prefill_chunk - 1) / e->h_ctx.prefill_chunk;
+  NvtxRange nv("ppsd.prefill chunks", 0, chunks);
   for (int i = 0; i < chunks; ++i) CU(cudaGraphLaunch(e->g_prefill, e->st));
   CU(cudaEventRecord(e->ev1, e->st));
   CU(cudaEventSynchronize(e->ev1));
@@ -1112,9 +1129,13 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   // small readback: committed .. error (8 int32 after SchedCfg)
   const size_t off = offsetof(Sched, t);
   const size_t len = offsetof(Sched, verify_counter) - off;
+  NvtxRange nv_decode("ppsd.decode");
   for (;;) {
     const int64_t n = std::max<int64_t>(1, (int64_t)stop - committed);
-    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(tick, e->st));
+    {
+      NvtxRange nv("ppsd.ticks", ticks_launched + 1, ticks_launched + n);
+      for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(tick, e->st));
+    }
     ticks_launched += n;
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
                        cudaMemcpyDeviceToHost, e->st));
@@ -1312,6 +1333,7 @@ extern "C" int ppsd_decode_ar(ppsd_engine* e, int32_t greedy, uint64_t rng_seed,
     ArCtl ctl{n_prompt - 1, e->first_local_layer, e->n_local_layers, n_prompt - 1};
     CU(cudaMemcpyAsync(e->d_arctl, &ctl, sizeof(ctl), cudaMemcpyHostToDevice, e->st));
     CU(cudaEventRecord(e->ev0, e->st));
+    NvtxRange nv("ppsd.ar tokens", 1, max_tokens);
     for (int i = 0; i < max_tokens; ++i) CU(cudaGraphLaunch(e->g_ar, e->st));
     CU(cudaEventRecord(e->ev1, e->st));
     launches += (int64_t)max_tokens * e->ar_launches;
@@ -1435,6 +1457,7 @@ static int run_eesd(ppsd_engine* e, int model, int gamma, const int32_t* prompt,
   int64_t rounds = 0;
   for (;;) {
     const int64_t n = std::max<int64_t>(1, (horizon - st.committed + gamma) / (gamma + 1));
+    NvtxRange nv("ppsd.eesd rounds", 1, n);
     for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(g, e->st));
     rounds += n;
     CU(cudaMemcpyAsync(&st, e->d_eesd, sizeof(EesdState), cudaMemcpyDeviceToHost, e->st));
@@ -2124,6 +2147,7 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   const size_t len = offsetof(Sched, verify_counter) - off;
   for (;;) {  // replicated state: every rank launches the same number of ticks
     const int64_t n = std::max<int64_t>(1, (int64_t)max_tokens - s.committed);
+    NvtxRange nv("ppsd.p2p ticks", 1, n);
     for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(e->g_p2p_tick, e->st));
     ticks_launched += n;
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
