@@ -234,9 +234,9 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
     const TcPlan& t = p.tc;
     // speculative start: measured slower on the 7B bench (427 vs 437 tok/s,
     // DESIGN.md §8), opt-in PPSD_TC_HINT=1
-    static const bool hints = getenv("PPSD_TC_HINT") && getenv("PPSD_TC_HINT")[0] == '1';
-    if (hints && (mat == kMatHead || mat == kMatHeadV)) a.hint_li = 0;  // one problem at most, the LM head
-    else if (hints && e->hint_first >= 0) a.hint_li = e->hint_first + layer_i;
+    static const int hints = getenv("PPSD_TC_HINT") ? atoi(getenv("PPSD_TC_HINT")) : 0;
+    if ((hints & 1) && (mat == kMatHead || mat == kMatHeadV)) a.hint_li = 0;  // one problem at most, the LM head
+    else if ((hints & 2) && e->hint_first >= 0 && ((hints & 4) || a.desc_early)) a.hint_li = e->hint_first + layer_i;
     if (mat == kMatHead || mat == kMatHeadV) {
       a.wp[0] = e->lm_head;
     } else {

@@ -249,15 +249,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           for (int j = jlo; j < jhi; j += NB, ++n) {
             const int nbj = min(NB, jhi - j);
             const int st = n % NS;
-            if (n < s_spec) continue;  // issued before the work descriptor was read
-            if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
-            if (g_tc_exp & 1) {
-              mbar_arrive(&full[st]);
-            } else {
-            mbar_expect_tx(&full[st], (uint32_t)nbj * tb);
-            for (int jj = 0; jj < nbj; ++jj)
-              bulk_g2s(smem + (size_t)st * w_stage + (size_t)jj * tb,
-                       w + ((size_t)(j + jj) * G + g0) * JSB, tb, &full[st], pol);
+            if (n >= s_spec) {  // (stages below s_spec were issued before the descriptor was read)
+              if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
+              if (g_tc_exp & 1) {
+                mbar_arrive(&full[st]);
+              } else {
+                mbar_expect_tx(&full[st], (uint32_t)nbj * tb);
+                for (int jj = 0; jj < nbj; ++jj)
+                  bulk_g2s(smem + (size_t)st * w_stage + (size_t)jj * tb,
+                           w + ((size_t)(j + jj) * G + g0) * JSB, tb, &full[st], pol);
+              }
             }
             // the ring is full: only now wait for the predecessor (and let the
             // successor launch; every thread of the CTA triggers after its wait)
