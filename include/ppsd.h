@@ -270,6 +270,10 @@ int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_prompt, int
 /* bf16 elements of a [rows][cols] matrix in the plain (tiled = 0) or the
  * TC-tiled (tiled = 1: K padded to a multiple of 64) layout */
 int ppsd_weight_elems(int32_t tiled, int64_t rows, int64_t cols, int64_t* elems);
+/* bf16 index of element (r, k) of a [rows][cols] matrix in the TC-tiled
+ * layout (k < cols padded to a multiple of 64; padding holds zeros) — for
+ * loaders that tile checkpoints on the host (paper_2509_19368_b200.tc_tile) */
+int ppsd_tc_offset(int64_t rows, int64_t cols, int64_t r, int64_t k, int64_t* off);
 int ppsd_init_weight(void* dst_bf16, int32_t layout, int64_t rows, int64_t cols,
                      uint64_t seed, const uint64_t* tids, const float* scales,
                      int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,

@@ -12,7 +12,7 @@ from .analytic import (SpeedupParams, eesd_speedup, expected_accept_len, n_stage
                        ppsd_over_eesd_lambda, ppsd_reference_speedup, ppsd_speedup)
 from .decode import (Engine, decode_autoregressive, decode_eesd, decode_ppsd, engine_for,
                      simulate_autoregressive, simulate_eesd, simulate_ppsd)
-from .models import ToyLM, TransformerConfig, TransformerLM
+from .models import ToyLM, TransformerConfig, TransformerLM, tc_tile
 from .pipeline import (ACTIVATION, CHECK_TOKEN, DRAFT_TOKEN, FINAL_TOKEN, TRACE_HEADER,
                        AcceptanceOracle, EventTrace, OracleMode, PipelineConfig, RunMetrics,
                        StageMessage, TraceRow, default_prompt, partition_stages, steady_state_view)
@@ -22,7 +22,7 @@ __all__ = [
     "ACTIVATION", "CHECK_TOKEN", "DRAFT_TOKEN", "FINAL_TOKEN", "TRACE_HEADER",
     "AcceptanceOracle", "Engine", "EventTrace", "OracleMode", "PipelineConfig", "RngStream",
     "RunMetrics", "SpeedupParams", "StageMessage", "ToyLM", "TraceRow", "TransformerConfig",
-    "TransformerLM", "decode_autoregressive", "decode_eesd", "decode_ppsd", "default_prompt", "derive_seed",
+    "TransformerLM", "tc_tile", "decode_autoregressive", "decode_eesd", "decode_ppsd", "default_prompt", "derive_seed",
     "eesd_speedup", "engine_for", "expected_accept_len", "mix64", "n_stages", "partition_stages",
     "ppsd_over_eesd_lambda", "ppsd_reference_speedup", "ppsd_speedup", "simulate_autoregressive",
     "simulate_eesd", "simulate_ppsd", "steady_state_view",

@@ -119,6 +119,7 @@ EXPORTS = {
     "ppsd_debug_matvec": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "ppsd_debug_tc_trace": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64)]),
+    "ppsd_tc_offset": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]),
     "ppsd_weight_elems": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]),
     "ppsd_init_weight": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_uint64,
                                    C.POINTER(C.c_uint64), C.POINTER(C.c_float), C.c_int32, C.c_int32,

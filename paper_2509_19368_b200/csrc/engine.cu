@@ -1548,6 +1548,16 @@ extern "C" int ppsd_weight_elems(int32_t tiled, int64_t rows, int64_t cols, int6
   return PPSD_OK;
 }
 
+extern "C" int ppsd_tc_offset(int64_t rows, int64_t cols, int64_t r, int64_t k, int64_t* off) {
+  if (rows <= 0 || cols <= 0 || rows % 8 || cols % 8 || r < 0 || r >= rows || k < 0 || !off)
+    return fail(PPSD_EINVAL, "bad TC-tiled coordinates");
+  int js, kp;
+  tc_layout((int)rows, (int)cols, &js, &kp);
+  if (k >= kp) return fail(PPSD_EINVAL, "bad TC-tiled coordinates");
+  *off = tc_offset((int)rows, (int)cols, r, k);
+  return PPSD_OK;
+}
+
 extern "C" int ppsd_init_weight(void* dst, int32_t layout, int64_t rows, int64_t cols, uint64_t seed,
                                 const uint64_t* tids, const float* scales, int32_t n_heads, int32_t n_kv_heads,
                                 int32_t head_dim, void* cuda_stream) {

@@ -152,6 +152,33 @@ def rope_tables(head_dim: int, theta: float, n_pos: int):
     return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
 
 
+def tc_layout(rows: int, cols: int) -> tuple[int, int]:
+    """(JS, KP) of the TC-tiled layout of a [rows][cols] matrix (csrc/kernels.cuh tc_layout)."""
+    kp = (cols + 63) // 64 * 64
+    nsl = kp // 64
+    js = 4 if nsl % 4 == 0 else 2 if nsl % 2 == 0 else 1
+    return js, kp
+
+
+def tc_tile(w: np.ndarray) -> np.ndarray:
+    """A row-major [rows][cols] matrix in the TC-tiled layout the tensor-core
+    GEMV streams: flat, cols padded with zeros to a multiple of
+    64, element (r, k) at csrc/kernels.cuh tc_offset. For loading checkpoints;
+    the random-init weights are written tiled on the GPU (ppsd_init_weight)."""
+    rows, cols = w.shape
+    if rows % 8 or cols % 8:
+        raise ValueError("TC-tiled matrices need rows and cols multiples of 8")
+    js, kp = tc_layout(rows, cols)
+    g = rows // 8
+    out = np.zeros(rows * kp, dtype=w.dtype)
+    r = np.arange(rows)[:, None]
+    k = np.arange(cols)[None, :]
+    slab, rr, c, e = k // 64, r % 8, (k % 64) // 8, k % 8
+    off = (((((slab // js) * g + r // 8) * js + slab % js) * 8 + rr) * 64) + ((c ^ rr) * 8) + e
+    out[off.ravel()] = w.ravel()
+    return out
+
+
 class TransformerLM:
     """Random-init Llama-shaped decoder resident on one GPU.
 

@@ -92,3 +92,36 @@ def test_host_api_mirrors_reference():
     assert abs(ppsd.ppsd_speedup(0.3226, 32, 8) - 1.319) <= 0.005
     m = ppsd.simulate_autoregressive(ppsd.PipelineConfig(40, 16), 10)
     assert m.ticks == 30
+
+
+def test_tc_tiled_layout_python_matches_library():
+    """paper_2509_19368_b200.tc_tile (the host-side checkpoint tiler) places
+    every element where the library's ppsd_tc_offset (csrc/kernels.cuh, the
+    layout the tensor-core GEMV and the device initialiser use) says, the
+    padding is zero, and the layout is a bijection onto rows x padded cols."""
+    import numpy as np
+    import paper_2509_19368_b200 as ppsd
+    from paper_2509_19368_b200 import _lib
+
+    L = _lib.load_library()
+    rng = np.random.default_rng(0)
+    for rows, cols in ((8, 64), (24, 176), (352, 64), (64, 1024), (16, 11008 // 8 * 8), (40, 13824)):
+        w = rng.standard_normal((rows, cols)).astype(np.float32)
+        t = ppsd.tc_tile(w)
+        n = C.c_int64()
+        assert L.ppsd_weight_elems(1, rows, cols, C.byref(n)) == 0 and n.value == t.size
+        # bijection: every logical element lands on its own slot, the rest is padding
+        idx = np.zeros(t.size, dtype=np.int64)
+        off = C.c_int64()
+        for r in rng.integers(0, rows, size=12):
+            for k in rng.integers(0, cols, size=12):
+                assert L.ppsd_tc_offset(rows, cols, int(r), int(k), C.byref(off)) == 0
+                assert t[off.value] == w[r, k]
+        js, kp = ppsd.models.tc_layout(rows, cols)
+        for r in range(0, rows, max(1, rows // 8)):
+            for k in range(0, kp, 8):
+                assert L.ppsd_tc_offset(rows, cols, r, k, C.byref(off)) == 0
+                idx[off.value] += 1
+        assert idx.max() <= 1
+        # the tiled array holds exactly the matrix's elements plus zero padding
+        assert np.array_equal(np.sort(t[t != 0]), np.sort(w[w != 0].ravel()))

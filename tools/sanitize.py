@@ -1,7 +1,7 @@
 """Small decodes for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): the tiny transformer (PPSD folded + pipelined, AR, EESD) and a
-2-layer Llama-2-7B-shaped model (PPSD folded, AR, EESD, K-split down
-projection, tcgen05 prefill), greedy.
+2-layer Llama-2-7B-shaped model (PPSD folded, AR, EESD; tcgen05 GEMVs with
+4-CTA split-K clusters for O / down, batched prefill), greedy.
 
     compute-sanitizer --tool racecheck python tools/sanitize.py
 """
