@@ -74,6 +74,11 @@ cudaError_t attn_set_attrs(const AttnArgs& a) { return dispatch(a, 0, 0, true); 
 // sized to one wave, a second wave of item-less CTAs costs ~2 us
 int attn_ctas_per_sm() { return g_attn_occ; }
 
+int attn_trace_enable(int on) { return cudaMemcpyToSymbol(g_attn_tr_on, &on, sizeof(int)) == cudaSuccess ? 0 : -1; }
+int attn_trace_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_attn_tr, sizeof(g_attn_tr)) == cudaSuccess ? 0 : -1;
+}
+
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) { return dispatch(a, grid, st, false); }
 
 }  // namespace ppsd

@@ -41,6 +41,22 @@ __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(
 constexpr int kAttnThreads = 128;  // one attention worker
 constexpr int kMergePages = 32;    // contexts up to 2048 positions merge from smem
 
+// Timeline of each worker's first item (debugging: compiled in only with
+// -DPPSD_ATTN_TRACE, enabled by ppsd_debug_tc_trace(5), read with -4):
+// [worker][event] %globaltimer ns. Events: 0 start, 1 descriptor staged,
+// 2 inputs visible, 3 q staged, 4 K/V landed, 5 scores, 6 softmax, 7 partial
+// stored, 8 ticket taken, 9 merged (last worker), 10 item done
+constexpr int kAttnTraceW = 1024;
+static __device__ unsigned long long g_attn_tr[kAttnTraceW][12];
+static __device__ int g_attn_tr_on;
+__device__ __forceinline__ void attn_mark(int worker, int first, int tid, int ev) {
+#ifdef PPSD_ATTN_TRACE
+  if (g_attn_tr_on && first && tid == 0 && worker < kAttnTraceW) g_attn_tr[worker][ev] = globaltimer();
+#else
+  (void)worker; (void)first; (void)tid; (void)ev;
+#endif
+}
+
 constexpr int kStageG = 32;      // groups staged in shared memory (more: read from global)
 constexpr int kStagePages = 64;  // page-table entries staged
 
@@ -50,6 +66,7 @@ struct AttnScratch {
   float qs[QPK][HD];
   float sc[QPK][kPage];
   float s_m[QPK], s_l[QPK];
+  float s_lw[QPK][4];  // per-warp softmax sums (QPK < 4)
   float s_pm[QPK][kMergePages], s_pl[QPK][kMergePages];
   int s_last;
   uint64_t bar;
@@ -77,16 +94,36 @@ template <int HD, typename KVT, int QPK, class Sync, class Wait>
 __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid, KVT* ks,
                            AttnScratch<HD, QPK>& S, uint32_t& phase, Sync sync, Wait wait_inputs) {
   constexpr int EPV = 16 / (int)sizeof(KVT);  // elements per 16-byte vector
-  constexpr int LPT = HD / EPV;                // lanes per token
+  constexpr int CPR = HD / EPV;                // 16-byte chunks per K / V row
+  static_assert(CPR >= 1 && CPR <= 32 && (32 % CPR) == 0, "head_dim / dtype combination");
+  // scores: LPT lanes per token, CPL chunks per lane; as few lanes as keep
+  // the lane's q slice within 32 registers (fewer butterfly shuffles)
+  constexpr int LPT0 = (HD * QPK + 31) / 32;
+  constexpr int LPT1 = LPT0 <= 1 ? 1 : LPT0 <= 2 ? 2 : LPT0 <= 4 ? 4 : LPT0 <= 8 ? 8 : LPT0 <= 16 ? 16 : 32;
+  constexpr int LPT = LPT1 < CPR ? LPT1 : CPR;
+  constexpr int CPL = CPR / LPT;
   constexpr int TPW = 32 / LPT;                // tokens per warp pass
   constexpr int BLK = kPage * HD;              // elements per K (or V) page block
-  static_assert(LPT >= 1 && LPT <= 32 && (32 % LPT) == 0, "head_dim / dtype combination");
+  constexpr int NIT = (kPage + 4 * TPW - 1) / (4 * TPW);  // score passes per warp
+  constexpr int UC0 = 32 / (QPK * CPL) < 1 ? 1 : 32 / (QPK * CPL);  // unrolled tokens per chunk
+  constexpr int UC = NIT < UC0 ? NIT : UC0;
+  static_assert(NIT % UC == 0, "score chunking");
+  // PV: a thread accumulates one 16-byte V chunk (EPV dims) of one head over
+  // every TS-th token; the TS token splits are added in order through the K
+  // block (free once the scores are taken)
+  constexpr int NGRP = QPK * CPR;                             // (head, chunk) groups
+  constexpr int GT = NGRP < kAttnThreads ? NGRP : kAttnThreads;  // threads per split
+  constexpr int TS0 = kAttnThreads / GT;
+  constexpr int TSC0 = 16 * (int)sizeof(KVT) / QPK;            // splits that fit the K block
+  constexpr int TSC = TSC0 < 1 ? 1 : TSC0;
+  constexpr int TS = TS0 < TSC ? TS0 : TSC;
   KVT* vs = ks + BLK;
   const Work* w = a.work;
   const int warp = tid >> 5, lane = tid & 31;
   const int H = a.dm.H, KVh = a.dm.KV;
   const float scale = 1.0f / sqrtf((float)HD);
 
+  attn_mark(worker, 1, tid, 0);
   // stage the descriptor + page table: independent loads, one round trip
   if (tid < kStageG) {
     S.st_slot[tid] = w->slot[tid];
@@ -98,6 +135,7 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
   if (tid == 0) S.st_G = w->G;
   for (int i = tid; i < min(a.max_pages, kStagePages); i += kAttnThreads) S.st_page[i] = a.page_table[i];
   sync();
+  attn_mark(worker, 1, tid, 1);
   const int G = S.st_G;
   const bool staged = G <= kStageG;
   auto wslot = [&](int g) { return staged ? S.st_slot[g] : w->slot[g]; };
@@ -158,6 +196,7 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
   const int early = have ? max(0, min(page_rows(it), wpos(it.g) - it.c * kPage)) : 0;
   if (early > 0 && tid == 0) issue_rows(it, 0, early, false);
   wait_inputs();
+  attn_mark(worker, 1, tid, 2);
 
   for (int item = worker, first = 1; have; item += nworkers, have = decode(item, it), first = 0) {
     const int g = it.g, vv = it.vv, kvh = it.kvh, c = it.c, nch = it.nch;
@@ -167,69 +206,175 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
     const float* qsrc = a.q + (size_t)slot * H * HD + (size_t)kvh * QPK * HD;
     for (int i = tid; i < QPK * HD; i += kAttnThreads) S.qs[i / HD][i % HD] = qsrc[i];
     sync();
+    attn_mark(worker, first, tid, 3);
     mbar_wait(&S.bar, phase);
     phase ^= 1;
+    attn_mark(worker, first, tid, 4);
 
-    // scores: LPT lanes per token, one 16-byte K vector per lane
-    const int li = lane % LPT, tw = lane / LPT;
-    for (int base = warp * TPW; base < n; base += 4 * TPW) {
-      const int tt = base + tw;
-      float part[QPK];
+    // scores: LPT lanes per token, one 16-byte K vector per lane; the
+    // lane's q slice sits in registers and a warp's tokens are unrolled in
+    // chunks of UC (independent chains: the K loads of a chunk are in flight
+    // together instead of one shared-memory round trip per token)
+    {
+      const int li = lane % LPT, tw = lane / LPT;
+      // lane (li, tw) reads its chunks in the rotated order (s + f) % CPL,
+      // f from the lane's place j in its 8-lane shared-memory wavefront: the
+      // 8 lanes hit 8 distinct 16-byte bank groups; its q slice is loaded
+      // once in the same order
+      const int jq = lane & 7, f = CPL >= 8 ? jq : jq / (8 / (CPL < 8 ? CPL : 8));
+      float qr[QPK][CPL][EPV];
 #pragma unroll
-      for (int i = 0; i < QPK; ++i) part[i] = 0.f;
-      if (tt < n) {
-        float kf[EPV];
-        unpack16<KVT>(lds128(ks + (size_t)tt * HD + li * EPV), kf);
+      for (int i = 0; i < QPK; ++i)
 #pragma unroll
-        for (int i = 0; i < QPK; ++i)
+        for (int sc = 0; sc < CPL; ++sc) {
+          const int ch = li * CPL + (sc + f) % CPL;
 #pragma unroll
-          for (int e = 0; e < EPV; ++e) part[i] = fmaf(kf[e], S.qs[i][li * EPV + e], part[i]);
+          for (int e = 0; e < EPV; ++e) qr[i][sc][e] = S.qs[i][ch * EPV + e];
+        }
+#pragma unroll
+      for (int c0 = 0; c0 < NIT; c0 += UC) {
+        uint4 kv[UC][CPL];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          const int tt = (warp + 4 * (c0 + u)) * TPW + tw;
+#pragma unroll
+          for (int sc = 0; sc < CPL; ++sc) {
+            const int ch = li * CPL + (sc + f) % CPL;
+            kv[u][sc] = tt < n ? lds128(ks + (size_t)tt * HD + ch * EPV) : make_uint4(0, 0, 0, 0);
+          }
+        }
+        float part[UC][QPK];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+#pragma unroll
+          for (int i = 0; i < QPK; ++i) part[u][i] = 0.f;
+#pragma unroll
+          for (int sc = 0; sc < CPL; ++sc) {
+            float kf[EPV];
+            unpack16<KVT>(kv[u][sc], kf);
+#pragma unroll
+            for (int i = 0; i < QPK; ++i)
+#pragma unroll
+              for (int e = 0; e < EPV; ++e) part[u][i] = fmaf(kf[e], qr[i][sc][e], part[u][i]);
+          }
+        }
+#pragma unroll
+        for (int off = LPT / 2; off > 0; off >>= 1)
+#pragma unroll
+          for (int u = 0; u < UC; ++u)
+#pragma unroll
+            for (int i = 0; i < QPK; ++i) part[u][i] += __shfl_xor_sync(0xffffffffu, part[u][i], off);
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+          const int tt = (warp + 4 * (c0 + u)) * TPW + tw;
+          if (li == 0 && tt < n)
+#pragma unroll
+            for (int i = 0; i < QPK; ++i) S.sc[i][tt] = part[u][i] * scale;
+        }
       }
-#pragma unroll
-      for (int off = LPT / 2; off > 0; off >>= 1)
-#pragma unroll
-        for (int i = 0; i < QPK; ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], off);
-      if (li == 0 && tt < n)
-#pragma unroll
-        for (int i = 0; i < QPK; ++i) S.sc[i][tt] = part[i] * scale;
     }
     sync();
+    attn_mark(worker, first, tid, 5);
 
-    for (int i = warp; i < QPK; i += 4) {  // chunk-local softmax statistics
-      float mx = -FLT_MAX;
-      for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, S.sc[i][tt]);
-      mx = warp_max(mx);
-      float l = 0.f;
-      for (int tt = lane; tt < n; tt += 32) {
-        const float p = expf(S.sc[i][tt] - mx);
-        S.sc[i][tt] = p;
-        l += p;
+    // chunk-local softmax statistics
+    if constexpr (QPK >= 4) {  // one warp per head
+      for (int i = warp; i < QPK; i += 4) {
+        float mx = -FLT_MAX;
+        for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, S.sc[i][tt]);
+        mx = warp_max(mx);
+        float l = 0.f;
+        for (int tt = lane; tt < n; tt += 32) {
+          const float p = expf(S.sc[i][tt] - mx);
+          S.sc[i][tt] = p;
+          l += p;
+        }
+        l = warp_sum(l);
+        if (lane == 0) { S.s_m[i] = mx; S.s_l[i] = l; }
       }
-      l = warp_sum(l);
-      if (lane == 0) { S.s_m[i] = mx; S.s_l[i] = l; }
+    } else {  // every warp takes the max, then exponentiates its 16 tokens
+      static_assert(kPage == 64, "16 tokens per warp");
+#pragma unroll
+      for (int i = 0; i < QPK; ++i) {
+        float mx = -FLT_MAX;
+        for (int tt = lane; tt < n; tt += 32) mx = fmaxf(mx, S.sc[i][tt]);
+        mx = warp_max(mx);
+        const int tt = warp * 16 + (lane & 15);
+        float p = 0.f;
+        if (lane < 16 && tt < n) {
+          p = expf(S.sc[i][tt] - mx);
+          S.sc[i][tt] = p;
+        }
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (lane == 0) {
+          S.s_lw[i][warp] = p;
+          if (warp == 0) S.s_m[i] = mx;
+        }
+      }
     }
     sync();
+    if constexpr (QPK < 4) {
+      if (tid < QPK) S.s_l[tid] = (S.s_lw[tid][0] + S.s_lw[tid][1]) + (S.s_lw[tid][2] + S.s_lw[tid][3]);
+    }
+    attn_mark(worker, first, tid, 6);
 
     float* pbase = a.part + (((size_t)slot * H + (size_t)kvh * QPK) * a.max_pages) * (HD + 2);
-    for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
-      const int i = idx / HD, d = idx - i * HD;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int tt = 0; tt < n; ++tt) acc = fmaf(S.sc[i][tt], tof(vs[(size_t)tt * HD + d]), acc);
-      pbase[((size_t)i * a.max_pages + c) * (HD + 2) + d] = acc;
+    // PV: thread -> (token split ts, group gi); group -> (head i, V chunk ch)
+    if (tid < TS * GT) {
+      const int ts = tid / GT;
+      float* pvs = reinterpret_cast<float*>(ks);  // [TS][QPK * HD]
+      for (int gi = tid % GT; gi < NGRP; gi += GT) {
+        const int i = gi / CPR, ch = gi - i * CPR;
+        float acc[EPV];
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) acc[e] = 0.f;
+        const KVT* vrow = vs + ch * EPV;
+#pragma unroll 4
+        for (int tt = ts; tt < n; tt += TS) {
+          float vf[EPV];
+          unpack16<KVT>(lds128(vrow + (size_t)tt * HD), vf);
+          const float pp = S.sc[i][tt];
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) acc[e] = fmaf(pp, vf[e], acc[e]);
+        }
+        if constexpr (TS == 1) {
+          float* dst = pbase + ((size_t)i * a.max_pages + c) * (HD + 2) + ch * EPV;
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) dst[e] = acc[e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) pvs[ts * QPK * HD + gi * EPV + e] = acc[e];
+        }
+      }
+    }
+    if constexpr (TS > 1) {
+      // the splits go through the K block with generic stores; the next
+      // item's bulk copy rewrites it through the async proxy: every writer
+      // orders its stores before that (CUTLASS's TMA-store fence pattern)
+      fence_proxy_async_smem();
+      sync();
+      const float* pvs = reinterpret_cast<const float*>(ks);
+      for (int idx = tid; idx < QPK * HD; idx += kAttnThreads) {
+        float acc = pvs[idx];
+#pragma unroll
+        for (int t2 = 1; t2 < TS; ++t2) acc += pvs[t2 * QPK * HD + idx];
+        const int i = idx / HD, d = idx - i * HD;
+        pbase[((size_t)i * a.max_pages + c) * (HD + 2) + d] = acc;
+      }
     }
     if (tid < QPK) {
       pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD] = S.s_m[tid];
       pbase[((size_t)tid * a.max_pages + c) * (HD + 2) + HD + 1] = S.s_l[tid];
     }
     sync();
-    if (tid == 0) {
-      __threadfence();
-      S.s_last = atomicAdd(&a.cnt[slot * KVh + kvh], 1) == nch - 1;
-    }
+    attn_mark(worker, first, tid, 7);
+    // arrival ticket: one acq_rel atomic (release: the CTA's partial stores,
+    // ordered before it by the barrier; acquire: the other pages' partials
+    // for the merge, made visible to the CTA by the barrier below)
+    if (tid == 0) S.s_last = atom_add_acqrel_gpu(&a.cnt[slot * KVh + kvh], 1) == (uint32_t)(nch - 1);
     sync();
+    attn_mark(worker, first, tid, 8);
     if (S.s_last) {  // ordered merge of the page partials (page statistics staged in smem)
-      __threadfence();
       if (nch <= kMergePages) {
         // one (head, dim) per thread: its page partials are loaded before the
         // page statistics are reduced (one L2 round trip for the merge)
@@ -299,8 +444,10 @@ __device__ void attn_items(const AttnArgs& a, int worker, int nworkers, int tid,
         }
       }
       if (tid == 0) a.cnt[slot * KVh + kvh] = 0;
+      attn_mark(worker, first, tid, 9);
     }
     sync();
+    attn_mark(worker, first, tid, 10);
   }
 }
 

@@ -117,6 +117,12 @@ __device__ __forceinline__ uint4 lds128s(uint32_t addr) {
                : "r"(addr));
   return v;
 }
+// global atomic add with acquire-release semantics at GPU scope (arrival tickets)
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(int32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 // shared-memory atomic add with acquire-release semantics at CTA scope
 __device__ __forceinline__ uint32_t atom_add_acqrel_cta(uint32_t* p, uint32_t v) {
   uint32_t old;

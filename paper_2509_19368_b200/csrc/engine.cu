@@ -1682,7 +1682,11 @@ int tc_pass_trace_read(unsigned long long* out);  // [8][128]
 // tensor-core GEMV pipeline timeline of CTA 0 (debugging): on = 1 records the
 // next launches, out = [8][128] %globaltimer ns of the last one
 extern "C" int ppsd_debug_tc_trace(int32_t on, uint64_t* out) {
-  // on / out & 2 (bit 1 of on >= 2): the layer pass's trace instead of the GEMV's
+  // on / out & 2 (bit 1 of on >= 2): the layer pass's trace instead of the GEMV's;
+  // on 4 / 5: attention trace off / on, on -4: read it (uint64 [1024][12])
+  if (on == 4 || on == 5) return attn_trace_enable(on & 1) ? fail(PPSD_ECUDA, "trace enable") : PPSD_OK;
+  if (on == -4) return out && !attn_trace_read(reinterpret_cast<unsigned long long*>(out)) ? PPSD_OK
+                                                                                      : fail(PPSD_ECUDA, "trace read");
   const bool pass = on >= 2 || (on < 0 && out && (on & 2));
   if (on >= 0 && (pass ? tc_pass_trace_enable(on & 1) : tc_trace_enable(on))) return fail(PPSD_ECUDA, "trace enable");
   if (out && (on == -2 ? tc_pass_trace_read(reinterpret_cast<unsigned long long*>(out))
