@@ -20,6 +20,11 @@ MODEL_BERNOULLI, MODEL_TOYLM, MODEL_TRANSFORMER = 0, 1, 2
 SCHEDULES = {"auto": 0, "pipelined": 1, "folded": 2}
 
 
+def schedule_name(code: int) -> str:
+    """The schedule a decode ran (ppsd_metrics.schedule)."""
+    return {v: k for k, v in SCHEDULES.items()}.get(code, "pipelined")
+
+
 class ModelDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int32), ("n_layers", C.c_int32), ("vocab", C.c_int32),

@@ -144,6 +144,13 @@ struct ppsd_engine {
   int p2p_world = 0;
   cudaGraphExec_t g_p2p_tick = nullptr;
   int64_t p2p_tick_launches = 0;
+  // rank fold (sched.h: sched_rfold_plan), greedy multi-rank: one graph per
+  // tick = [IF setter, eager stages, exit head, IF(batch){gather, deferred
+  // layers, final heads}, pack (, scheduler: p2p)]
+  bool rfold_ok = false;   // this stage range folds (>= 2 deferred stages, batch fits)
+  bool mr_rf = false;      // the current multi-rank decode runs it
+  cudaGraphExec_t g_compute_rf = nullptr, g_p2p_tick_rf = nullptr;
+  int64_t compute_rf_launches = 0, p2p_tick_rf_launches = 0, rf_body_launches = 0;
   int64_t tick_launches = 0, ar_launches = 0, prefill_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   // host staging
@@ -621,6 +628,8 @@ static void free_engine(ppsd_engine* e) {
   if (e->g_mr_prefill) cudaGraphExecDestroy(e->g_mr_prefill);
   for (auto& kv : e->eesd_graphs) cudaGraphExecDestroy(kv.second.first);
   if (e->g_p2p_tick) cudaGraphExecDestroy(e->g_p2p_tick);
+  if (e->g_compute_rf) cudaGraphExecDestroy(e->g_compute_rf);
+  if (e->g_p2p_tick_rf) cudaGraphExecDestroy(e->g_p2p_tick_rf);
   for (void* p : e->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* b : {(void*)e->d_xbuf, (void*)e->d_p2p_outbox, (void*)e->d_xcount, (void*)e->d_peer_xbuf,
                   (void*)e->d_xerr})
@@ -857,8 +866,15 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       if (ok) e->wstride[m] = WStride{(const void*)(uintptr_t)(ptr(l0) - (long long)l0 * st), st, l0 + nl};
     }
     const int qd = d.H * d.hd;
-    // rows: chains / prefill chunk [0, nbuf); exit-head layer copies [nbuf, 2*nbuf)
-    const size_t nb = (size_t)e->nbuf * (e->hl ? 2 : 1);
+    // rank fold: a stage range of a multi-rank split (not the whole model)
+    // whose deferred stages span >= 2 stages and whose batch fits one group;
+    // runs in greedy decodes unless the schedule is PIPELINED (ppsd_get_schedule)
+    e->rfold_ok = (e->lo > 1 || e->hi < e->S) && !e->hl && sched_rfold_useful(&e->cfg, e->lo, e->hi) &&
+                  sched_rfold_width(&e->cfg, e->lo, e->hi) <= kMaxVec;
+    c.rf_row0 = e->nbuf;
+    // rows: chains / prefill chunk [0, nbuf); exit-head layer copies or the
+    // rank fold's batch rows [nbuf, 2*nbuf)
+    const size_t nb = (size_t)e->nbuf * (e->hl || e->rfold_ok ? 2 : 1);
     CU(dalloc(&e->d_x, sizeof(float) * nb * d.d));
     CU(dalloc(&e->d_q, sizeof(float) * nb * qd));
     CU(dalloc(&e->d_o, sizeof(float) * nb * qd));
@@ -1221,7 +1237,7 @@ extern "C" int ppsd_decode(ppsd_engine* e, int32_t greedy, uint64_t rng_seed, co
 extern "C" int ppsd_set_schedule(ppsd_engine* e, int32_t schedule) {
   if (!e) return fail(PPSD_EINVAL, "null argument");
   if (schedule < PPSD_SCHEDULE_AUTO || schedule > PPSD_SCHEDULE_FOLDED) return fail(PPSD_EINVAL, "unknown schedule");
-  if (schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok)
+  if (schedule == PPSD_SCHEDULE_FOLDED && !e->fold_ok && !e->rfold_ok)
     return fail(PPSD_EUNSUPPORTED, "this engine cannot run the folded schedule");
   e->schedule = schedule;
   return PPSD_OK;
@@ -1232,7 +1248,9 @@ extern "C" int ppsd_get_schedule(ppsd_engine* e, int32_t greedy, int32_t* schedu
   const bool fold = e->fold_ok && e->md.kind == PPSD_MODEL_TRANSFORMER &&
                     (e->schedule == PPSD_SCHEDULE_FOLDED || (e->schedule == PPSD_SCHEDULE_AUTO && e->fold_auto)) &&
                     (greedy || e->cfg.k == 1);
-  *schedule = fold ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
+  // a rank of a multi-rank split: the per-rank fold (greedy)
+  const bool rfold = e->rfold_ok && greedy && e->schedule != PPSD_SCHEDULE_PIPELINED;
+  *schedule = fold || rfold ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
   return PPSD_OK;
 }
 
@@ -1757,6 +1775,117 @@ extern "C" int ppsd_read_logits(ppsd_engine* e, int32_t which, float* out) {
 // Every rank runs the identical scheduler, so ranks agree on every tick
 // without any other message.
 
+// Rank-fold tick graph (sched.h: sched_rfold_plan). The scheduler kernel of
+// the previous launch (or step) planned the tick; the first kernel opens the
+// IF node when the plan has a deferred batch (the handle resets to 0 at every
+// launch). p2p: the scheduler kernel for the next tick closes the graph.
+static int build_rf_graph(ppsd_engine* e, bool with_sched, cudaGraphExec_t* out, int64_t* n_launches) {
+  const SchedCfg& C = e->cfg;
+  const int lo = e->lo, hi = e->hi, k = C.k;
+  const int eager = lo <= k ? C.stage_first[k] + C.stage_layers[k] - C.stage_first[lo] : 0;
+  const int dlo = sched_rfold_first(&C, lo);
+  const int deferred = C.stage_first[hi] + C.stage_layers[hi] - C.stage_first[dlo];
+  cudaStream_t main_st = e->st, body_st = nullptr;
+  CU(cudaStreamCreateWithFlags(&body_st, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  int n_outer = 0, n_body = 0;
+  bool ok = true;
+  std::string err;
+  auto need = [&](bool cond, const char* what) {
+    if (!cond && ok) {
+      ok = false;
+      const cudaError_t le = g_launch_err != cudaSuccess ? g_launch_err : cudaGetLastError();
+      err = std::string(what) + ": " + cudaGetErrorString(le);
+    }
+  };
+  g_launch_err = cudaSuccess;
+  cudaError_t ce = cudaStreamBeginCapture(main_st, cudaStreamCaptureModeThreadLocal);
+  if (ce != cudaSuccess) {
+    cudaStreamDestroy(body_st);
+    CU(ce);
+  }
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaGraph_t cg = nullptr;
+  cudaGraphConditionalHandle h = 0;
+  need(cudaStreamGetCaptureInfo(main_st, &cs, nullptr, &cg, &deps, &nd) == cudaSuccess, "capture info");
+  if (ok) need(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault) == cudaSuccess,
+               "conditional handle");
+  if (ok) need(launch_pdl(rf_cond_kernel, dim3(1), dim3(32), 0, main_st, (const TickCtx*)e->d_ctx,
+                          (unsigned long long)h) == cudaSuccess, "IF setter");
+  n_outer = 1;
+  if (ok && eager > 0) {  // the chain reaching stage lo: stages lo..k, exit head
+    const int m = enqueue_layers(e, e->d_work, eager, false);
+    need(m >= 0, "eager layers");
+    n_outer += m;
+    need(ok && enqueue_gemv(e, e->d_work, 0, kMatHead) == cudaSuccess, "exit head");
+    n_outer += 1;
+  }
+  cudaGraph_t body = nullptr;
+  if (ok) {
+    need(cudaStreamGetCaptureInfo(main_st, &cs, nullptr, &cg, &deps, &nd) == cudaSuccess, "capture info");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode = nullptr;
+    if (ok) need(cudaGraphAddNode(&cnode, cg, deps, nd, &cp) == cudaSuccess, "conditional node");
+    if (ok) body = cp.conditional.phGraph_out[0];
+    if (ok) need(cudaStreamUpdateCaptureDependencies(main_st, &cnode, 1, cudaStreamSetCaptureDependencies) ==
+                     cudaSuccess, "capture deps");
+  }
+  if (ok && body) {  // body: gather, deferred layers (batched plans), final heads
+    need(cudaStreamBeginCaptureToGraph(body_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+             cudaSuccess, "body capture");
+    if (ok) {
+      e->st = body_st;
+      need(launch_pdl(rf_gather_kernel, dim3(1), dim3(256), 0, body_st, (const TickCtx*)e->d_ctx) == cudaSuccess,
+           "gather");
+      n_body = 1;
+      e->small_batch = sched_rfold_width(&C, lo, hi) <= 5;
+      const int m = enqueue_layers(e, e->d_work_deep, deferred, true);
+      need(m >= 0, "deferred layers");
+      n_body += m;
+      if (ok && hi == e->S) {
+        need(enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
+             "final heads");
+        n_body += 1;
+      }
+      e->small_batch = false;
+      e->st = main_st;
+      cudaGraph_t bg = body;
+      need(cudaStreamEndCapture(body_st, &bg) == cudaSuccess, "body end capture");
+    }
+  }
+  // after the IF node: plain launches (a programmatic edge needs a kernel predecessor)
+  if (ok) {
+    pack_outbox_kernel<<<1, 256, 0, main_st>>>((const TickCtx*)e->d_ctx, 0);
+    need(cudaGetLastError() == cudaSuccess, "pack");
+    n_outer += 1;
+  }
+  if (ok && with_sched) {
+    need(launch_pdl(sched_tick_kernel, dim3(1), dim3(256), 0, main_st, (const TickCtx*)e->d_ctx, 0) ==
+             cudaSuccess, "scheduler");
+    n_outer += 1;
+  }
+  e->st = main_st;
+  ce = cudaStreamEndCapture(main_st, &g);
+  cudaStreamDestroy(body_st);
+  if (!ok) {
+    if (g) cudaGraphDestroy(g);
+    return fail(PPSD_ECUDA, "rank-fold tick graph: " + err);
+  }
+  CU(ce);
+  ce = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  CU(ce);
+  *n_launches = n_outer;
+  e->rf_body_launches = n_body;
+  return PPSD_OK;
+}
+
 static int build_mr_graphs(ppsd_engine* e) {
   if (e->g_compute) return PPSD_OK;
   int rc = capture(
@@ -1871,10 +2000,21 @@ extern "C" int ppsd_step_begin(ppsd_engine* e, const int32_t* prompt, int32_t n_
   c.owner_S = stage_owner[e->S];
   c.owner_prev = e->lo > 1 ? stage_owner[e->lo - 1] : -1;
   c.n_prompt = n_prompt;
+  // greedy decodes fold this rank's stages where they can (ppsd_get_schedule)
+  e->mr_rf = e->rfold_ok && e->mr_greedy && e->schedule != PPSD_SCHEDULE_PIPELINED;
+  if (e->mr_rf && !e->g_compute_rf) {
+    rc = build_rf_graph(e, false, &e->g_compute_rf, &e->compute_rf_launches);
+    if (rc) return rc;
+  }
+  c.rfold = e->mr_rf ? 1 : 0;
+  c.has_cond = 0;
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
-  s.c.fold = 0;  // multi-rank runs use the pipelined tick graphs
+  s.c.fold = 0;  // the single-device fold needs every stage; ranks fold their own range (rfold)
+  s.c.rfold = e->mr_rf ? 1 : 0;
+  s.c.rf_lo = e->lo;
+  s.c.rf_hi = e->hi;
   s.c.model = 1;
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;
@@ -1913,8 +2053,8 @@ extern "C" int ppsd_prefill_compute(ppsd_engine* e) {
 extern "C" int ppsd_step_compute(ppsd_engine* e) {
   if (!e || !e->g_compute) return fail(PPSD_ESTATE, "call ppsd_step_begin first");
   if (e->mr_ticks_launched == 0) CU(cudaEventRecord(e->ev2, e->st));  // decode starts (prefill done)
-  CU(cudaGraphLaunch(e->g_compute, e->st));
-  e->mr_launches += e->compute_launches;
+  CU(cudaGraphLaunch(e->mr_rf ? e->g_compute_rf : e->g_compute, e->st));
+  e->mr_launches += e->mr_rf ? e->compute_rf_launches : e->compute_launches;
   return PPSD_OK;
 }
 
@@ -1957,7 +2097,13 @@ extern "C" int ppsd_step_end(ppsd_engine* e, int32_t* out_tokens, ppsd_metrics* 
   fill_metrics(e, s, out);
   out->decode_ms = ms;    // decode ticks on this rank's stream (CUDA events)
   out->prefill_ms = pre;  // pipelined prefill steps
-  out->gpu_launches = e->mr_launches;
+  out->gpu_launches = e->mr_launches + (e->mr_rf ? (int64_t)s.fold_batches * e->rf_body_launches : 0);
+  out->schedule = e->mr_rf ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
+  if (e->mr_rf) {  // this rank's deferred batches (sched_rfold_plan)
+    out->deep_batches = s.fold_batches;
+    out->deep_vectors = s.fold_vectors;
+    out->deep_pos_sum = s.fold_pos_sum;
+  }
   if (out_tokens)
     CU(cudaMemcpy(out_tokens, e->d_tokens + e->mr_n_prompt, sizeof(int32_t) * e->mr_stop, cudaMemcpyDeviceToHost));
   if (trace) {
@@ -2093,6 +2239,12 @@ extern "C" int ppsd_p2p_connect(ppsd_engine* e, int32_t rank, const void* ipc_ha
         &e->g_p2p_tick, &e->p2p_tick_launches);
     if (rc) return rc;
   }
+  if (e->rfold_ok && !e->g_p2p_tick_rf) {
+    CU(cudaFuncGetAttributes(&fa, rf_cond_kernel));
+    CU(cudaFuncGetAttributes(&fa, rf_gather_kernel));
+    rc = build_rf_graph(e, true, &e->g_p2p_tick_rf, &e->p2p_tick_rf_launches);
+    if (rc) return rc;
+  }
   return PPSD_OK;
 }
 
@@ -2111,7 +2263,10 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   const int64_t max_ticks = (int64_t)max_tokens * e->S * e->cfg.per + (int64_t)e->S * e->cfg.per + 8;
   if (max_ticks * (e->S + 2) > e->trace_cap) return fail(PPSD_ESTATE, "p2p trace reservation too small");
   TickCtx& c = e->h_ctx;
+  e->mr_rf = e->rfold_ok && e->mr_greedy && e->schedule != PPSD_SCHEDULE_PIPELINED && e->g_p2p_tick_rf;
   c.fold = 0;
+  c.rfold = e->mr_rf ? 1 : 0;
+  c.has_cond = 0;
   c.trace = e->d_trace;
   c.trace_cap = e->trace_cap;
   c.n_prompt = n_prompt;
@@ -2125,7 +2280,10 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   Sched& s = *e->h_sched;
   memset(&s, 0, sizeof(Sched));
   s.c = e->cfg;
-  s.c.fold = 0;  // multi-rank runs use the pipelined tick graphs
+  s.c.fold = 0;
+  s.c.rfold = e->mr_rf ? 1 : 0;
+  s.c.rf_lo = e->lo;
+  s.c.rf_hi = e->hi;
   s.c.model = 1;
   s.c.force_reject = force_reject;
   s.c.stop = max_tokens;
@@ -2162,7 +2320,8 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   for (;;) {  // replicated state: every rank launches the same number of ticks
     const int64_t n = std::max<int64_t>(1, (int64_t)max_tokens - s.committed);
     NvtxRange nv("ppsd.p2p ticks", 1, n);
-    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(e->g_p2p_tick, e->st));
+    cudaGraphExec_t tick = e->mr_rf ? e->g_p2p_tick_rf : e->g_p2p_tick;
+    for (int64_t i = 0; i < n; ++i) CU(cudaGraphLaunch(tick, e->st));
     ticks_launched += n;
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(&s) + off, reinterpret_cast<char*>(e->d_sched) + off, len,
                        cudaMemcpyDeviceToHost, e->st));
@@ -2183,7 +2342,14 @@ extern "C" int ppsd_p2p_decode(ppsd_engine* e, const int32_t* prompt, int32_t n_
   fill_metrics(e, s, out);
   out->decode_ms = ms;
   out->prefill_ms = pre;
-  out->gpu_launches = launches + ticks_launched * e->p2p_tick_launches;
+  out->gpu_launches = launches + ticks_launched * (e->mr_rf ? e->p2p_tick_rf_launches : e->p2p_tick_launches) +
+                      (e->mr_rf ? (int64_t)s.fold_batches * e->rf_body_launches : 0);
+  out->schedule = e->mr_rf ? PPSD_SCHEDULE_FOLDED : PPSD_SCHEDULE_PIPELINED;
+  if (e->mr_rf) {
+    out->deep_batches = s.fold_batches;
+    out->deep_vectors = s.fold_vectors;
+    out->deep_pos_sum = s.fold_pos_sum;
+  }
   if (out_tokens) CU(cudaMemcpy(out_tokens, e->d_tokens + n_prompt, sizeof(int32_t) * max_tokens, cudaMemcpyDeviceToHost));
   if (trace) {
     const int64_t nr = std::min<int64_t>(s.trace_n, trace_cap);

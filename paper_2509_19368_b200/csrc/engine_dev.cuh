@@ -59,6 +59,10 @@ struct TickCtx {
   Work* work_deep;
   unsigned long long cond;  // cudaGraphConditionalHandle of the folded tick graph
   int32_t has_cond;         // 0: deep part captured inline (PPSD_FOLD_COND=0, profiling)
+  // folded stage range of one rank (sched.h: sched_rfold_plan; multi-rank,
+  // greedy): deferred batches in activation rows rf_row0 .. rf_row0 + width
+  int32_t rfold;
+  int32_t rf_row0;
   // transformer-layer exit head (ppsd_model_desc.exit_head_layer): the draft
   // is the norm head on that decoder layer's output for a COPY of the
   // exit-layer state (rows head_row..), so the chain's own state continues
@@ -104,6 +108,8 @@ __global__ void ar_begin_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void ar_end_kernel(const TickCtx* ctxp, ArCtl* ctl, int with_head);
 __global__ void toy_tick_kernel(const TickCtx* ctxp);
 __global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
+__global__ void rf_cond_kernel(const TickCtx* ctxp, unsigned long long handle);
+__global__ void rf_gather_kernel(const TickCtx* ctxp);
 __global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void p2p_wait_kernel(const TickCtx* ctxp);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);

@@ -104,6 +104,28 @@ void ppsdh_fold_plan(void* p, int32_t* out) {
   out[4] = h->s.c.shallow_layers;
 }
 
+// rank fold (sched.h: sched_rfold_plan) of stages lo..hi; returns the batch width bound
+int ppsdh_set_rfold(void* p, int lo, int hi) {
+  HostSched* h = (HostSched*)p;
+  h->s.c.rfold = 1;
+  h->s.c.rf_lo = lo;
+  h->s.c.rf_hi = hi;
+  return sched_rfold_width(&h->s.c, lo, hi);
+}
+int ppsdh_rfold_first(void* p, int lo) { return sched_rfold_first(&((HostSched*)p)->s.c, lo); }
+int ppsdh_rfold_useful(void* p, int lo, int hi) { return sched_rfold_useful(&((HostSched*)p)->s.c, lo, hi); }
+
+// out: [fold_nb, fold_base, deep_done, rf_arrived, deep_done before]
+void ppsdh_rfold_plan(void* p, int32_t* out) {
+  HostSched* h = (HostSched*)p;
+  out[4] = h->s.deep_done;
+  sched_rfold_plan(&h->s);
+  out[0] = h->s.fold_nb;
+  out[1] = h->s.fold_base;
+  out[2] = h->s.deep_done;
+  out[3] = h->s.rf_arrived;
+}
+
 int ppsdh_chain_pos(void* p, int slot) { return ((HostSched*)p)->s.ch_pos[slot]; }
 int ppsdh_chain_tok(void* p, int slot) { return ((HostSched*)p)->s.ch_tok[slot]; }
 uint64_t ppsdh_prefix_digest(void* p, int n) { return ((HostSched*)p)->pdig[n]; }

@@ -27,6 +27,14 @@ struct Work {
   int32_t head_out[2];          // argmax written by the head kernel
   int32_t vec_out[kMaxVec];     // kMatHeadV: argmax of each vector of group 0 (final head)
   int32_t src_slot;             // exit-head layer (head_copy_kernel): first row copied into slot[0]
+  // rank fold (sched.h: sched_rfold_plan), written by the scheduler kernel:
+  // `work` = the eager stages of the chain reaching stage lo, `work_deep` =
+  // the deferred batch; the box of this tick carries row out_row (-1: none),
+  // the exit token exit_tok (-2: this tick's exit head, -1: not the owner) and
+  // the final token vec_out[final_idx] of work_deep (-1: none); rf_src: the
+  // batch chains' activation slots, gathered into the batch rows
+  int32_t out_row, out_slot, out_pos, exit_tok, final_idx;
+  int32_t rf_src[kMaxVec];
 };
 
 struct LayerW {

@@ -225,6 +225,10 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       final_tok = (c.greedy && s.final_slot >= 0)
                       ? c.work_deep->vec_out[s.ch_pos[s.final_slot] - s.fold_base] : final_tok;
     }
+    // rank fold: the chain that ran its eager stages last tick keeps its
+    // draft until the machine emits it at stage k
+    if (c.rfold && !begin && c.work->slot[0] >= 0 && c.work->head_slot[0] >= 0)
+      s.ch_draft[c.work->slot[0]] = c.work->head_out[0];
     if (!begin)
       sched_finish(&s, exit_tok, final_tok, c.tokens, c.pdig, c.trace, c.trace_cap, s_final_ok);
     sched_plan(&s);
@@ -255,6 +259,41 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       }
       s_launch_slot = row;
       s_launch_pos = row >= 0 ? s.ch_pos[s.work[1]] : 0;
+    } else if (c.rfold) {  // sched.h: sched_rfold_plan
+      sched_rfold_plan(&s);
+      const int lo = c.lo, hi = c.hi, k = s.c.k;
+      const int a = s.work[lo];
+      const bool eager = lo <= k;  // the rank owns the exit stage: stages lo..k + exit head on arrival
+      w->G = 1;
+      w->slot[0] = eager ? a : -1;
+      w->pos[0] = a >= 0 ? s.c.n_prompt + s.ch_pos[a] - 2 : 0;
+      w->first[0] = s.c.stage_first[lo];
+      w->nl[0] = eager ? s.c.stage_first[k] + s.c.stage_layers[k] - s.c.stage_first[lo] : 1;
+      w->nv[0] = 1;
+      w->head_slot[0] = eager ? a : -1;
+      w->head_slot[1] = -1;
+      const int ex = s.exit_slot;
+      w->exit_tok = !eager || ex < 0 ? -1 : k == lo ? -2 : s.ch_draft[ex];
+      Work* wd = c.work_deep;
+      const int dlo = sched_rfold_first(&s.c, lo);
+      wd->G = 1;
+      wd->slot[0] = s.fold_nb > 0 ? c.rf_row0 : -1;
+      wd->pos[0] = s.c.n_prompt + s.fold_base - 2;
+      wd->first[0] = s.c.stage_first[dlo];
+      wd->nl[0] = s.c.stage_first[hi] + s.c.stage_layers[hi] - s.c.stage_first[dlo];
+      wd->nv[0] = s.fold_nb > 0 ? s.fold_nb : 1;
+      wd->head_slot[0] = wd->head_slot[1] = -1;
+      for (int j = 0; j < s.fold_nb; ++j) wd->rf_src[j] = (s.fold_base + j) % s.c.nslot;
+      // this tick's box: the chain due at stage hi (its row of the latest batch)
+      const int due = s.work[hi];
+      const int di = due >= 0 ? s.ch_pos[due] - s.fold_base : -1;
+      w->out_row = due >= 0 && hi < s.c.S ? c.rf_row0 + di : -1;
+      w->out_slot = due;
+      w->out_pos = due >= 0 ? s.c.n_prompt + s.ch_pos[due] - 2 : -1;
+      w->final_idx = due >= 0 && hi == s.c.S ? di : -1;
+      if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
+      s_launch_slot = (s.launched && lo == 1) ? s.work[1] : -1;
+      s_launch_pos = s_launch_slot >= 0 ? s.ch_pos[s_launch_slot] : 0;
     } else {
       w->G = c.hi - c.lo + 1;
       for (int g = 0; g < w->G; ++g) {
@@ -298,16 +337,23 @@ __global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, i
   const TickCtx c = *ctxp;
   int32_t* hdr = reinterpret_cast<int32_t*>(c.outbox);
   const Work* w = prefill ? c.work_ar : c.work;
-  const int slot = w->slot[w->G - 1];
-  const bool send = slot >= 0 && (prefill || c.hi < c.model_stages);
+  const bool rf = c.rfold && !prefill;  // rank fold: the due chain's row of the latest batch
+  const int slot = rf ? w->out_slot : w->slot[w->G - 1];
+  const int row = rf ? w->out_row : slot;
+  const bool send = row >= 0 && (prefill || c.hi < c.model_stages);
   if (threadIdx.x == 0) {
-    hdr[0] = w->head_slot[0] >= 0 ? w->head_out[0] : -1;
-    hdr[1] = w->head_slot[1] >= 0 ? w->head_out[1] : -1;
+    if (rf) {
+      hdr[0] = w->exit_tok == -2 ? w->head_out[0] : w->exit_tok;
+      hdr[1] = w->final_idx >= 0 ? c.work_deep->vec_out[w->final_idx] : -1;
+    } else {
+      hdr[0] = w->head_slot[0] >= 0 ? w->head_out[0] : -1;
+      hdr[1] = w->head_slot[1] >= 0 ? w->head_out[1] : -1;
+    }
     hdr[2] = send ? slot : -1;
-    hdr[3] = send ? w->pos[w->G - 1] : -1;
+    hdr[3] = send ? (rf ? w->out_pos : w->pos[w->G - 1]) : -1;
   }
   if (send) {
-    const float* x = c.x + (size_t)slot * c.d;
+    const float* x = c.x + (size_t)row * c.d;
     for (int i = threadIdx.x; i < c.d; i += blockDim.x) c.outbox[kBoxHeader + i] = x[i];
   }
   if (c.box_logits && !prefill) {  // sampling: the exit / final logits of the heads this rank owns
@@ -320,6 +366,30 @@ __global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, i
   if (c.p2p) {  // NVLink peer stores into every rank's exchange buffer + release flags
     __syncthreads();
     p2p_publish(c);
+  }
+}
+
+// Rank fold: open the deferred batch's graph IF node for this launch (the
+// scheduler kernel planned the tick at the end of the previous launch).
+__global__ void rf_cond_kernel(const TickCtx* ctxp, unsigned long long handle) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0 && ctxp->work_deep->slot[0] >= 0) cudaGraphSetConditional(handle, 1u);
+}
+
+// Rank fold: the batch chains' activations (stage-lo inputs, or the eager
+// stages' outputs) from their slots into the consecutive batch rows.
+__global__ void __launch_bounds__(256) rf_gather_kernel(const TickCtx* ctxp) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  const Work* wd = c.work_deep;
+  if (wd->slot[0] < 0) return;
+  const int nv = wd->nv[0], d4 = c.d / 4;
+  for (int j = 0; j < nv; ++j) {
+    const float4* src = reinterpret_cast<const float4*>(c.x + (size_t)wd->rf_src[j] * c.d);
+    float4* dst = reinterpret_cast<float4*>(c.x + (size_t)(wd->slot[0] + j) * c.d);
+    for (int i = threadIdx.x; i < d4; i += blockDim.x) dst[i] = src[i];
   }
 }
 

@@ -45,6 +45,8 @@ struct SchedCfg {
   int32_t n_prompt;
   int32_t nslot;
   int32_t fold;         // 1: folded single-GPU execution (sched_fold_plan)
+  int32_t rfold;        // 1: folded stage range rf_lo..rf_hi of one rank (sched_rfold_plan)
+  int32_t rf_lo, rf_hi;
   double alpha;         // Bernoulli acceptance rate
   uint64_t verify_seed; // derive_seed(rng.seed, "verify") (pipesim.py:693)
   int32_t stage_layers[kMaxStages + 1];  // 1-based
@@ -72,7 +74,7 @@ struct Sched {
   int32_t fold_nb;       // vectors in this tick's deep batch, 0 = none
   int32_t fold_row;      // fold row of the chain launched this tick, -1 = none
   int32_t fold_batches;  // deep batches run so far
-  int32_t fold_pad_;
+  int32_t rf_arrived;    // rank fold: highest position that reached stage rf_lo
   int64_t fold_vectors;  // chains that went through a deep batch
   int64_t fold_pos_sum;  // sum of their positions (attention context accounting)
   int32_t ch_draft[kMaxSlots];  // eager exit-head argmax per chain
@@ -96,6 +98,7 @@ PPSD_HD void sched_reset(Sched* s) {
   s->fold_nb = 0;
   s->fold_row = kNone;
   s->fold_batches = 0;
+  s->rf_arrived = 0;
   s->fold_vectors = s->fold_pos_sum = 0;
 }
 
@@ -235,7 +238,8 @@ PPSD_HD void sched_finish(Sched* s, int exit_tok, int final_tok, int32_t* tokens
     sched_emit(s, slot, 1, tr, cap);
   }
   if (rollback != kNone) {  // pipesim.py:779-786
-    if (s->c.fold) s->deep_done = rollback;  // deep results past the rollback belong to flushed chains
+    if (s->c.fold || s->c.rfold) s->deep_done = rollback;  // deep results past the rollback belong to flushed chains
+    if (s->c.rfold && s->rf_arrived > rollback) s->rf_arrived = rollback;
     s->tq_n = 0;
     for (int st = 1; st <= S; ++st) s->cur[st] = kNone;
     s->draft_head = rollback;
@@ -282,6 +286,48 @@ PPSD_HD void sched_fold_plan(Sched* s) {
 // Largest fold row / batch the folded schedule can need: chains in flight.
 PPSD_HD int sched_fold_width(const SchedCfg* c) { return (c->S - 1) * c->per + 1; }
 
+// Folded execution of ONE RANK's stage range lo..hi (multi-rank, greedy;
+// SchedCfg.rfold). The single-device fold above, restricted to a rank: the
+// rank's stages up to the exit stage k ("eager": lo..k when lo <= k) run with
+// the exit head in the tick the chain reaches stage lo, and the rest of its
+// stages ("deferred": max(lo, k+1)..hi) run as ONE batch for every chain
+// that has reached stage lo past deep_done, in the tick the oldest of them is
+// due at stage hi (its activation goes into this tick's box, or its final
+// head decides this tick's verdict). The rank streams its deferred weights
+// once per batch instead of once per tick. Chains arrive at stage lo in
+// position order, so a batch is the consecutive positions deep_done+1 ..
+// rf_arrived; every chain of a batch is due at stage hi before the next batch
+// is planned (the next batch is planned only when a chain past it is due), so
+// the batch rows stay valid until then. Rollback: chains past the rejected
+// position are flushed everywhere (sched_finish). Ticks, verdicts, tokens and
+// the trace are the machine's; only WHEN a rank's forwards run changes.
+PPSD_HD void sched_rfold_plan(Sched* s) {
+  s->fold_nb = 0;
+  const int lo = s->c.rf_lo, hi = s->c.rf_hi;
+  const int a = s->work[lo];
+  if (a != kNone && s->ch_pos[a] > s->rf_arrived) s->rf_arrived = s->ch_pos[a];
+  const int due = s->work[hi];
+  if (due != kNone && s->ch_pos[due] > s->deep_done) {
+    s->fold_base = s->deep_done + 1;
+    s->fold_nb = s->rf_arrived - s->deep_done;
+    s->deep_done = s->rf_arrived;
+    s->fold_batches += 1;
+    s->fold_vectors += s->fold_nb;
+    s->fold_pos_sum += (int64_t)s->fold_nb * (s->fold_base + s->rf_arrived) / 2;
+  }
+}
+
+// First deferred stage of a rank fold, and the largest batch it can plan:
+// chains reach stage lo at most one per tick and are due (hi - lo) * per
+// ticks later.
+PPSD_HD int sched_rfold_first(const SchedCfg* c, int lo) { return lo > c->k ? lo : c->k + 1; }
+PPSD_HD int sched_rfold_width(const SchedCfg* c, int lo, int hi) { return (hi - lo) * c->per + 1; }
+// A rank folds when its deferred part spans >= 2 stages (a single deferred
+// stage is due the tick its chain arrives: every batch would hold one chain).
+PPSD_HD bool sched_rfold_useful(const SchedCfg* c, int lo, int hi) {
+  return hi - sched_rfold_first(c, lo) + 1 >= 2;
+}
+
 // Host-side configuration helper (also used by the CPU test build).
 PPSD_HD int sched_configure(SchedCfg* c, int n_layers, int exit_depth, int exit_stage,
                             int comm_latency) {
@@ -303,6 +349,7 @@ PPSD_HD int sched_configure(SchedCfg* c, int n_layers, int exit_depth, int exit_
   }
   c->shallow_layers = c->stage_first[k] + c->stage_layers[k];
   c->fold = 0;
+  c->rfold = c->rf_lo = c->rf_hi = 0;
   c->nslot = (S - 1) * c->per + 2;
   if (c->nslot > kMaxSlots || S * c->per + 2 > kTransitCap) return -1;
   return 0;

@@ -124,7 +124,8 @@ class StageShard:
         metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects, m.accepts + m.rejects,
                                self.cfg.ar_ticks_per_token)
         self.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches,
-                         ticks=m.ticks)
+                         ticks=m.ticks, schedule=_lib.schedule_name(m.schedule), deep_batches=m.deep_batches,
+                         deep_vectors=m.deep_vectors)
         return out.tolist(), metrics, EventTrace.from_array(rows[: n.value])
 
 
@@ -247,5 +248,7 @@ def decode_ppsd_p2p(shard: StageShard, prompt, max_tokens: int, *, force_reject:
     _lib.check(rc, "p2p_decode")
     metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects, m.accepts + m.rejects,
                            shard.cfg.ar_ticks_per_token)
-    shard.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches, ticks=m.ticks)
+    shard.last = dict(decode_ms=m.decode_ms, prefill_ms=m.prefill_ms, gpu_launches=m.gpu_launches, ticks=m.ticks,
+                      schedule=_lib.schedule_name(m.schedule), deep_batches=m.deep_batches,
+                      deep_vectors=m.deep_vectors)
     return out.tolist(), metrics, EventTrace.from_array(rows[: n.value])

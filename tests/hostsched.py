@@ -43,6 +43,10 @@ def lib():
         L.ppsdh_set_fold.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_fold_width.argtypes = [C.c_void_p]
         L.ppsdh_fold_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+        L.ppsdh_set_rfold.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ppsdh_rfold_first.argtypes = [C.c_void_p, C.c_int]
+        L.ppsdh_rfold_useful.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ppsdh_rfold_plan.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.ppsdh_chain_pos.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_chain_tok.argtypes = [C.c_void_p, C.c_int]
         L.ppsdh_prefix_digest.argtypes = [C.c_void_p, C.c_int]
@@ -240,3 +244,121 @@ def run_bernoulli(n_layers, exit_depth, alpha, horizon, verify_seed, *, exit_sta
     while hs.plan()[0]:
         hs.finish()
     return hs.metrics(), hs.trace_rows()
+
+
+def run_toy_multirank_folded(lm, n_layers, exit_depth, prompt, stop, world, *, exit_stage=0,
+                             comm_latency=0, force_reject=False, max_batch=16):
+    """Multi-rank emulation with the per-rank fold (sched.h: sched_rfold_plan):
+    `world` replicated schedulers, one per rank, each owning a contiguous stage
+    range (distributed.stage_owner). A rank whose deferred part spans >= 2
+    stages folds: its eager stages (lo..k) + exit head run when a chain
+    reaches stage lo, its deferred stages run as one batch when the oldest
+    unprocessed chain is due at stage hi; other ranks run every planned stage
+    in its tick. Activations move between ranks only through the box of the
+    tick the sender's stage hi is planned, and arrive at the end of that tick
+    (the engine's exchange). Every input is checked to exist when used.
+    Returns (tokens, metrics, trace, {rank: batch sizes})."""
+    owner = [-1] + [(st - 1) * world // -(-n_layers // exit_depth) for st in
+                    range(1, -(-n_layers // exit_depth) + 1)]
+    ranks = []
+    for r in range(world):
+        hs = HostSched(n_layers, exit_depth, exit_stage=exit_stage, comm_latency=comm_latency,
+                       model=1, force_reject=force_reject, stop=stop, prompt=prompt,
+                       toy_seed=lm.seed)
+        sts = [st for st in range(1, hs.S + 1) if owner[st] == r]
+        lo, hi = sts[0], sts[-1]
+        fold = bool(lib().ppsdh_rfold_useful(hs.h, lo, hi))
+        width = 0
+        if fold:
+            width = lib().ppsdh_set_rfold(hs.h, lo, hi)
+            fold = width <= max_batch
+            assert fold, "the engine runs such a rank pipelined"
+        ranks.append(dict(hs=hs, lo=lo, hi=hi, fold=fold, width=width, dlo=lib().ppsdh_rfold_first(hs.h, lo),
+                          act={}, draft={}, final={}, out={}, recv={}, batches=[]))
+    hs0 = ranks[0]["hs"]
+    if stop == 0:
+        return [], sp.make_metrics(0, 0, 0, 0, 0, hs0.S * hs0.per), [], {}
+    layers = hs0.layers
+    S = hs0.S
+    first = [0] + [sum(layers[:i]) for i in range(S)]  # 1-based: first[st] = first layer of stage st
+    last = [0] + [sum(layers[:i + 1]) for i in range(S)]
+    while True:
+        plans = [R["hs"].plan() for R in ranks]
+        r0, work, info = plans[0]
+        for p in plans[1:]:
+            assert p == plans[0]  # replicated
+        if not r0:
+            break
+        k = info[6]
+        exit_slot, final_slot = info[2], info[3]
+        sent = {}
+        exit_tok = final_tok = -1
+        for rank, R in enumerate(ranks):
+            hs, lo, hi = R["hs"], R["lo"], R["hi"]
+            pos_of = hs.chain_pos
+
+            def stage_input(slot):
+                pos = pos_of(slot)
+                if lo == 1:
+                    return hs.prefix_digest(hs.n_prompt + pos - 1)
+                assert pos in R["recv"], f"rank {rank}: chain {pos} used before its box arrived"
+                return R["recv"][pos]
+
+            if R["fold"]:
+                out5 = (C.c_int32 * 5)()
+                lib().ppsdh_rfold_plan(hs.h, out5)
+                nb, base, deep_done, arrived, before = list(out5)
+                a = work[lo]
+                if a >= 0:  # arrival at stage lo: input now, eager stages + exit head
+                    pos = pos_of(a)
+                    d = stage_input(a)
+                    if lo <= k:
+                        d = lm.advance_digest(d, first[lo], last[k])
+                        fin = lm.advance_digest(d, last[k], n_layers)
+                        R["draft"][pos] = sp.first_argmax(lm.exit_logits(fin, d))
+                    R["act"][pos] = d
+                if nb > 0:
+                    assert base == before + 1 and 1 <= nb <= R["width"] and deep_done == base + nb - 1
+                    assert arrived == deep_done
+                    for p in range(base, base + nb):
+                        assert p in R["act"], f"rank {rank}: batch chain {p} has no input"
+                        o = lm.advance_digest(R["act"][p], first[R["dlo"]], last[hi])
+                        R["out"][p] = o
+                        if hi == S:
+                            R["final"][p] = sp.first_argmax(lm.logits(o))
+                    R["batches"].append(nb)
+                due = work[hi]
+                if due >= 0:
+                    p = pos_of(due)
+                    assert p <= deep_done and p in R["out"], f"rank {rank}: chain {p} due without output"
+                    if hi < S:
+                        sent[rank] = (p, R["out"][p])
+                    else:
+                        final_tok = R["final"][p]
+                if lo <= k <= hi and exit_slot >= 0:
+                    exit_tok = R["draft"][pos_of(exit_slot)]
+            else:  # pipelined rank: every planned stage in its tick
+                for st in range(lo, hi + 1):
+                    slot = work[st]
+                    if slot < 0:
+                        continue
+                    pos = pos_of(slot)
+                    d = stage_input(slot) if st == lo else R["act"][pos]
+                    R["act"][pos] = lm.advance_digest(d, first[st], last[st])
+                    if st == k:
+                        fin = lm.advance_digest(R["act"][pos], last[k], n_layers)
+                        exit_tok = sp.first_argmax(lm.exit_logits(fin, R["act"][pos]))
+                    if st == hi and hi < S:
+                        sent[rank] = (pos, R["act"][pos])
+                    if st == S:
+                        final_tok = sp.first_argmax(lm.logits(R["act"][pos]))
+        for rank, (p, d) in sent.items():  # the exchange at the end of the tick
+            ranks[rank + 1]["recv"][p] = d
+        for R in ranks:
+            R["hs"].finish(exit_tok, final_tok)
+    ms = [R["hs"].metrics() for R in ranks]
+    rows = [R["hs"].trace_rows() for R in ranks]
+    for m, rw in zip(ms[1:], rows[1:]):
+        assert m == ms[0] and rw == rows[0]
+    m = ms[0]
+    return hs0.tokens(m[0]), m, rows[0], {i: R["batches"] for i, R in enumerate(ranks) if R["fold"]}

@@ -142,3 +142,37 @@ def test_loopback_edge_lengths(n_prompt, max_tokens, mode):
         assert toks == want[0]
         assert m == want[1]
         assert tr.to_csv() == want[2].to_csv()
+
+
+@pytest.mark.parametrize("world,k,comm,force", [(2, 1, 0, False), (2, 2, 0, False), (4, 1, 0, False),
+                                                (3, 1, 0, False), (2, 1, 1, False), (2, 1, 0, True)])
+def test_loopback_rank_fold(world, k, comm, force):
+    """Per-rank fold (sched.h: sched_rfold_plan): 8 one-layer stages, so every
+    rank with >= 2 deferred stages batches them (eager exit stages when it owns
+    k, draft kept per chain when k > lo). Greedy tokens, metrics and trace equal
+    the single-device decode, and equal the same ranks run pipelined."""
+    from paper_2509_19368_b200.distributed import StageShard
+
+    config = ppsd.TransformerConfig(8, 512, 8, 8, 64, 1408, 2048, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 1, exit_stage=k, comm_latency=comm)
+    prompt = [int(t) for t in np.random.default_rng(29).integers(0, config.vocab, size=19)]
+    full = ppsd.TransformerLM(config, seed=11, deep_scale=0.3, deep_from=k)
+    want = ppsd.decode_ppsd(full, cfg, prompt, 48, "greedy", ppsd.RngStream(0), force_reject=force)
+    shards = [StageShard(config, cfg, r, world, seed=11, deep_scale=0.3, deep_from=k) for r in range(world)]
+    folded = [s.engine.schedule("greedy") == "folded" for s in shards]
+    assert any(folded), "no rank folds in this split"
+    for sched in ("auto", "pipelined"):
+        for s in shards:
+            s.engine.set_schedule(sched)
+        res = run_loopback(shards, prompt, 48, force_reject=force)
+        for toks, m, tr in res:
+            assert toks == want[0]
+            assert m == want[1]
+            assert tr.to_csv() == want[2].to_csv()
+        for s, f in zip(shards, folded):
+            ran = s.last["schedule"]
+            assert ran == ("folded" if f and sched == "auto" else "pipelined"), (sched, ran)
+            if ran == "folded":
+                # its deferred layers stream once per batch, not once per tick
+                assert 0 < s.last["deep_batches"] < s.last["ticks"], s.last
+                assert s.last["deep_vectors"] > s.last["deep_batches"], s.last

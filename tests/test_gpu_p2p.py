@@ -180,3 +180,37 @@ def test_p2p_two_processes_ipc():
         assert toks == want_t, rank
         assert m == tuple(want_m.__dict__.values()), rank
         assert csv == want_tr.to_csv(), rank
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_threads_rank_fold(world, monkeypatch):
+    """Per-rank fold over the peer-store transport: 8 one-layer stages."""
+    monkeypatch.setenv("PPSD_PDL", "0")
+    from paper_2509_19368_b200.distributed import StageShard, decode_ppsd_p2p, p2p_connect, p2p_prepare
+
+    config = ppsd.TransformerConfig(**CONFIG, kv_dtype="bf16", max_ctx=512)
+    cfg = ppsd.PipelineConfig(8, 1)
+    prompt = [int(t) for t in np.random.default_rng(31).integers(0, config.vocab, size=17)]
+    full = ppsd.TransformerLM(config, seed=5, deep_scale=0.3, deep_from=1)
+    want_t, want_m, want_tr = ppsd.decode_ppsd(full, cfg, prompt, 64, "greedy", ppsd.RngStream(0))
+    shards = [StageShard(config, cfg, r, world, seed=5, deep_scale=0.3, deep_from=1) for r in range(world)]
+    assert any(s.engine.schedule("greedy") == "folded" for s in shards)
+    xbufs = [p2p_prepare(s)[1] for s in shards]
+    for s in shards:
+        p2p_connect(s, local_xbufs=xbufs)
+    results = [None] * world
+
+    def run(i):
+        results[i] = decode_ppsd_p2p(shards[i], prompt, 64)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in threads), "p2p decode hung"
+    for toks, m, tr in results:
+        assert toks == want_t
+        assert m == want_m
+        assert tr.to_csv() == want_tr.to_csv()
+    assert any(s.last["schedule"] == "folded" and 0 < s.last["deep_batches"] < s.last["ticks"] for s in shards)

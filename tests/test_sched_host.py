@@ -55,3 +55,29 @@ def test_sched_folded_matches_reference(case):
     if case["max_tokens"] > 0:
         # one deep pass verifies several chains: fewer passes than verdicts
         assert sum(batches) >= m[0] and len(batches) <= m[0]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("case", load_golden("toylm_decode.json"), ids=lambda c: c["name"])
+def test_sched_rank_folded_matches_reference(case, world):
+    """Multi-rank with the per-rank fold (sched.h: sched_rfold_plan): every
+    rank whose deferred stages span >= 2 stages batches them; tokens, metrics
+    and trace stay the reference's, every input exists when a rank uses it,
+    and folding ranks stream their deferred weights fewer times than ticks."""
+    from hostsched import run_toy_multirank_folded
+
+    lm = sp.ToyLMPort(case["n_layers"], case["vocab"], case["lm_seed"], case["beta"])
+    cfg = case["cfg"]
+    S = -(-cfg["n_layers"] // cfg["exit_depth"])
+    if world > S:
+        pytest.skip("more ranks than stages")
+    toks, m, rows, batches = run_toy_multirank_folded(
+        lm, cfg["n_layers"], cfg["exit_depth"], case["prompt"], case["max_tokens"], world,
+        exit_stage=cfg.get("exit_stage", 0) or 0, comm_latency=cfg.get("comm_latency", 0),
+        force_reject=case.get("force_reject", False))
+    assert toks == case["tokens"]
+    assert list(m[:4]) == case["metrics"][:4]
+    assert m[4:] == tuple(case["metrics"][4:])
+    assert sp.trace_csv(rows) == case["trace_csv"]
+    for r, b in batches.items():
+        assert len(b) <= m[1], (r, len(b), m[1])
