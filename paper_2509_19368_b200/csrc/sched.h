@@ -322,10 +322,13 @@ PPSD_HD void sched_rfold_plan(Sched* s) {
 // ticks later.
 PPSD_HD int sched_rfold_first(const SchedCfg* c, int lo) { return lo > c->k ? lo : c->k + 1; }
 PPSD_HD int sched_rfold_width(const SchedCfg* c, int lo, int hi) { return (hi - lo) * c->per + 1; }
-// A rank folds when its deferred part spans >= 2 stages (a single deferred
-// stage is due the tick its chain arrives: every batch would hold one chain).
+// A rank folds when it has deferred stages and more than one stage: a batch
+// then holds up to (hi - lo) * per + 1 chains. (A one-stage rank past the
+// exit is due the tick its chain arrives; a rank owning the exit stage
+// batches even a single deferred stage, because the chain arriving this tick
+// runs its eager stages before the batch.)
 PPSD_HD bool sched_rfold_useful(const SchedCfg* c, int lo, int hi) {
-  return hi - sched_rfold_first(c, lo) + 1 >= 2;
+  return sched_rfold_first(c, lo) <= hi && hi > lo;
 }
 
 // Host-side configuration helper (also used by the CPU test build).

@@ -148,8 +148,8 @@ def test_loopback_edge_lengths(n_prompt, max_tokens, mode):
                                                 (3, 1, 0, False), (2, 1, 1, False), (2, 1, 0, True)])
 def test_loopback_rank_fold(world, k, comm, force):
     """Per-rank fold (sched.h: sched_rfold_plan): 8 one-layer stages, so every
-    rank with >= 2 deferred stages batches them (eager exit stages when it owns
-    k, draft kept per chain when k > lo). Greedy tokens, metrics and trace equal
+    rank with deferred stages and more than one stage batches them (eager exit
+    stages when it owns k, draft kept per chain when k > lo). Greedy tokens, metrics and trace equal
     the single-device decode, and equal the same ranks run pipelined."""
     from paper_2509_19368_b200.distributed import StageShard
 

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=256)
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--xfer-us", type=float, default=13.3)  # tools/p2p_overhead.py: loopback peer-store exchange, 7B
+    ap.add_argument("--schedule", choices=["auto", "pipelined"], default="auto")  # auto: ranks fold where they can
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -44,6 +45,8 @@ def main():
     cfg = ppsd.PipelineConfig(config.n_layers, args.exit)
     shards = [StageShard(config, cfg, r, args.world, seed=0, deep_scale=args.deep_scale, deep_from=args.exit)
               for r in range(args.world)]
+    for s in shards:
+        s.engine.set_schedule(args.schedule)
     ps = ppsd.RngStream(ppsd.derive_seed(0, "run")).split("prompt")
     prompt = [ps.randbelow(config.vocab) for _ in range(args.prompt)]
 
@@ -102,6 +105,8 @@ def main():
         "alpha": m.alpha_all_measured, "ticks": m.ticks, "committed": m.committed_tokens,
         "rank_compute_ms_mean": [round(float(x), 4) for x in used[:, :, 0].mean(axis=0)],
         "rank_sched_ms_mean": [round(float(x), 4) for x in used[:, :, 1].mean(axis=0)],
+        "rank_schedule": [s.last["schedule"] for s in shards],
+        "rank_deep_batches": [s.last["deep_batches"] for s in shards],
         "xfer_us_assumed": args.xfer_us,
         "projected_tick_ms": round(float(tick_ms.mean()), 4),
         "projected_tokens_per_s": round(m.committed_tokens / total_s, 2),
