@@ -12,7 +12,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libppsd.so")
+# PPSD_LIB: another build of the library (A/B experiments, e.g. tools/quick_decode.py)
+LIB_PATH = os.environ.get("PPSD_LIB") or os.path.join(HERE, "libppsd.so")
 
 PPSD_OK, PPSD_EINVAL, PPSD_ECUDA, PPSD_ESTATE, PPSD_EUNSUPPORTED = 0, -1, -2, -3, -4
 MODEL_BERNOULLI, MODEL_TOYLM, MODEL_TRANSFORMER = 0, 1, 2

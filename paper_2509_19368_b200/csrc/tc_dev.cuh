@@ -118,6 +118,15 @@ constexpr int kTcTraceN = 128;
 static __device__ unsigned long long g_tc_trace[8][kTcTraceN];
 static __device__ int g_tc_trace_on;
 static __device__ int g_tc_exp;  // experiments: 1 = no weight copies, 2 = no operand stores
+// the experiment switch: a global load on the producer's critical path, so
+// only trace builds read it
+__device__ __forceinline__ int tc_exp() {
+#ifdef PPSD_TC_TRACE
+  return g_tc_exp;
+#else
+  return 0;
+#endif
+}
 static __device__ unsigned long long g_tc_cta[160][4];  // per CTA: start, first copy, last MMA issued, exit
 // compiled in only with -DPPSD_TC_TRACE (the probes perturb the pipeline)
 __device__ __forceinline__ void tc_cta_mark(int k) {

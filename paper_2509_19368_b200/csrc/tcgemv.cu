@@ -65,6 +65,23 @@
 
 namespace ppsd {
 
+// this launch's matrix for global layer li (the LM head: head_w)
+template <int EPI>
+__device__ __forceinline__ const unsigned char* tc_weights_t(const GemvArgs& a, int li) {
+  if constexpr (EPI == kMatHead || EPI == kMatHeadV) {
+    return reinterpret_cast<const unsigned char*>(a.head_w);
+  } else {
+    if (a.wstride && li < a.wn)  // layers at a fixed stride: no dependent load
+      return reinterpret_cast<const unsigned char*>(a.wbase) + (size_t)li * a.wstride;
+    if (a.wp[0] && li < kTcMaxWp)  // launch parameter
+      return reinterpret_cast<const unsigned char*>(a.wp[li]);
+    const LayerW& L = a.layers[li];
+    return reinterpret_cast<const unsigned char*>(EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o
+                                                  : EPI == kMatGU ? L.gu : L.down);
+  }
+}
+#define tc_weights(a, li) tc_weights_t<EPI>(a, li)
+
 template <int EPI, int CS>
 __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a) {
   constexpr bool kHead2 = EPI == kMatHead;   // PPSD tick: exit (v=0) + final (v=1) head
@@ -134,7 +151,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
     if (wsp) {  // the first tile of this CTA's share of one problem
       const int sc = CS > 1 ? (int)cluster_rank() : 0;
       const int snc = (int)gridDim.x / CS, sb = (int)blockIdx.x / CS;
-      const int su0 = (int)((long long)G * sb / snc), su1 = (int)((long long)G * (sb + 1) / snc);
+      const int su0 = (int)((unsigned)(G * sb) / (unsigned)snc), su1 = (int)((unsigned)(G * (sb + 1)) / (unsigned)snc);
       const int sjlo = NJ * sc / CS, sjhi = NJ * (sc + 1) / CS;
       TcTiles tl;
       tl.init(su0, su1, G, TG);
@@ -177,8 +194,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
       atomicOr(a.err, kGemvErrHint);
       np = 0;
     }
-    s_np = np;
     s_spec = np == 1 ? spec_n : 0;
+    s_np = np;
     if (np == 0 && spec_n > 0) {  // nothing to do: let the copies land before exit
       for (int i = 0; i < spec_n; ++i) {
         mbar_arrive(&full[i]);
@@ -216,34 +233,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
   // the ranks' row sums in rank order
   const int crank = CS > 1 ? (int)cluster_rank() : 0;
   const int ncl = (int)gridDim.x / CS, b = (int)blockIdx.x / CS;  // clusters, this cluster
-  const int u0 = (int)((long long)U * b / ncl), u1 = (int)((long long)U * (b + 1) / ncl);
+  // (32-bit: U * ncl < 2^31 for every plan; a 64-bit division is a slow subroutine)
+  const int u0 = (int)((unsigned)(U * b) / (unsigned)ncl), u1 = (int)((unsigned)(U * (b + 1)) / (unsigned)ncl);
   const int ncta = U < ncl ? U : ncl;  // clusters with work (heads: argmax tickets)
   const int jlo = NJ * crank / CS, jhi = NJ * (crank + 1) / CS;
 
   if (u0 < u1) {
     if (warp == 0) {  // ---------------- bulk-copy producer ----------------
       if (lane == 0) {
+        tc_trace(7, 5);
         const uint64_t pol = policy_evict_first();
+        tc_trace(7, 6);
         TcTiles tl;
         tl.init(u0, u1, G, TG);
         int tp, g0, tg, n = 0;
         bool triggered = false;
         while (tl.next(tp, g0, tg)) {
-          const unsigned char* w;
-          if (kHead) {
-            w = reinterpret_cast<const unsigned char*>(a.head_w);
-          } else {
-            const int li = s_li[tp];
-            if (a.wstride && li < a.wn) {  // layers at a fixed stride: no dependent load
-              w = reinterpret_cast<const unsigned char*>(a.wbase) + (size_t)li * a.wstride;
-            } else if (a.wp[0] && li < kTcMaxWp) {  // launch parameter
-              w = reinterpret_cast<const unsigned char*>(a.wp[li]);
-            } else {
-              const LayerW& L = a.layers[li];
-              w = reinterpret_cast<const unsigned char*>(EPI == kMatQKV ? L.qkv : EPI == kMatO ? L.o
-                                                         : EPI == kMatGU ? L.gu : L.down);
-            }
-          }
+          if (n == 0) tc_trace(7, 7);
+          const unsigned char* w = tc_weights(a, kHead ? 0 : s_li[tp]);
           const uint32_t tb = (uint32_t)tg * JSB;
           tc_trace(7, 4);
           for (int j = jlo; j < jhi; j += NB, ++n) {
@@ -251,13 +258,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
             const int st = n % NS;
             if (n >= s_spec) {  // (stages below s_spec were issued before the descriptor was read)
               if (n >= NS) mbar_wait(&empty[st], ((n / NS) & 1) ^ 1);
-              if (g_tc_exp & 1) {
+              if (tc_exp() & 1) {
                 mbar_arrive(&full[st]);
               } else {
                 mbar_expect_tx(&full[st], (uint32_t)nbj * tb);
-                for (int jj = 0; jj < nbj; ++jj)
+                if (n == 0) tc_trace(7, 8);
+                for (int jj = 0; jj < nbj; ++jj) {
                   bulk_g2s(smem + (size_t)st * w_stage + (size_t)jj * tb,
                            w + ((size_t)(j + jj) * G + g0) * JSB, tb, &full[st], pol);
+                  if (n == 0 && jj == 0) tc_trace(7, 9);
+                }
               }
             }
             // the ring is full: only now wait for the predecessor (and let the
@@ -285,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
             const int xG = X.R >> 3, xncl = (int)gridDim.x / X.cs;
             if ((int)blockIdx.x < xncl * X.cs) {
               const int xb = (int)blockIdx.x / X.cs, xr = (int)blockIdx.x % X.cs;
-              const int xu0 = (int)((long long)xG * xb / xncl), xu1 = (int)((long long)xG * (xb + 1) / xncl);
+              const int xu0 = (int)((unsigned)(xG * xb) / (unsigned)xncl), xu1 = (int)((unsigned)(xG * (xb + 1)) / (unsigned)xncl);
               const int xjlo = X.nj * xr / X.cs, xjhi = X.nj * (xr + 1) / X.cs;
               const uint32_t xJSB = (uint32_t)X.js << 10;
               TcTiles xt;
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
           const uint32_t ba = ring_b + (uint32_t)st * b_stage;
           const int per_v = nbj * JS * 8;  // 16-byte K chunks of one vector in this stage
           const int items = nvp * per_v;
-          for (int i0 = 0; i0 < ((g_tc_exp & 2) ? 0 : items); i0 += 4 * tstride) {
+          for (int i0 = 0; i0 < ((tc_exp() & 2) ? 0 : items); i0 += 4 * tstride) {
             float xv[4][8];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {  // all loads of up to 4 items first

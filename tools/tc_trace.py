@@ -36,6 +36,8 @@ for n in range(128):
     print(f"stage {n:3d}: {rel(t[0, n]):7.2f} {rel(t[1, n]):7.2f} {rel(t[2, n]):7.2f} {rel(t[3, n]):7.2f}")
 print("startup: work read %.2f, barriers %.2f, syncthreads %.2f, cluster %.2f, weight ptr %.2f" %
       tuple(rel(t[7, i]) for i in range(5)))
+print("producer: entry %.2f, policy %.2f, first tile %.2f, expect_tx %.2f, first copy issued %.2f" %
+      tuple(rel(t[7, i]) for i in range(5, 10)))
 for i in range(4):
     if t[4, i] > 0:
         print(f"tile {i}: epilogue saw acc_full at {rel(t[4, i]):7.2f}")
