@@ -28,8 +28,9 @@ __device__ __forceinline__ uint64_t* xbuf_flags(float* xbuf, int world, int box_
   return reinterpret_cast<uint64_t*>(xbuf + (size_t)2 * world * box_words);
 }
 
-// store this rank's box (already built in c.outbox) into every rank's buffer
-// and release the flags; returns the exchange number. Block-wide.
+// store this rank's box (already built in c.outbox) into the ranks' buffers
+// (activation to the next rank only) and release the flags; returns the
+// exchange number. Block-wide.
 __device__ inline uint64_t p2p_publish(const TickCtx& c) {
   __shared__ uint64_t s_e;
   if (threadIdx.x == 0) {
@@ -40,9 +41,16 @@ __device__ inline uint64_t p2p_publish(const TickCtx& c) {
   __syncthreads();
   const uint64_t e = s_e;
   const size_t slot = ((e & 1) * c.world + c.rank) * (size_t)c.box_words;
+  // point to point: the activation [kBoxHeader, kBoxHeader + d) goes only to
+  // the rank that runs the next stage (rank + 1, contiguous split); the
+  // header (draft / final tokens) and, sampling, the owners' logits go to
+  // every rank (the replicated scheduler reads them)
+  const int act_end = kBoxHeader + c.d;
   for (int r = 0; r < c.world; ++r) {
     float* dst = c.peer_xbuf[r] + slot;
-    for (int i = threadIdx.x; i < c.box_used; i += blockDim.x) dst[i] = c.outbox[i];
+    const bool act = r == c.rank + 1;
+    for (int i = threadIdx.x; i < c.box_used; i += blockDim.x)
+      if (act || i < kBoxHeader || i >= act_end) dst[i] = c.outbox[i];
   }
   __threadfence_system();  // every storing thread orders its box stores before the flag
   __syncthreads();
