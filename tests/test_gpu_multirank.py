@@ -145,7 +145,8 @@ def test_loopback_edge_lengths(n_prompt, max_tokens, mode):
 
 
 @pytest.mark.parametrize("world,k,comm,force", [(2, 1, 0, False), (2, 2, 0, False), (4, 1, 0, False),
-                                                (3, 1, 0, False), (2, 1, 1, False), (2, 1, 0, True)])
+                                                (3, 1, 0, False), (2, 1, 1, False), (2, 1, 0, True),
+                                                (4, 3, 0, False), (2, 6, 0, False), (4, 3, 1, True)])
 def test_loopback_rank_fold(world, k, comm, force):
     """Per-rank fold (sched.h: sched_rfold_plan): 8 one-layer stages, so every
     rank with deferred stages and more than one stage batches them (eager exit
@@ -174,5 +175,8 @@ def test_loopback_rank_fold(world, k, comm, force):
             assert ran == ("folded" if f and sched == "auto" else "pipelined"), (sched, ran)
             if ran == "folded":
                 # its deferred layers stream once per batch, not once per tick
+                # (with k > 1 chains launch k ticks apart: batches of one)
                 assert 0 < s.last["deep_batches"] < s.last["ticks"], s.last
-                assert s.last["deep_vectors"] > s.last["deep_batches"], s.last
+                assert s.last["deep_vectors"] >= s.last["deep_batches"], s.last
+                if k == 1:
+                    assert s.last["deep_vectors"] > s.last["deep_batches"], s.last
