@@ -69,6 +69,8 @@ struct ppsd_engine {
   ppsd_pipeline_desc pd{};
   int device = 0, num_sms = 148;
   int attn_per_sm = 8;  // attention CTAs per SM: one resident wave
+  bool attn_cl = false;  // one-vector launches use the cluster attention kernel (attn.cu)
+  bool tick_g1 = false;  // capturing tick launches whose `work` has one group (folded shallow, rank-fold eager)
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
   bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
   int hint_first = -1;       // capturing single-problem launches whose first layer is known (speculative start)
@@ -313,10 +315,18 @@ static AttnArgs make_attn_args(ppsd_engine* e, Work* w, int layer_i) {
   return a;
 }
 
-static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i) {
+static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i, bool batched = true) {
   // PPSD_PROFILE_SKIP_ATTN=1: timing experiments only (wrong results)
   static const bool skip = getenv("PPSD_PROFILE_SKIP_ATTN") && atoi(getenv("PPSD_PROFILE_SKIP_ATTN")) != 0;
   if (skip) return cudaSuccess;
+  if (!batched && e->attn_cl) {
+    // one vector per group: a cluster per (group, kv head) row. Rows: the
+    // tick descriptor's groups (one per local stage) unless the capture has
+    // one group (AR, EESD draft, exit-head layer, folded shallow, rank-fold eager)
+    const bool one = w != e->d_work || e->tick_g1;
+    const int rows = (one ? 1 : e->hi - e->lo + 1) * e->dm.KV;
+    return attn_cl_launch(make_attn_args(e, w, layer_i), rows, e->st);
+  }
   return attn_launch(make_attn_args(e, w, layer_i), attn_grid(e), e->st);
 }
 
@@ -382,7 +392,7 @@ static int enqueue_layers(ppsd_engine* e, Work* w, int n_slots, bool batched) {
   int n = 0;
   for (int i = 0; i < n_slots; ++i) {
     if (enqueue_gemv(e, w, i, kMatQKV, batched) != cudaSuccess) return -1;
-    if (enqueue_attn(e, w, i) != cudaSuccess) return -1;
+    if (enqueue_attn(e, w, i, batched) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatO, batched) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatGU, batched) != cudaSuccess) return -1;
     if (enqueue_gemv(e, w, i, kMatDown, batched) != cudaSuccess) return -1;
@@ -450,7 +460,9 @@ static int build_fold_graph(ppsd_engine* e) {
   n_outer = 1;
   if (ok) {
     e->hint_first = e->lo == 1 ? 0 : -1;  // sched.cu: the launched chain's layers [0, shallow)
+    e->tick_g1 = true;
     const int m = enqueue_layers(e, e->d_work, shallow, false);
+    e->tick_g1 = false;
     e->hint_first = -1;
     need(m >= 0, "shallow layers");
     n_outer += m;
@@ -786,6 +798,9 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       aa.dm = d;
       CU(attn_set_attrs(aa));
       e->attn_per_sm = std::max(1, std::min(8, attn_ctas_per_sm()));
+      // cluster attention for the one-vector launches (PPSD_ATTN_CL=0: off)
+      const char* cv = getenv("PPSD_ATTN_CL");
+      e->attn_cl = !(cv && cv[0] == '0') && attn_cl_setup(aa);
     }
     e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
     e->final_norm = w->final_norm;
@@ -1717,8 +1732,9 @@ extern "C" int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32
                                double* bytes_per_launch) {
   // Decode attention of one group of n_vec vectors whose longest context is
   // ctx positions (positions ctx-n_vec .. ctx-1), walking the local layers
-  // so consecutive launches read different KV; the plan the decode graphs use
-  // for that vector count (cluster kernel, or split-K with PPSD_ATTN=splitk).
+  // so consecutive launches read different KV; the kernel the decode graphs
+  // use for that vector count (one vector: the cluster kernel unless
+  // PPSD_ATTN_CL=0; more: split-K).
   if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "probe needs a transformer engine");
   if (n_vec < 1 || n_vec > kMaxVec || ctx < n_vec || ctx > e->md.max_ctx || reps < 1)
     return fail(PPSD_EINVAL, "bad attention probe arguments");
@@ -1732,7 +1748,7 @@ extern "C" int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32
   w.nl[0] = e->n_local_layers;
   w.head_slot[0] = w.head_slot[1] = -1;
   CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
-  auto launch = [&](int i) { return enqueue_attn(e, e->d_work_ar, i % e->n_local_layers); };
+  auto launch = [&](int i) { return enqueue_attn(e, e->d_work_ar, i % e->n_local_layers, n_vec > 1); };
   for (int i = 0; i < 3; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev0, e->st));
   for (int i = 0; i < reps; ++i) CU(launch(i));
@@ -1816,7 +1832,9 @@ static int build_rf_graph(ppsd_engine* e, bool with_sched, cudaGraphExec_t* out,
                           (unsigned long long)h) == cudaSuccess, "IF setter");
   n_outer = 1;
   if (ok && eager > 0) {  // the chain reaching stage lo: stages lo..k, exit head
+    e->tick_g1 = true;
     const int m = enqueue_layers(e, e->d_work, eager, false);
+    e->tick_g1 = false;
     need(m >= 0, "eager layers");
     n_outer += m;
     need(ok && enqueue_gemv(e, e->d_work, 0, kMatHead) == cudaSuccess, "exit head");

@@ -220,6 +220,8 @@ cudaError_t tc_pass_launch(const TcPassArgs& a, int cs, int hd, int qpk, int kv_
 cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 int attn_ctas_per_sm();
+bool attn_cl_setup(const AttnArgs& a);
+cudaError_t attn_cl_launch(const AttnArgs& a, int rows, cudaStream_t st);
 int attn_trace_enable(int on);
 int attn_trace_read(unsigned long long* out);
 
