@@ -783,7 +783,15 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
         // (<= 5 vectors x 3 parts) for the decode tick, the folded deep batch
         // and the PPSD head; 3 (<= 16 vectors) for prefill chunks and EESD
         const int nblk = b ? 3 : 1;
-        if (tc_pick(p.K, p.R, nblk, e->num_sms, &p.tc, m) != 0)
+        // PPSD_TC_GRID=<qkv>,<o>,<gu>,<down>: SMs a matrix's plan spreads over
+        // (experiments; 0 or absent: all)
+        int sms = e->num_sms;
+        if (const char* gv = getenv("PPSD_TC_GRID")) {
+          int f[4] = {0, 0, 0, 0};
+          sscanf(gv, "%d,%d,%d,%d", &f[0], &f[1], &f[2], &f[3]);
+          if (m < 4 && f[m] > 0 && f[m] <= e->num_sms) sms = f[m];
+        }
+        if (tc_pick(p.K, p.R, nblk, sms, &p.tc, m) != 0)
           return fail(PPSD_EUNSUPPORTED, "no tensor-core GEMV plan for matrix " + std::to_string(m) + " [" +
                                              std::to_string(p.R) + " x " + std::to_string(p.K) + "]");
         CU(tc_set_attrs(m, p.tc.cs, p.tc.smem));
