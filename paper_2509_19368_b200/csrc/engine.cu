@@ -269,9 +269,10 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
     a.bar_off = t.bar_off;
     // L2 prefetch of the next GEMV of the layer: QKV -> O the whole O slice
     // (attention leaves HBM idle in between), O -> GU, GU -> down, down -> next
-    // QKV the first 96 KB per CTA (the next launch's first stages; measured
-    // 443.3 -> 446.9 tok/s, 192 KB: 444.1). PPSD_TC_NEXT=<KB> overrides.
-    static const int nx_kb = getenv("PPSD_TC_NEXT") ? atoi(getenv("PPSD_TC_NEXT")) : 96;
+    // QKV the first 48 KB per CTA (the next launch's first stages; re-measured
+    // after the cluster attention: 0 KB 459.4, 32 466.1, 48 466.4, 64 464.1,
+    // 96 461.3 tok/s). PPSD_TC_NEXT=<KB> overrides.
+    static const int nx_kb = getenv("PPSD_TC_NEXT") ? atoi(getenv("PPSD_TC_NEXT")) : 48;
     if (mat <= kMatDown && (mat == kMatQKV || nx_kb > 0)) {
       const int nm = (mat + 1) % 4;
       const GemvPlan& np_ = &p == &e->gpb[mat] ? e->gpb[nm] : e->gp[nm];
