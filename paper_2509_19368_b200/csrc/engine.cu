@@ -71,6 +71,7 @@ struct ppsd_engine {
   int attn_per_sm = 8;  // attention CTAs per SM: one resident wave
   bool attn_cl = false;  // one-vector launches use the cluster attention kernel (attn.cu)
   bool tick_g1 = false;  // capturing tick launches whose `work` has one group (folded shallow, rank-fold eager)
+  bool comb_capture = false;  // capturing the folded body's final heads with the combined exit head
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
   bool small_batch = false;  // capturing batched launches of <= 5 vectors (tick plans serve them)
   int hint_first = -1;       // capturing single-problem launches whose first layer is known (speculative start)
@@ -239,6 +240,7 @@ static GemvArgs make_gemv_args(ppsd_engine* e, Work* w, int layer_i, int mat, co
   a.head_cnt = e->d_head_cnt;
   a.err = e->d_kerr;
   a.hint_li = -1;
+  a.comb_exit = mat == kMatHeadV && e->comb_capture ? 1 : 0;
   {
     const TcPlan& t = p.tc;
     // speculative start: measured slower on the 7B bench (427 vs 437 tok/s,
@@ -439,6 +441,15 @@ static int capture(ppsd_engine* e, F body, cudaGraphExec_t* out, int64_t* nlaunc
 // handle resets to 0 at every launch (cudaGraphCondAssignDefault).
 static int build_fold_graph(ppsd_engine* e) {
   const int shallow = e->cfg.shallow_layers, deep = e->md.n_layers - shallow;
+  // exit head inside the deep batch's final-head launch (one LM-head pass
+  // instead of two in batch ticks): the batch plus the exit vector must fit
+  // the tick plan (<= 5 vectors), no exit-head layer; PPSD_FOLD_COMB=0: off
+  const char* cbv = getenv("PPSD_FOLD_COMB");
+  const char* fcv = getenv("PPSD_FOLD_COND");
+  const bool comb = !(cbv && cbv[0] == '0') && !e->hl && sched_fold_width(&e->cfg) + 1 <= 5 &&
+                    !(fcv && atoi(fcv) == 0) && e->nbuf - 1 >= sched_fold_width(&e->cfg);
+  e->h_ctx.fold_comb = comb ? 1 : 0;
+  e->h_ctx.comb_row = e->nbuf - 1;
   cudaStream_t main_st = e->st, body_st = nullptr;
   CU(cudaStreamCreateWithFlags(&body_st, cudaStreamNonBlocking));
   cudaGraph_t g = nullptr;
@@ -520,13 +531,21 @@ static int build_fold_graph(ppsd_engine* e) {
     if (ok) {
       e->st = body_st;
       e->small_batch = sched_fold_width(&e->cfg) <= 5;
+      if (comb) {  // the launched chain's exit state, before the deep layers advance its row
+        need(launch_pdl(fold_exit_copy_kernel, dim3(1), dim3(256), 0, body_st, (const TickCtx*)e->d_ctx) ==
+                 cudaSuccess, "exit copy");
+        n_body += 1;
+      }
       e->hint_first = shallow;  // sched.cu: the batch's layers [shallow, N)
       const int m = enqueue_layers(e, e->d_work_deep, deep, true);
       e->hint_first = -1;
       need(m >= 0, "deep layers");
-      n_body = m;
-      need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
+      n_body += m;
+      e->comb_capture = comb;
+      need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true,
+                              comb ? e->d_logits : e->d_logits + e->dm.V) == cudaSuccess,
            "final heads");
+      e->comb_capture = false;
       n_body += 1;
       e->small_batch = false;
       e->st = main_st;

@@ -63,6 +63,11 @@ struct TickCtx {
   // greedy): deferred batches in activation rows rf_row0 .. rf_row0 + width
   int32_t rfold;
   int32_t rf_row0;
+  // folded tick with a deep batch: the launched chain's exit head runs as
+  // vector 0 of the batch's final-head launch, on a copy of its exit state in
+  // row comb_row (the batch advances the chain's own row past the exit)
+  int32_t fold_comb;
+  int32_t comb_row;
   // transformer-layer exit head (ppsd_model_desc.exit_head_layer): the draft
   // is the norm head on that decoder layer's output for a COPY of the
   // exit-layer state (rows head_row..), so the chain's own state continues
@@ -110,6 +115,7 @@ __global__ void toy_tick_kernel(const TickCtx* ctxp);
 __global__ void pack_outbox_kernel(const TickCtx* ctxp, int prefill);
 __global__ void rf_cond_kernel(const TickCtx* ctxp, unsigned long long handle);
 __global__ void rf_gather_kernel(const TickCtx* ctxp);
+__global__ void fold_exit_copy_kernel(const TickCtx* ctxp);
 __global__ void mr_prefill_begin_kernel(const TickCtx* ctxp, ArCtl* ctl);
 __global__ void p2p_wait_kernel(const TickCtx* ctxp);
 __global__ void toy_ar_kernel(const TickCtx* ctxp, int n_prompt, int max_tokens);

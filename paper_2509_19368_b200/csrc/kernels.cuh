@@ -34,6 +34,9 @@ struct Work {
   // the final token vec_out[final_idx] of work_deep (-1: none); rf_src: the
   // batch chains' activation slots, gathered into the batch rows
   int32_t out_row, out_slot, out_pos, exit_tok, final_idx;
+  // folded tick with a deep batch: the exit head of this row runs as vector 0
+  // of the final-head launch (GemvArgs.comb_exit), -1: none
+  int32_t head_exit;
   int32_t rf_src[kMaxVec];
 };
 
@@ -110,6 +113,9 @@ struct GemvArgs {
   // >= 0: the launch has at most one problem, layer hint_li (any value for
   // the heads): the producer starts streaming before reading the descriptor
   int32_t hint_li;
+  // kMatHeadV: vector 0 is the exit head of work->head_exit when >= 0 (logits
+  // rows: exit 0, batch 1..)
+  int32_t comb_exit;
   // L2 prefetch of the NEXT GEMV's weights (this CTA's slice of its first
   // nx_bytes), issued after this launch's last copy: it lands while the
   // launch drains, the next launch starts and (QKV -> O) attention runs

@@ -219,8 +219,10 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       final_tok = reinterpret_cast<const int32_t*>(inbox + (size_t)c.owner_S * c.box_words)[1];
     }
     if (c.fold && !begin) {
-      // the chain launched last tick ran its shallow stages and exit head eagerly
-      if (s.launched) s.ch_draft[s.work[1]] = c.work->head_out[0];
+      // the chain launched last tick ran its shallow stages and exit head
+      // eagerly (with a deep batch and fold_comb: inside the final-head launch)
+      if (s.launched)
+        s.ch_draft[s.work[1]] = c.fold_comb && s.fold_nb > 0 ? c.work_deep->head_out[0] : c.work->head_out[0];
       if (c.greedy) exit_tok = s.exit_slot >= 0 ? s.ch_draft[s.exit_slot] : -1;
       final_tok = (c.greedy && s.final_slot >= 0)
                       ? c.work_deep->vec_out[s.ch_pos[s.final_slot] - s.fold_base] : final_tok;
@@ -252,6 +254,12 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
       wd->nl[0] = s.c.n_layers - s.c.shallow_layers;
       wd->nv[0] = s.fold_nb > 0 ? s.fold_nb : 1;
       wd->head_slot[0] = wd->head_slot[1] = -1;
+      wd->head_exit = -1;
+      if (c.fold_comb && s.fold_nb > 0 && row >= 0) {  // exit head inside the final-head launch
+        wd->head_exit = c.comb_row;
+        wd->src_slot = row;
+        w->head_slot[0] = -1;
+      }
       if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
       if (c.hl) {  // exit-head layer on a copy of the launched chain's exit state
         plan_head_layer(c, c.work_head, row, w->pos[0], 1);
@@ -367,6 +375,19 @@ __global__ void __launch_bounds__(256) pack_outbox_kernel(const TickCtx* ctxp, i
     __syncthreads();
     p2p_publish(c);
   }
+}
+
+// Folded tick with a deep batch (fold_comb): the launched chain's exit state
+// into row comb_row before the deep layers advance its own row.
+__global__ void __launch_bounds__(256) fold_exit_copy_kernel(const TickCtx* ctxp) {
+  pdl_wait();
+  pdl_trigger();
+  const TickCtx c = *ctxp;
+  const Work* wd = c.work_deep;
+  if (wd->head_exit < 0) return;
+  const float4* src = reinterpret_cast<const float4*>(c.x + (size_t)wd->src_slot * c.d);
+  float4* dst = reinterpret_cast<float4*>(c.x + (size_t)wd->head_exit * c.d);
+  for (int i = threadIdx.x; i < c.d / 4; i += blockDim.x) dst[i] = src[i];
 }
 
 // Rank fold: open the deferred batch's graph IF node for this launch (the

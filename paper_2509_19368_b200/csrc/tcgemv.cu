@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
   // the first ring stages before reading the work descriptor (and, for the
   // first kernel of a tick, before the scheduler kernel has finished).
   __shared__ int s_spec;  // stages issued speculatively
+  __shared__ int s_ex;    // kHeadV: 1 if vector 0 is a combined exit head
   int spec_n = 0;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -175,7 +176,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
     if (kHead2) {
       if (work->head_slot[0] >= 0 || work->head_slot[1] >= 0) { s_pg[0] = -1; s_nv[0] = 2; np = 1; }
     } else if (kHeadV) {
-      if (work->G >= 1 && work->slot[0] >= 0 && work->nv[0] > 0) { s_pg[0] = 0; s_nv[0] = work->nv[0]; np = 1; }
+      // a.comb_exit: vector 0 is the exit head of row work->head_exit (if >= 0),
+      // the batch follows (the folded tick's exit + final heads in one pass)
+      const int ex = a.comb_exit && work->head_exit >= 0 ? 1 : 0;
+      s_ex = ex;
+      if (work->G >= 1 && work->slot[0] >= 0 && work->nv[0] > 0) { s_pg[0] = 0; s_nv[0] = work->nv[0] + ex; np = 1; }
     } else {
       for (int g = 0; g < work->G && np < kTcMaxProb; ++g)
         if (work->slot[g] >= 0 && a.layer_i < work->nl[g] && work->nv[g] > 0) {
@@ -400,8 +405,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
                 if (sl >= 0) sp = a.x + (size_t)sl * a.dm.d;
                 np_ = v == 0 ? a.head_norm0 : a.head_norm1;
               } else if (kHeadV) {
-                sp = a.x + (size_t)(work->slot[0] + v) * a.dm.d;
-                np_ = a.head_norm1;
+                const int ex = s_ex;
+                sp = a.x + (size_t)(ex && v == 0 ? work->head_exit : work->slot[0] + v - ex) * a.dm.d;
+                np_ = ex && v == 0 ? a.head_norm0 : a.head_norm1;
               } else {
                 const int sl = work->slot[g] + v;
                 const LayerW& L = a.layers[work->first[g] + a.layer_i];
@@ -530,7 +536,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
               const int sl = work->head_slot[v];
               if (sl >= 0) sp = a.x + (size_t)sl * a.dm.d;
             } else if (kHeadV) {
-              sp = a.x + (size_t)(work->slot[0] + v) * a.dm.d;
+              const int ex = s_ex;
+              sp = a.x + (size_t)(ex && v == 0 ? work->head_exit : work->slot[0] + v - ex) * a.dm.d;
             } else {
               sp = a.x + (size_t)(work->slot[s_pg[tp]] + v) * a.dm.d;
             }
@@ -696,13 +703,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
               if (y > bestv[v]) { bestv[v] = y; besti[v] = rr; }  // rows ascend per thread
             }
           }
-        } else {  // kHeadV
+        } else {  // kHeadV (comb_exit: logits row 0 = the exit vector, rows 1.. the batch)
           if (valid) {
+            const int lrow0 = a.comb_exit ? 1 - s_ex : 0;
 #pragma unroll
             for (int v = 0; v < kMaxVec; ++v) {
               if (v >= nvp) break;
               const float y = yv(v);
-              a.logits[(size_t)v * a.dm.V + rr] = y;
+              a.logits[(size_t)(v + lrow0) * a.dm.V + rr] = y;
               if (y > hbv[v]) { hbv[v] = y; hbi[v] = rr; }
             }
           }
@@ -768,7 +776,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
               for (int w = 1; w < 4; ++w)
                 if (tc_better(s_bv[w][v], s_bi[w][v], bv, bi)) { bv = s_bv[w][v]; bi = s_bi[w][v]; }
               if (kHead2) wk->head_out[v] = work->head_slot[v] >= 0 ? bi : -1;
-              else wk->vec_out[v] = bi;
+              else if (s_ex && v == 0) wk->head_out[0] = bi;
+              else wk->vec_out[v - s_ex] = bi;
             }
             *ticket = 0;
           }
