@@ -169,12 +169,13 @@ def algorithmic_bytes(trace, config, cfg, n_prompt, last=None):
         deep = config.n_layers - shallow
         launches = [r.position for r in trace if r.kind == ACTIVATION and r.stage == 1]
         nb, nvec, psum = last["deep_batches"], last["deep_vectors"], last["deep_pos_sum"]
+        comb = last.get("comb_heads", 0)  # exit heads that rode in a batch's final-head pass
         weights = len(launches) * shallow * layer_b + nb * deep * layer_b
-        heads = (len(launches) + nb) * config.head_bytes()
+        heads = (len(launches) + nb - comb) * config.head_bytes()
         kv = (shallow * kv_b * sum(n_prompt + p - 1 for p in launches)
               + deep * kv_b * (psum + nvec * (n_prompt - 1)))
         return weights + heads + kv, dict(schedule="folded", shallow_passes=len(launches),
-                                          deep_batches=nb, deep_vectors=nvec, weight_bytes=weights,
+                                          deep_batches=nb, deep_vectors=nvec, comb_heads=comb, weight_bytes=weights,
                                           head_bytes=heads, kv_bytes=kv)
     head_ticks = set()
     weights = kv = 0

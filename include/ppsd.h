@@ -142,6 +142,9 @@ typedef struct {
    * chains they carried and the sum of those chains' positions */
   int32_t schedule;
   int64_t deep_batches, deep_vectors, deep_pos_sum;
+  /* folded: deep batches whose final-head pass also ran the launched chain's
+   * exit head (one LM-head pass instead of two) */
+  int64_t comb_heads;
 } ppsd_metrics;
 
 typedef struct {

@@ -68,7 +68,7 @@ class Metrics(C.Structure):
         ("alpha_all_measured", C.c_double), ("throughput", C.c_double),
         ("speedup_vs_ar", C.c_double), ("decode_ms", C.c_double), ("prefill_ms", C.c_double),
         ("gpu_launches", C.c_int64), ("schedule", C.c_int32), ("deep_batches", C.c_int64),
-        ("deep_vectors", C.c_int64), ("deep_pos_sum", C.c_int64),
+        ("deep_vectors", C.c_int64), ("deep_pos_sum", C.c_int64), ("comb_heads", C.c_int64),
     ]
 
 

@@ -1222,6 +1222,7 @@ static int run_machine(ppsd_engine* e, int model, int n_prompt, int stop, int fo
   out->deep_batches = s.fold_batches;
   out->deep_vectors = s.fold_vectors;
   out->deep_pos_sum = s.fold_pos_sum;
+  out->comb_heads = s.fold_comb;
   if (trace) {
     const int64_t nrows = std::min<int64_t>(s.trace_n, trace_cap);
     if (nrows > 0)

@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(256) sched_tick_kernel(const TickCtx* ctxp, in
         wd->head_exit = c.comb_row;
         wd->src_slot = row;
         w->head_slot[0] = -1;
+        s.fold_comb += 1;
       }
       if (s.fold_nb > 0 && c.has_cond) cudaGraphSetConditional(c.cond, 1u);
       if (c.hl) {  // exit-head layer on a copy of the launched chain's exit state

@@ -77,6 +77,7 @@ struct Sched {
   int32_t rf_arrived;    // rank fold: highest position that reached stage rf_lo
   int64_t fold_vectors;  // chains that went through a deep batch
   int64_t fold_pos_sum;  // sum of their positions (attention context accounting)
+  int64_t fold_comb;     // deep batches that also ran the launched chain's exit head (TickCtx.fold_comb)
   int32_t ch_draft[kMaxSlots];  // eager exit-head argmax per chain
 };
 
@@ -100,6 +101,7 @@ PPSD_HD void sched_reset(Sched* s) {
   s->fold_batches = 0;
   s->rf_arrived = 0;
   s->fold_vectors = s->fold_pos_sum = 0;
+  s->fold_comb = 0;
 }
 
 PPSD_HD void sched_trace(Sched* s, TraceRow* tr, int64_t cap, int st, int kind, int pos, int tok,

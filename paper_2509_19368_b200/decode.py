@@ -88,7 +88,7 @@ class Engine:
                          ticks=m.ticks, committed=m.committed_tokens,
                          schedule={v: k for k, v in _lib.SCHEDULES.items()}.get(m.schedule, "pipelined"),
                          deep_batches=m.deep_batches, deep_vectors=m.deep_vectors,
-                         deep_pos_sum=m.deep_pos_sum)
+                         deep_pos_sum=m.deep_pos_sum, comb_heads=m.comb_heads)
         metrics = make_metrics(m.committed_tokens, m.ticks, m.accepts, m.rejects,
                                m.accepts + m.rejects, self.cfg.ar_ticks_per_token)
         trace = EventTrace.from_array(rows[:n_rows]) if rows is not None else EventTrace()

@@ -29,7 +29,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.ModelDesc) == 4 * 12 + 8 + 8 + 8
     assert C.sizeof(_lib.PipelineDesc) == 8 * 4
     assert C.sizeof(_lib.TraceRowC) == 24
-    assert C.sizeof(_lib.Metrics) == 4 * 8 + 8 + 5 * 8 + 8 + 8 + 3 * 8
+    assert C.sizeof(_lib.Metrics) == 4 * 8 + 8 + 5 * 8 + 8 + 8 + 4 * 8
     # ...and what gcc computes from include/ppsd.h itself
     import subprocess
     import tempfile
@@ -39,9 +39,10 @@ def test_struct_layouts_match_header():
 #include <stddef.h>
 #include "ppsd.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ppsd_model_desc), sizeof(ppsd_pipeline_desc),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ppsd_model_desc), sizeof(ppsd_pipeline_desc),
          sizeof(ppsd_metrics), sizeof(ppsd_trace_row), offsetof(ppsd_metrics, schedule),
-         offsetof(ppsd_metrics, deep_pos_sum), sizeof(ppsd_weights), offsetof(ppsd_weights, exit_layer));
+         offsetof(ppsd_metrics, deep_pos_sum), sizeof(ppsd_weights), offsetof(ppsd_weights, exit_layer),
+         offsetof(ppsd_metrics, comb_heads));
   return 0;
 }
 '''
@@ -53,7 +54,7 @@ int main(void) {
         got = [int(x) for x in subprocess.check_output([exe], text=True).split()]
     assert got == [C.sizeof(_lib.ModelDesc), C.sizeof(_lib.PipelineDesc), C.sizeof(_lib.Metrics),
                    C.sizeof(_lib.TraceRowC), _lib.Metrics.schedule.offset, _lib.Metrics.deep_pos_sum.offset,
-                   C.sizeof(_lib.Weights), _lib.Weights.exit_layer.offset]
+                   C.sizeof(_lib.Weights), _lib.Weights.exit_layer.offset, _lib.Metrics.comb_heads.offset]
 
 
 def test_sm100a_cubin_embedded():
