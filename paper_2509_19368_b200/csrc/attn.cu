@@ -33,12 +33,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
 // the arrival ticket; the leader merges in page order (attn_merge), so
 // results are bit-identical to attn_kernel, which the batched launches keep.
 // Rows past kMergePages pages keep global partials (the same merge reads them).
-constexpr int kClWorkers = 1;
+#ifndef PPSD_CL_WORKERS
+#define PPSD_CL_WORKERS 1
+#endif
+constexpr int kClWorkers = PPSD_CL_WORKERS;  // page workers per CTA (A/B builds: -DPPSD_CL_WORKERS=2)
 template <int HD, typename KVT, int QPK, int CS>
 __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ AttnScratch<HD, QPK> SW[kClWorkers];
-  __shared__ int s_row[5];  // g, kv head, pos, local layer, slot (g < 0: idle row)
+  __shared__ int s_row[6];  // g, kv head, pos, local layer, slot, group's first pos (g < 0: idle row)
   using Gm = AttnGeom<HD, KVT, QPK>;
   constexpr int BLK = Gm::BLK, PS = HD + 2, NW = kClWorkers;
   const int tid = threadIdx.x, wk = tid >> 7, wt = tid & 127;
@@ -58,6 +61,7 @@ __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const
     S0.st_pos[tid] = w->pos[tid];
     S0.st_first[tid] = w->first[tid];
     S0.st_nl[tid] = w->nl[tid];
+    S0.st_nv[tid] = w->nv[tid];
   } else if (tid >= 64 && tid < 64 + NW * kPg) {
     const int ww = (tid - 64) / kPg, k = (tid - 64) % kPg;
     const int c = rank + CS * ww + NW * CS * k;
@@ -70,24 +74,30 @@ __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const
   }
   __syncthreads();
   if (tid == 0) {
-    // row -> (group, kv head): active one-vector groups in order, KV rows each
-    int r = row, g = -1;
+    // row -> (group, vector, kv head): active groups in order, KV rows per
+    // vector (one vector per group unless a.multi: batched launches, vector
+    // v of group g at slot[g] + v, position pos[g] + v)
+    int r = row, g = -1, v = 0;
     const int G = min(S0.st_G, kStageG);
     for (int gg = 0; gg < G; ++gg) {
       if (S0.st_slot[gg] < 0 || a.layer_i >= S0.st_nl[gg]) continue;
-      if (r < KVh) {
+      const int nvg = a.multi ? S0.st_nv[gg] : 1;
+      if (r < nvg * KVh) {
         g = gg;
+        v = r / KVh;
+        r -= v * KVh;
         break;
       }
-      r -= KVh;
+      r -= nvg * KVh;
     }
     s_row[0] = g;
     s_row[1] = r;
     if (g >= 0) {
-      s_row[2] = S0.st_pos[g];
+      s_row[2] = S0.st_pos[g] + v;
       const int gl = S0.st_first[g] + a.layer_i;
       s_row[3] = gl == a.hl_global ? a.hl_local : gl - a.first_local;
-      s_row[4] = S0.st_slot[g];
+      s_row[4] = S0.st_slot[g] + v;
+      s_row[5] = S0.st_pos[g];
     }
   }
   __syncthreads();
@@ -111,8 +121,10 @@ __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const
   };
   auto page_rows = [&](int c) { return min(kPage, pos + 1 - c * kPage); };
   auto sync = [wk] { named_bar_sync(1 + wk, kAttnThreads); };
-  // rows of the first page below this layer's written position: before the wait
-  const int early = c0 < nch ? max(0, min(page_rows(c0), pos - c0 * kPage)) : 0;
+  // rows of the first page below the group's first position written by this
+  // layer (earlier vectors of the group write theirs too): before the wait
+  const int pos0 = g >= 0 ? s_row[5] : 0;
+  const int early = c0 < nch ? max(0, min(page_rows(c0), pos0 - c0 * kPage)) : 0;
   if (early > 0 && wt == 0) issue_rows(c0, 0, early, false);
   pdl_wait();
   pdl_trigger();
@@ -163,6 +175,7 @@ __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const
 namespace {
 int g_attn_occ = 0;
 int g_attn_cl_cs = 0;  // cluster size of the cluster kernel (0: unavailable)
+bool g_attn_cl4 = false;  // clusters of 4 available (batched launches)
 
 template <int HD, typename KVT, int QPK, int CS>
 size_t cl_smem() {
@@ -211,10 +224,16 @@ cudaError_t launch_cl(const AttnArgs& a, int rows, cudaStream_t st, bool attrs) 
 }
 
 // the cluster kernel for (hd, dtype, qpk): hd 128 and qpk <= 2 (the leader's
-// page slots must fit shared memory); cluster size 16, else 8
+// page slots must fit shared memory); cluster size 16, else 8. Launches may
+// ask for clusters of 4 (cs = 4: batched launches, more rows per wave).
 template <typename KVT, int QPK>
-cudaError_t cl_qpk(const AttnArgs& a, int rows, cudaStream_t st, bool attrs) {
+cudaError_t cl_qpk(const AttnArgs& a, int rows, cudaStream_t st, bool attrs, int cs) {
   if (attrs) {
+    g_attn_cl_cs = 0;
+    // clusters of 4 for the batched launches (attributes only)
+    launch_cl<128, KVT, QPK, 4>(a, rows, st, true);
+    cudaGetLastError();
+    g_attn_cl4 = g_attn_cl_cs == 4;
     g_attn_cl_cs = 0;
     // clusters of 8 (portable; 16 measured ~3 us slower per launch), PPSD_ATTN_CL=16 to compare
     const char* v = getenv("PPSD_ATTN_CL");
@@ -225,14 +244,17 @@ cudaError_t cl_qpk(const AttnArgs& a, int rows, cudaStream_t st, bool attrs) {
     cudaGetLastError();
     return g_attn_cl_cs ? cudaSuccess : (e == cudaSuccess ? cudaErrorNotSupported : e);
   }
+  if (cs == 4) return g_attn_cl4 ? launch_cl<128, KVT, QPK, 4>(a, rows, st, false) : cudaErrorNotSupported;
   return g_attn_cl_cs == 16 ? launch_cl<128, KVT, QPK, 16>(a, rows, st, false)
                             : launch_cl<128, KVT, QPK, 8>(a, rows, st, false);
 }
-cudaError_t cl_dispatch(const AttnArgs& a, int rows, cudaStream_t st, bool attrs) {
+cudaError_t cl_dispatch(const AttnArgs& a, int rows, cudaStream_t st, bool attrs, int cs = 0) {
   if (a.dm.hd != 128) return cudaErrorNotSupported;
   const int qpk = a.dm.H / a.dm.KV;
-  if (qpk == 1) return a.dm.kv_bf16 ? cl_qpk<__nv_bfloat16, 1>(a, rows, st, attrs) : cl_qpk<float, 1>(a, rows, st, attrs);
-  if (qpk == 2) return a.dm.kv_bf16 ? cl_qpk<__nv_bfloat16, 2>(a, rows, st, attrs) : cl_qpk<float, 2>(a, rows, st, attrs);
+  if (qpk == 1)
+    return a.dm.kv_bf16 ? cl_qpk<__nv_bfloat16, 1>(a, rows, st, attrs, cs) : cl_qpk<float, 1>(a, rows, st, attrs, cs);
+  if (qpk == 2)
+    return a.dm.kv_bf16 ? cl_qpk<__nv_bfloat16, 2>(a, rows, st, attrs, cs) : cl_qpk<float, 2>(a, rows, st, attrs, cs);
   return cudaErrorNotSupported;
 }  // attn_set_attrs: resident CTAs per SM of the configured instantiation
 
@@ -294,6 +316,9 @@ cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st) { return d
 // cluster kernel: attrs once per engine (returns false when unavailable for
 // the shape), launch with `rows` >= the active one-vector (group, kv head) rows
 bool attn_cl_setup(const AttnArgs& a) { return cl_dispatch(a, 0, 0, true) == cudaSuccess; }
-cudaError_t attn_cl_launch(const AttnArgs& a, int rows, cudaStream_t st) { return cl_dispatch(a, rows, st, false); }
+bool attn_cl4_ok() { return g_attn_cl4; }
+cudaError_t attn_cl_launch(const AttnArgs& a, int rows, cudaStream_t st, int cs) {
+  return cl_dispatch(a, rows, st, false, cs);
+}
 
 }  // namespace ppsd

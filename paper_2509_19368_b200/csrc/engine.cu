@@ -70,6 +70,9 @@ struct ppsd_engine {
   int device = 0, num_sms = 148;
   int attn_per_sm = 8;  // attention CTAs per SM: one resident wave
   bool attn_cl = false;  // one-vector launches use the cluster attention kernel (attn.cu)
+  bool attn_clb = false;  // batched launches may use it too (clusters of 4, attn_clb_vec rows)
+  int attn_clb_cs = 4;    // their cluster size (4, or 8 = the one-vector kernel's)
+  int attn_clb_vec = 0;   // vectors the batched capture in progress can hold (0: split-K kernel)
   bool tick_g1 = false;  // capturing tick launches whose `work` has one group (folded shallow, rank-fold eager)
   bool comb_capture = false;  // capturing the folded body's final heads with the combined exit head
   WStride wstride[4];  // per matrix kind (kMatQKV..kMatDown), when the layers are strided
@@ -330,6 +333,13 @@ static cudaError_t enqueue_attn(ppsd_engine* e, Work* w, int layer_i, bool batch
     const int rows = (one ? 1 : e->hi - e->lo + 1) * e->dm.KV;
     return attn_cl_launch(make_attn_args(e, w, layer_i), rows, e->st);
   }
+  if (batched && e->attn_clb && e->attn_clb_vec > 0) {
+    // a bounded batch (folded deep batch): a cluster of 4 per (vector, kv
+    // head) row; the same page partials and ordered merge as attn_kernel
+    AttnArgs a = make_attn_args(e, w, layer_i);
+    a.multi = 1;
+    return attn_cl_launch(a, e->attn_clb_vec * e->dm.KV, e->st, e->attn_clb_cs);
+  }
   return attn_launch(make_attn_args(e, w, layer_i), attn_grid(e), e->st);
 }
 
@@ -494,7 +504,9 @@ static int build_fold_graph(ppsd_engine* e) {
   const char* cv = getenv("PPSD_FOLD_COND");
   if (ok && cv && atoi(cv) == 0) {
     e->hint_first = shallow;
+    e->attn_clb_vec = sched_fold_width(&e->cfg);
     const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+    e->attn_clb_vec = 0;
     e->hint_first = -1;
     need(m >= 0, "deep layers");
     need(ok && enqueue_gemv(e, e->d_work_deep, 0, kMatHeadV, true, e->d_logits + e->dm.V) == cudaSuccess,
@@ -537,7 +549,9 @@ static int build_fold_graph(ppsd_engine* e) {
         n_body += 1;
       }
       e->hint_first = shallow;  // sched.cu: the batch's layers [shallow, N)
+      e->attn_clb_vec = sched_fold_width(&e->cfg);
       const int m = enqueue_layers(e, e->d_work_deep, deep, true);
+      e->attn_clb_vec = 0;
       e->hint_first = -1;
       need(m >= 0, "deep layers");
       n_body += m;
@@ -829,6 +843,10 @@ static int create_impl(const ppsd_model_desc* md, const ppsd_weights* w, const p
       // cluster attention for the one-vector launches (PPSD_ATTN_CL=0: off)
       const char* cv = getenv("PPSD_ATTN_CL");
       e->attn_cl = !(cv && cv[0] == '0') && attn_cl_setup(aa);
+      // batched cluster launches (PPSD_ATTN_CLB=0: split-K kernel for every batch)
+      const char* cb = getenv("PPSD_ATTN_CLB");
+      e->attn_clb = e->attn_cl && !(cb && cb[0] == '0') && attn_cl4_ok();
+      e->attn_clb_cs = cb && atoi(cb) == 8 ? 8 : 4;
     }
     e->lm_head = reinterpret_cast<const __nv_bfloat16*>(w->lm_head);
     e->final_norm = w->final_norm;
@@ -1763,7 +1781,8 @@ extern "C" int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32
   // ctx positions (positions ctx-n_vec .. ctx-1), walking the local layers
   // so consecutive launches read different KV; the kernel the decode graphs
   // use for that vector count (one vector: the cluster kernel unless
-  // PPSD_ATTN_CL=0; more: split-K).
+  // PPSD_ATTN_CL=0; more: the folded deep batch's clusters of 4 unless
+  // PPSD_ATTN_CLB=0, then split-K).
   if (!e || e->md.kind != PPSD_MODEL_TRANSFORMER) return fail(PPSD_EINVAL, "probe needs a transformer engine");
   if (n_vec < 1 || n_vec > kMaxVec || ctx < n_vec || ctx > e->md.max_ctx || reps < 1)
     return fail(PPSD_EINVAL, "bad attention probe arguments");
@@ -1778,6 +1797,11 @@ extern "C" int ppsd_probe_attn(ppsd_engine* e, int32_t n_vec, int32_t ctx, int32
   w.head_slot[0] = w.head_slot[1] = -1;
   CU(cudaMemcpyAsync(e->d_work_ar, &w, sizeof(Work), cudaMemcpyHostToDevice, e->st));
   auto launch = [&](int i) { return enqueue_attn(e, e->d_work_ar, i % e->n_local_layers, n_vec > 1); };
+  e->attn_clb_vec = n_vec > 1 ? n_vec : 0;  // a bounded batch (folded deep batch kernel)
+  struct Reset {
+    ppsd_engine* e;
+    ~Reset() { e->attn_clb_vec = 0; }
+  } reset{e};
   for (int i = 0; i < 3; ++i) CU(launch(i));
   CU(cudaEventRecord(e->ev0, e->st));
   for (int i = 0; i < reps; ++i) CU(launch(i));
@@ -1892,7 +1916,9 @@ static int build_rf_graph(ppsd_engine* e, bool with_sched, cudaGraphExec_t* out,
            "gather");
       n_body = 1;
       e->small_batch = sched_rfold_width(&C, lo, hi) <= 5;
+      e->attn_clb_vec = sched_rfold_width(&C, lo, hi);
       const int m = enqueue_layers(e, e->d_work_deep, deferred, true);
+      e->attn_clb_vec = 0;
       need(m >= 0, "deferred layers");
       n_body += m;
       if (ok && hi == e->S) {

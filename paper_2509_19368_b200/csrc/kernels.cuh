@@ -147,6 +147,7 @@ struct AttnArgs {
   int32_t first_local;  // global index of the first local layer
   int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
   int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
+  int32_t multi;        // cluster kernel: rows enumerate every vector of a group (batched launches)
 };
 
 // one matrix of the persistent layer pass (tcpass.cu); the arithmetic plan
@@ -227,7 +228,8 @@ cudaError_t attn_launch(const AttnArgs& a, int grid, cudaStream_t st);
 cudaError_t attn_set_attrs(const AttnArgs& a);
 int attn_ctas_per_sm();
 bool attn_cl_setup(const AttnArgs& a);
-cudaError_t attn_cl_launch(const AttnArgs& a, int rows, cudaStream_t st);
+bool attn_cl4_ok();  // clusters of 4 (batched launches) after attn_cl_setup
+cudaError_t attn_cl_launch(const AttnArgs& a, int rows, cudaStream_t st, int cs = 0);
 int attn_trace_enable(int on);
 int attn_trace_read(unsigned long long* out);
 

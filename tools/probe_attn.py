@@ -30,7 +30,8 @@ def main():
     lm = ppsd.TransformerLM(config, seed=0)
     cfg = ppsd.PipelineConfig(args.layers, 1)
     rows = []
-    for mode in ("splitk",):
+    mode = os.environ.get("PPSD_ATTN_CLB", "cluster")
+    if True:
         eng = Engine(lm.model_desc(), lm.weights_struct(), cfg, device=lm.device.index)
         for nv in (1, 4, 11):
             for ctx in (128, 384, 640, 1000):
