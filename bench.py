@@ -78,6 +78,13 @@ def workload(args, world):
     return name, exit_depth
 
 
+def tokens_digest(toks):
+    """Order-sensitive 40-bit digest of a token list (N=1 and N>1 lines are comparable)."""
+    import numpy as np
+
+    return int(np.bitwise_xor.reduce(np.asarray(toks, dtype=np.int64) * 1000003 + np.arange(len(toks)))) & (2**40 - 1)
+
+
 def workload_label(name, cfg, world):
     where = "1 GPU" if world == 1 else f"{world} GPUs"
     return (f"Llama-2-{name.upper()}-shaped greedy PPSD decode, E={cfg.exit_depth} ({cfg.n_stages} stages on "
@@ -373,6 +380,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "alpha_measured": alpha, "ticks": m0.ticks, "accepts": m0.accepts, "rejects": m0.rejects,
+        "tokens_digest": tokens_digest(toks0),
         "tick_speedup": m0.speedup_vs_ar,
         "ppsd_speedup_eq7": ppsd.ppsd_speedup(alpha, config.n_layers, exit_depth) if alpha is not None else None,
         "ar_tokens_per_s": round(ar_tps, 3), "speedup_vs_our_ar": round(value / ar_tps, 4),
@@ -493,7 +501,7 @@ def run_pipelined(args, world, rank, local):
     hbm, _ = peaks()
 
     # every rank must hold the same tokens (replicated scheduler)
-    digest = int(np.bitwise_xor.reduce(np.asarray(toks, dtype=np.int64) * 1000003 + np.arange(len(toks)))) & (2**40 - 1)
+    digest = tokens_digest(toks)
     agg = torch.tensor([sum(dec), sum(e2e), digest, -digest, -rank_gbs, rank_gbs], dtype=torch.float64,
                        device=reduce_dev)
     dist.all_reduce(agg, op=dist.ReduceOp.MAX)
@@ -522,7 +530,8 @@ def run_pipelined(args, world, rank, local):
         "rank_roofline": {"min_gbs": round(rmin, 1), "max_gbs": round(rmax, 1), "peak": hbm,
                           "min_frac": round(rmin / hbm, 4), "min_frac_nominal_8tbs": round(rmin / NOMINAL_HBM_GBS, 4)},
         "clocks": clk.summary(), "gpu_launches": launches,
-        "alpha_measured": m.alpha_all_measured, "ticks": m.ticks, "tick_speedup": m.speedup_vs_ar,
+        "alpha_measured": m.alpha_all_measured, "ticks": m.ticks, "accepts": m.accepts, "rejects": m.rejects,
+        "tokens_digest": digest, "tick_speedup": m.speedup_vs_ar,
         "ppsd_speedup_eq7": ppsd.ppsd_speedup(m.alpha_all_measured, config.n_layers, exit_depth)
         if m.alpha_all_measured is not None else None,
     }

@@ -24,15 +24,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(const AttnArgs a) {
                            });
 }
 
-// Cluster decode attention for one-vector groups (decode ticks, AR): one
-// thread-block cluster of CS CTAs per (group, kv head) row, two 128-thread
-// page workers per CTA; worker w of rank r takes the row's pages
-// r + CS w, r + CS (w + 2), ... with the split-K kernel's page arithmetic
-// (attn_page) and stores each page partial into the cluster leader's shared
-// memory over DSMEM. One cluster barrier replaces the global partials and
-// the arrival ticket; the leader merges in page order (attn_merge), so
-// results are bit-identical to attn_kernel, which the batched launches keep.
-// Rows past kMergePages pages keep global partials (the same merge reads them).
+// Cluster decode attention: one thread-block cluster of CS CTAs per
+// (group, kv head) row for one-vector groups (decode ticks, AR; CS 8), or
+// per (group, vector, kv head) row for a bounded batch (a.multi: folded deep
+// batches; CS 4). kClWorkers 128-thread page workers per CTA (1; 2 measured
+// slower); worker w of rank r takes the row's pages r + CS w, r + CS (w + NW),
+// ... with the split-K kernel's page arithmetic (attn_page) and stores each
+// page partial into the cluster leader's shared memory over DSMEM. One
+// cluster barrier replaces the global partials and the arrival ticket; the
+// leader merges in page order (attn_merge), so results are bit-identical to
+// attn_kernel (prefill chunks and EESD verify keep it). Rows past
+// kMergePages pages keep global partials (the same merge reads them).
 #ifndef PPSD_CL_WORKERS
 #define PPSD_CL_WORKERS 1
 #endif
