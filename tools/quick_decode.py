@@ -38,6 +38,7 @@ def main():
         toks, m, _ = eng.decode(prompt, bench.NEW_TOKENS, trace=False)
         ms.append(eng.last["decode_ms"])
     out["ppsd_tok_s"] = round(bench.NEW_TOKENS / statistics.median(ms[1:]) * 1e3, 2)
+    out["prefill_ms"] = eng.last.get("prefill_ms")
     out["schedule"] = eng.last["schedule"]
     out["alpha"] = m.alpha_all_measured
     ms = []
