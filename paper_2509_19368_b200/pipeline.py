@@ -102,16 +102,29 @@ class TraceRow(NamedTuple):
 class EventTrace:
     """Chronological message log; rows come back from the device trace ring."""
 
-    __slots__ = ("_rows",)
+    __slots__ = ("_list", "_arr")
 
     def __init__(self, rows=None):
-        self._rows: list[TraceRow] = list(rows or [])
+        self._list: list[TraceRow] = list(rows or [])
+        self._arr = None
 
     @classmethod
     def from_array(cls, arr) -> "EventTrace":
-        """arr: int32 [n, 6] of (tick, stage, kind, position, token|-1, verdict)."""
-        return cls(TraceRow(int(t), int(s), KINDS[k], int(p), None if tok < 0 else int(tok), VERDICTS[v])
-                   for t, s, k, p, tok, v in arr.tolist())
+        """arr: int32 [n, 6] of (tick, stage, kind, position, token|-1, verdict),
+        the rows the device trace ring returned; the TraceRow objects are built
+        on first use (a 512-token decode returns ~4k rows: ~4 ms of Python the
+        decode call itself does not need to pay)."""
+        tr = cls()
+        tr._arr = arr
+        return tr
+
+    @property
+    def _rows(self) -> list[TraceRow]:
+        if self._arr is not None:
+            self._list = [TraceRow(int(t), int(s), KINDS[k], int(p), None if tok < 0 else int(tok), VERDICTS[v])
+                          for t, s, k, p, tok, v in self._arr.tolist()] + self._list
+            self._arr = None
+        return self._list
 
     def add(self, tick: int, stage: int, message: StageMessage, verdict: str = "") -> None:
         self._rows.append(TraceRow(tick, stage, message.kind, message.position, message.token, verdict))
@@ -126,7 +139,7 @@ class EventTrace:
     __iter__ = rows
 
     def __len__(self) -> int:
-        return len(self._rows)
+        return len(self._list) + (0 if self._arr is None else len(self._arr))
 
     def write_csv(self, dest) -> None:
         if hasattr(dest, "write"):
