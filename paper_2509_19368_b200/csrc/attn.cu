@@ -92,6 +92,12 @@ __global__ void __launch_bounds__(kAttnThreads* kClWorkers) attn_cl_kernel(const
       }
       r -= nvg * KVh;
     }
+    if (blockIdx.x == 0 && a.err) {  // every active (vector, kv head) row must have a cluster
+      int need = 0;
+      for (int gg = 0; gg < G; ++gg)
+        if (S0.st_slot[gg] >= 0 && a.layer_i < S0.st_nl[gg]) need += (a.multi ? S0.st_nv[gg] : 1) * KVh;
+      if (need * CS > (int)gridDim.x || S0.st_G > kStageG) atomicOr(a.err, kAttnErrRows);
+    }
     s_row[0] = g;
     s_row[1] = r;
     if (g >= 0) {

@@ -318,6 +318,7 @@ static AttnArgs make_attn_args(ppsd_engine* e, Work* w, int layer_i) {
   a.first_local = e->first_local_layer;
   a.hl_global = e->hl ? e->md.n_layers : -1;
   a.hl_local = e->n_local_layers;
+  a.err = e->d_kerr;
   return a;
 }
 
@@ -1089,7 +1090,8 @@ static int check_kerr(ppsd_engine* e) {
   CU(cudaMemcpy(&v, e->d_kerr, sizeof(v), cudaMemcpyDeviceToHost));
   if (v == 0) return PPSD_OK;
   CU(cudaMemset(e->d_kerr, 0, sizeof(v)));
-  return fail(PPSD_ESTATE, v & kGemvErrHint ? "GEMV speculative start: hint did not match the work (results discarded)"
+  return fail(PPSD_ESTATE, v & kAttnErrRows ? "cluster attention: more active vectors than launched rows (results discarded)"
+                          : v & kGemvErrHint ? "GEMV speculative start: hint did not match the work (results discarded)"
                           : "layer pass: a grid barrier timed out (results discarded)");
 }
 

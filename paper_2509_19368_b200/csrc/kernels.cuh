@@ -129,6 +129,7 @@ struct TcPlan {
 };
 constexpr int kGemvErrPassTimeout = 2;  // a layer-pass grid barrier waited > 5 s
 constexpr int kGemvErrHint = 4;         // a speculative-start hint did not match the work descriptor
+constexpr int kAttnErrRows = 8;         // a cluster attention launch had fewer rows than active vectors
 
 struct AttnArgs {
   const Work* work;
@@ -148,6 +149,7 @@ struct AttnArgs {
   int32_t hl_global;    // exit-head layer: its global index (-1: none) ...
   int32_t hl_local;     // ... and its slot in the KV pool (after the local layers)
   int32_t multi;        // cluster kernel: rows enumerate every vector of a group (batched launches)
+  int32_t* err;         // sticky device error word (kAttnErrRows), checked by the host
 };
 
 // one matrix of the persistent layer pass (tcpass.cu); the arithmetic plan
