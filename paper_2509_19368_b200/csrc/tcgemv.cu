@@ -571,6 +571,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
               if (v < nvp) xres[v] = __ldcg(xr + (size_t)v * a.dm.d);
           }
         }
+        // QKV: each vector's RoPE factors and KV page for this thread's row,
+        // fetched while the MMAs run (the epilogue is then compute + stores,
+        // not a chain of dependent loads per vector)
+        float rcs[kMaxVec], rsn[kMaxVec];
+        int rpg[kMaxVec];
+        if constexpr (EPI == kMatQKV) {
+          const int hd = a.dm.hd, H = a.dm.H, KVh = a.dm.KV;
+          const int rr0 = g0 * 8 + rl0, head = rr0 / hd, wi = rr0 - head * hd;
+          const bool live = rl0 < tg * 8 && !(lane & 1);
+          const int pos0 = work->pos[s_pg[tp]];
+#pragma unroll
+          for (int v = 0; v < kMaxVec; ++v) {
+            rcs[v] = 0.f;
+            rsn[v] = 0.f;
+            rpg[v] = 0;
+            if (v < nvp && live) {
+              const int pos = pos0 + v;
+              if (head < H + KVh) {
+                rcs[v] = a.rope_cos[(size_t)pos * (hd >> 1) + (wi >> 1)];
+                rsn[v] = a.rope_sin[(size_t)pos * (hd >> 1) + (wi >> 1)];
+              }
+              if (head >= H) rpg[v] = a.page_table[pos / kPage];
+            }
+          }
+        }
         mbar_wait(&acc_full[buf], (ti >> 1) & 1);
         tc_fence_after_sync();
         if (et == 0) tc_trace(4, ti);
@@ -636,26 +661,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
         };
         if constexpr (EPI == kMatQKV || EPI == kMatGU) {
           const int g = s_pg[tp];
+          const int slot0 = work->slot[g], pos0 = work->pos[g];
+          void* kv_cache = nullptr;  // this row's K or V cache (QKV rows past the q heads)
+          if (EPI == kMatQKV && valid && !(lane & 1) && rr / a.dm.hd >= a.dm.H) {
+            const LayerW& L = a.layers[work->first[g] + a.layer_i];
+            kv_cache = rr / a.dm.hd < a.dm.H + a.dm.KV ? L.kc : L.vc;
+          }
 #pragma unroll
           for (int v = 0; v < kMaxVec; ++v) {
             if (v >= nvp) break;
             const float y = yv(v);
             const float yp = __shfl_xor_sync(0xffffffffu, y, 1);
             if (!valid || (lane & 1)) continue;
-            const int slot = work->slot[g] + v, pos = work->pos[g] + v;
+            const int slot = slot0 + v, pos = pos0 + v;
             if (EPI == kMatGU) {
               a.h[(size_t)slot * a.dm.ffn + (rr >> 1)] = y / (1.0f + expf(-y)) * yp;
             } else {
               const int H = a.dm.H, KVh = a.dm.KV, hd = a.dm.hd;
-              const LayerW& L = a.layers[work->first[g] + a.layer_i];
               const int head = rr / hd, wi = rr - head * hd;
               float o0 = y, o1 = yp;
               void* cache = nullptr;
               int kvh = 0;
               if (head < H + KVh) {
-                const int half = hd >> 1;
-                const float cs = a.rope_cos[(size_t)pos * half + (wi >> 1)];
-                const float sn = a.rope_sin[(size_t)pos * half + (wi >> 1)];
+                const float cs = rcs[v];
+                const float sn = rsn[v];
                 o0 = y * cs - yp * sn;
                 o1 = yp * cs + y * sn;
                 if (head < H) {
@@ -663,15 +692,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tcgemv_kernel(const GemvArgs a)
                   q[0] = o0;
                   q[1] = o1;
                 } else {
-                  cache = L.kc;
+                  cache = kv_cache;
                   kvh = head - H;
                 }
               } else {
-                cache = L.vc;
+                cache = kv_cache;
                 kvh = head - H - KVh;
               }
               if (cache) {
-                const int page = a.page_table[pos / kPage];
+                const int page = rpg[v];
                 const size_t off = (((size_t)page * KVh + kvh) * kPage + (pos % kPage)) * hd + wi;
                 if (a.dm.kv_bf16) {
                   *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(cache) + off) =
